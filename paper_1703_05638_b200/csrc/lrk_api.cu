@@ -1,0 +1,813 @@
+// lrk_api.cu — C ABI (include/lrk.h): context, workspace, and the host-side
+// orchestration of each reference entry point over the device kernels.
+// No host<->device synchronisation happens inside an apply except where the
+// ABI returns host values (ranks, traces, inner products) at the very end.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/lrk.h"
+#include "lrk_device.cuh"
+#include "lrk_kernels.h"
+#include "lrk_misc.h"
+
+using namespace lrk;
+
+namespace {
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+}  // namespace
+
+struct lrk_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  int64_t launches = 0;
+  // operator
+  bool has_op = false;
+  lrk_operator_desc op{};
+  int64_t n_x = 0;
+  int n = 0;
+  double* dS = nullptr;       // n x n DST-I (symmetric, orthogonal)
+  double* dTheta = nullptr;   // n_x: eigenvalues of S^{-1} M  = 1/(1+tau*lambda)
+  double* dThetaM = nullptr;  // n_x: theta / m_scale (eigenvalues of S^{-1})
+  double* dE0 = nullptr;      // n_t: e_0
+  double* dInvLam = nullptr;  // n_x: 1/lambda (steady Poisson solve)
+  // observation
+  bool has_obs = false;
+  int obs_kind = LRK_OBS_FULL;
+  int n_obs = 0, s1 = 0, s2 = 0;
+  int32_t* dList = nullptr;
+  double *dS1T = nullptr, *dS2 = nullptr, *dS1 = nullptr, *dS2T = nullptr;
+  std::map<std::string, Buf> ws;
+  ~lrk_ctx() {
+    for (auto& kv : ws) cudaFree(kv.second.p);
+    cudaFree(dS); cudaFree(dTheta); cudaFree(dThetaM); cudaFree(dE0); cudaFree(dInvLam);
+    cudaFree(dList); cudaFree(dS1T); cudaFree(dS2); cudaFree(dS1); cudaFree(dS2T);
+  }
+};
+
+namespace {
+
+int fail(lrk_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(c, LRK_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKL()                                                                      \
+  do {                                                                             \
+    ++c->launches;                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(c, LRK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY(expr)                 \
+  do {                            \
+    int st_ = (expr);             \
+    if (st_ != LRK_OK) return st_; \
+  } while (0)
+
+template <typename T>
+T* wsp(lrk_ctx* c, const std::string& name, size_t count, bool zero = false) {
+  Buf& b = c->ws[name];
+  const size_t need = count * sizeof(T) + 256;
+  if (b.bytes < need) {
+    if (b.p) {
+      cudaDeviceSynchronize();
+      cudaFree(b.p);
+      b.p = nullptr;
+      b.bytes = 0;
+    }
+    if (cudaMalloc(&b.p, need) != cudaSuccess) {
+      cudaGetLastError();
+      c->err = "cudaMalloc failed for workspace " + name;
+      return nullptr;
+    }
+    b.bytes = need;
+    cudaMemset(b.p, 0, need);
+  } else if (zero) {
+    cudaMemset(b.p, 0, need);
+  }
+  return static_cast<T*>(b.p);
+}
+
+#define WS(T, var, name, count)                                                      \
+  T* var = wsp<T>(c, name, (size_t)(count));                                         \
+  if (!var) return LRK_ERR_CUDA;
+
+inline int grid1(int64_t n, int per = 256, int cap = 4096) {
+  int64_t g = (n + per - 1) / per;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+int pick_ncta(lrk_ctx* c, int64_t rows) {
+  int64_t k = rows / 384;
+  if (k < 1) k = 1;
+  if (k > c->num_sms) k = c->num_sms;
+  return (int)k;
+}
+
+// --------------------------------------------------------------- GEMMs
+int gemm(lrk_ctx* c, int M, int N, int K, const double* A, int64_t lda, int64_t sA,
+         const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+         double alpha, int batch, const int* batch_dev, cudaStream_t s) {
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K;
+  g.A = A; g.lda = lda; g.sA = sA;
+  g.B = B; g.ldb = ldb; g.sB = sB;
+  g.C = C; g.ldc = ldc; g.sC = sC;
+  g.alpha = alpha; g.beta = 0.0;
+  g.batch = batch; g.batch_dev = batch_dev;
+  g.m_dev = nullptr; g.m_mult = 1;
+  CK(launch_gemm(g, s));
+  ++c->launches;
+  return LRK_OK;
+}
+
+// Y[:, j] = alpha * (S (x) S) X[:, j]: 2-D DST-I of each column.
+int dst2(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int ncols,
+         const int* ncols_dev, double alpha, cudaStream_t s) {
+  if (ncols <= 0) return LRK_OK;
+  const int n = c->n;
+  const int64_t nx = c->n_x;
+  WS(double, T, "dst_T", nx * (int64_t)ncols);
+  // T_j = X_j S      (X_j: n x n row-major view of column j)
+  TRY(gemm(c, n, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
+  // Y_j = alpha S T_j
+  TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s));
+  return LRK_OK;
+}
+
+// Uobs_j = S[i2,:] Xhat_j S[:,i1]   (sensor-subgrid values of a spectral column)
+int subgrid_gather(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int ncols,
+                   const int* ncols_dev, cudaStream_t s) {
+  const int n = c->n, s1 = c->s1, s2 = c->s2;
+  WS(double, T, "sg_T", (int64_t)n * s1 * ncols);
+  TRY(gemm(c, n, s1, n, X, n, ldx, c->dS1T, s1, 0, T, s1, (int64_t)n * s1, 1.0, ncols, ncols_dev, s));
+  TRY(gemm(c, s2, s1, n, c->dS2, n, 0, T, s1, (int64_t)n * s1, Y, s1, ldy, 1.0, ncols, ncols_dev, s));
+  return LRK_OK;
+}
+
+// Zhat_j = S[:,i2] Z_j S[i1,:]   (spectral image of a sensor-subgrid field)
+int subgrid_scatter(lrk_ctx* c, const double* Z, int64_t ldz, double* Y, int64_t ldy, int ncols,
+                    const int* ncols_dev, cudaStream_t s) {
+  const int n = c->n, s1 = c->s1, s2 = c->s2;
+  WS(double, T, "ss_T", (int64_t)s2 * n * ncols);
+  TRY(gemm(c, s2, n, s1, Z, s1, ldz, c->dS1, n, 0, T, n, (int64_t)s2 * n, 1.0, ncols, ncols_dev, s));
+  TRY(gemm(c, n, n, s2, c->dS2T, s2, 0, T, n, (int64_t)s2 * n, Y, n, ldy, 1.0, ncols, ncols_dev, s));
+  return LRK_OK;
+}
+
+// ---------------------------------------------------------------- sweep
+struct SweepOut {
+  double* U = nullptr;  // n_x x ucap (slot 0)
+  double* V = nullptr;  // n_t x ucap
+  double* sigma = nullptr;
+  int* info = nullptr;  // device [rank, which, err, pad]
+  int* trace = nullptr; // device nflush+1
+  int ucap = 0;
+  int nflush = 0;
+  int64_t ldu = 0, ldv = 0;
+};
+
+int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, int rb,
+              const int* rb_dev, const double* W2, int64_t ldw2, int adjoint, int p, double eps0,
+              int r_max, SweepOut& o, cudaStream_t s) {
+  if (p < 1 || p > PMAX)
+    return fail(c, LRK_ERR_UNSUPPORTED, "compress_every must lie in [1, 16] on the device path");
+  const int64_t nx = c->n_x;
+  const int nt = c->op.n_t;
+  const int ucap = (r_max >= 0 && r_max < NMAX) ? std::max(r_max, 1) : NMAX;
+  const int ncta = pick_ncta(c, nx);
+  const int nflush = (nt + p - 1) / p;
+  WS(double, U0, tag + "U0", nx * (int64_t)ucap);
+  WS(double, U1, tag + "U1", nx * (int64_t)ucap);
+  WS(double, V0, tag + "V0", (int64_t)nt * ucap);
+  WS(double, V1, tag + "V1", (int64_t)nt * ucap);
+  WS(double, sig, tag + "sig", NMAX);
+  WS(int, info, tag + "info", 8);
+  WS(int, trace, tag + "trace", nflush + 1);
+  WS(double, ybuf, "sw_ybuf", nx * (int64_t)p);
+  WS(double, qbuf, "sw_qbuf", nx * (int64_t)p);
+  WS(double, yprev, "sw_yprev", nx);
+  const int64_t pst = sweep_part_stride();
+  WS(double, part, "sw_part", 3 * (int64_t)ncta * pst);
+  const int64_t sst = sweep_scratch_stride(ncta);
+  WS(double, scratch, "sw_scratch", (int64_t)ncta * sst);
+  WS(unsigned, bar, "sw_bar", 4);
+  WS(SweepArgs, dargs, tag + "args", 1);
+  SweepArgs a{};
+  a.n_x = nx; a.n_t = nt; a.adjoint = adjoint; a.p = p; a.r_max = r_max; a.eps0 = eps0;
+  a.theta = c->dTheta; a.rowscale = c->dThetaM;
+  a.B = B; a.ldb = ldb; a.rb = rb; a.rb_dev = rb_dev;
+  a.W2 = W2; a.ldw2 = ldw2;
+  a.U0 = U0; a.U1 = U1; a.ldu = nx; a.V0 = V0; a.V1 = V1; a.ldv = nt; a.ucap = ucap;
+  a.sigma = sig; a.info = info; a.trace = trace;
+  a.ybuf = ybuf; a.ldy = nx; a.qbuf = qbuf; a.ldq = nx; a.yprev = yprev;
+  a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
+  a.bar = bar; a.ncta = ncta;
+  CK(cudaMemcpyAsync(dargs, &a, sizeof(a), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
+  CK(launch_sweep(dargs, 1, ncta, s));
+  ++c->launches;
+  o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
+  o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
+  return LRK_OK;
+}
+
+// -------------------------------------------------------------- truncate
+struct TruncOut {
+  int* info = nullptr;
+};
+
+int run_truncate(lrk_ctx* c, const std::string& tag, int64_t n_x, int n_t, const double* W1,
+                 int64_t ld1, const double* W2, int64_t ld2, int R, const int* R_dev, int flags,
+                 double eps0, int r_max, double* out1, int64_t ldo1, double* out2, int64_t ldo2,
+                 int cap, double* sigma, double* sv_all, int no_flip, TruncOut& o, cudaStream_t s) {
+  if (R > NMAX)
+    return fail(c, LRK_ERR_UNSUPPORTED,
+                "lr_truncate on the device supports at most 160 concatenated columns");
+  const int ncta = pick_ncta(c, std::max<int64_t>(n_x, n_t));
+  const int Rw = std::max(R, 1);
+  WS(double, Q1, "tr_Q1", n_x * (int64_t)Rw);
+  WS(double, Q2, "tr_Q2", (int64_t)n_t * Rw);
+  const int64_t ldt = std::max<int64_t>(n_x, n_t);
+  WS(double, tmpw, "tr_tmp", ldt * PMAX);
+  const int64_t pst = trunc_part_stride();
+  WS(double, part, "tr_part", 3 * (int64_t)ncta * pst);
+  const int64_t sst = trunc_scratch_stride(ncta);
+  WS(double, scratch, "tr_scratch", (int64_t)ncta * sst);
+  WS(unsigned, bar, "tr_bar", 4);
+  WS(int, info, tag + "info", 8);
+  WS(TruncArgs, dargs, tag + "args", 1);
+  TruncArgs a{};
+  a.n_x = n_x; a.n_t = n_t; a.R = R; a.R_dev = R_dev; a.flags = flags; a.r_max = r_max; a.eps0 = eps0;
+  a.W1 = W1; a.ld1 = ld1; a.W2 = W2; a.ld2 = ld2;
+  a.Q1 = Q1; a.ldq1 = n_x; a.Q2 = Q2; a.ldq2 = n_t;
+  a.tmpw = tmpw; a.ldtmp = ldt;
+  a.out1 = out1; a.ldo1 = ldo1; a.out2 = out2; a.ldo2 = ldo2; a.cap = cap;
+  a.sigma = sigma; a.sv_all = sv_all; a.info = info;
+  a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
+  a.bar = bar; a.ncta = ncta; a.no_flip = no_flip;
+  CK(cudaMemcpyAsync(dargs, &a, sizeof(a), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
+  CK(launch_truncate(dargs, ncta, s));
+  ++c->launches;
+  o.info = info;
+  return LRK_OK;
+}
+
+// _svd_flip on device factors (rank on device)
+int flip(lrk_ctx* c, double* U, int64_t ldu, int64_t n_x, double* V, int64_t ldv, int n_t,
+         const int* r_dev, int rcap, cudaStream_t s) {
+  if (rcap <= 0) return LRK_OK;
+  const int nparts = grid1(n_x, 4096, 64);
+  WS(double, part, "flip_part", (int64_t)rcap * nparts * 3);
+  flip_partial_kernel<<<dim3(nparts, rcap), 256, 0, s>>>(U, ldu, n_x, r_dev, rcap, part);
+  CKL();
+  flip_apply_kernel<<<dim3(grid1(std::max<int64_t>(n_x, n_t), 256, 256), rcap), 256, 0, s>>>(
+      U, ldu, n_x, V, ldv, n_t, r_dev, rcap, part, nparts);
+  CKL();
+  return LRK_OK;
+}
+
+int check_op(lrk_ctx* c) {
+  if (!c->has_op) return fail(c, LRK_ERR_CONFIG, "no operator installed (lrk_set_operator)");
+  if (c->op.kind != LRK_OP_HEAT)
+    return fail(c, LRK_ERR_UNSUPPORTED,
+                "device spatial solves are implemented for the heat operator only "
+                "(convection-diffusion solves are not yet on the device)");
+  return LRK_OK;
+}
+
+// Observation + weight + truncation of the forward pane (apply_obs_weight,
+// hessian.py:138-156).  Output: spectral Zhat (n_x x cap), Z2 (n_t x cap), zinfo.
+int obs_weight(lrk_ctx* c, const SweepOut& y, double w, double eps0, int r_max, double** Zhat,
+               double** Z2, int** zinfo, int* zcap, cudaStream_t s) {
+  const int64_t nx = c->n_x;
+  const int nt = c->op.n_t;
+  const int cap = y.ucap;
+  WS(double, W2s, "ob_W2s", (int64_t)nt * cap);
+  // W2s = V diag(w * sigma)
+  scale_cols_kernel<<<dim3(grid1(nt, 256, 64), cap), 256, 0, s>>>(y.V, y.ldv, nt, y.sigma,
+                                                                   y.info, cap, w, W2s, nt);
+  CKL();
+  WS(double, Zh, "ob_Zhat", nx * (int64_t)cap);
+  WS(double, Zt, "ob_Z2", (int64_t)nt * cap);
+  TruncOut to;
+  if (c->obs_kind == LRK_OBS_FULL) {
+    TRY(run_truncate(c, "ob_", nx, nt, y.U, y.ldu, W2s, nt, cap, y.info,
+                     LRK_TRUNC_W1_ORTHO | LRK_TRUNC_W2_ORTHOSCALED, eps0, r_max, Zh, nx, Zt, nt,
+                     cap, nullptr, nullptr, 1, to, s));
+  } else {
+    const int no = c->n_obs;
+    WS(double, Uo, "ob_Uobs", (int64_t)no * cap);
+    WS(double, Zo, "ob_Zobs", (int64_t)no * cap);
+    if (c->obs_kind == LRK_OBS_SUBGRID) {
+      TRY(subgrid_gather(c, y.U, y.ldu, Uo, no, cap, y.info, s));
+    } else {
+      WS(double, Up, "ob_Uphys", nx * (int64_t)cap);
+      TRY(dst2(c, y.U, y.ldu, Up, nx, cap, y.info, 1.0, s));
+      gather_rows_kernel<<<dim3(grid1(no, 256, 256), cap), 256, 0, s>>>(Up, nx, c->dList, no,
+                                                                         y.info, cap, Uo, no);
+      CKL();
+    }
+    TRY(run_truncate(c, "ob_", no, nt, Uo, no, W2s, nt, cap, y.info, LRK_TRUNC_W2_ORTHOSCALED,
+                     eps0, r_max, Zo, no, Zt, nt, cap, nullptr, nullptr, 1, to, s));
+    if (c->obs_kind == LRK_OBS_SUBGRID) {
+      TRY(subgrid_scatter(c, Zo, no, Zh, nx, cap, to.info, s));
+    } else {
+      WS(double, Zp, "ob_Zphys", nx * (int64_t)cap);
+      fill_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(Zp, nx, nx, cap, 0.0);
+      CKL();
+      scatter_rows_kernel<<<dim3(grid1(no, 256, 256), cap), 256, 0, s>>>(Zo, no, c->dList, no,
+                                                                          to.info, cap, Zp, nx);
+      CKL();
+      TRY(dst2(c, Zp, nx, Zh, nx, cap, to.info, 1.0, s));
+    }
+  }
+  *Zhat = Zh;
+  *Z2 = Zt;
+  *zinfo = to.info;
+  *zcap = cap;
+  return LRK_OK;
+}
+
+int hd_check(lrk_ctx* c, const lrk_hessian_desc* hd) {
+  if (!hd) return fail(c, LRK_ERR_CONFIG, "null Hessian descriptor");
+  if (!(hd->eps0 > 0.0 && hd->eps0 < 1.0))
+    return fail(c, LRK_ERR_SHAPE, "eps0 must lie in (0, 1)");
+  if (!c->has_obs) return fail(c, LRK_ERR_CONFIG, "no observation layout installed");
+  if (!(hd->gamma_prior > 0.0)) return fail(c, LRK_ERR_CONFIG, "gamma_prior must be positive");
+  return LRK_OK;
+}
+
+int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOut& g,
+                  const int* extra_info, int* out, cudaStream_t s) {
+  std::vector<int> t1(f.nflush + 1), t2(g.nflush + 1);
+  int zr[8] = {0}, er[8] = {0};
+  CK(cudaMemcpyAsync(t1.data(), f.trace, t1.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(t2.data(), g.trace, t2.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(zr, zinfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (extra_info) CK(cudaMemcpyAsync(er, extra_info, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int m = zr[0];
+  for (int v : t1) m = std::max(m, v);
+  for (int v : t2) m = std::max(m, v);
+  if (extra_info) m = std::max(m, er[0]);
+  *out = m;
+  return LRK_OK;
+}
+
+}  // namespace
+
+// ======================================================================== ABI
+extern "C" {
+
+const char* lrk_version(void) { return "lrk-b200 0.1.0 (sm_100a, fp64)"; }
+
+int lrk_ctx_create(int device, lrk_ctx** out) {
+  if (!out) return LRK_ERR_CONFIG;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) { cudaGetLastError(); return LRK_ERR_CUDA; }
+  lrk_ctx* c = new lrk_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return LRK_OK;
+}
+
+void lrk_ctx_destroy(lrk_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  delete c;
+}
+
+const char* lrk_last_error(const lrk_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t lrk_launch_count(const lrk_ctx* c) { return c ? c->launches : 0; }
+
+int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
+  if (!c || !op) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  if (op->dim != 2) return fail(c, LRK_ERR_UNSUPPORTED, "only dim=2 operators are implemented");
+  if (op->n_side < 2 || op->n_t < 1 || !(op->tau > 0) || !(op->h > 0) || !(op->m_scale > 0))
+    return fail(c, LRK_ERR_CONFIG, "invalid operator descriptor");
+  const int n = op->n_side;
+  const int64_t nx = (int64_t)n * n;
+  std::vector<double> S((size_t)n * n), th(nx), thm(nx), il(nx), l1(n), e0(op->n_t, 0.0);
+  const double f = std::sqrt(2.0 / (n + 1));
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k)
+      S[(size_t)j * n + k] = f * std::sin(M_PI * (double)(j + 1) * (double)(k + 1) / (n + 1));
+  const double h = op->h;
+  for (int m = 0; m < n; ++m) {
+    const double sv = std::sin((m + 1) * M_PI * h / 2.0);
+    l1[m] = (4.0 / (h * h)) * sv * sv;  // discretize.py:137-144 (per axis)
+  }
+  for (int i2 = 0; i2 < n; ++i2)
+    for (int i1 = 0; i1 < n; ++i1) {
+      const double lam = l1[i1] + l1[i2];
+      const double t = 1.0 / (1.0 + op->tau * lam);
+      th[(size_t)i2 * n + i1] = t;
+      thm[(size_t)i2 * n + i1] = t / op->m_scale;
+      il[(size_t)i2 * n + i1] = 1.0 / lam;
+    }
+  e0[0] = 1.0;
+  cudaFree(c->dS); cudaFree(c->dTheta); cudaFree(c->dThetaM); cudaFree(c->dE0);
+  cudaFree(c->dInvLam);
+  c->dS = c->dTheta = c->dThetaM = c->dE0 = c->dInvLam = nullptr;
+  CK(cudaMalloc(&c->dInvLam, nx * sizeof(double)));
+  CK(cudaMemcpy(c->dInvLam, il.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&c->dS, S.size() * sizeof(double)));
+  CK(cudaMalloc(&c->dTheta, nx * sizeof(double)));
+  CK(cudaMalloc(&c->dThetaM, nx * sizeof(double)));
+  CK(cudaMalloc(&c->dE0, e0.size() * sizeof(double)));
+  CK(cudaMemcpy(c->dS, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->dTheta, th.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->dThetaM, thm.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->dE0, e0.data(), e0.size() * sizeof(double), cudaMemcpyHostToDevice));
+  c->op = *op;
+  c->n = n;
+  c->n_x = nx;
+  c->has_op = true;
+  c->has_obs = false;
+  return LRK_OK;
+}
+
+int lrk_set_observation(lrk_ctx* c, const lrk_obs_desc* obs) {
+  if (!c || !obs) return LRK_ERR_CONFIG;
+  if (!c->has_op) return fail(c, LRK_ERR_CONFIG, "install the operator first");
+  CK(cudaSetDevice(c->device));
+  const int n = c->n;
+  cudaFree(c->dList); cudaFree(c->dS1T); cudaFree(c->dS2); cudaFree(c->dS1); cudaFree(c->dS2T);
+  c->dList = nullptr; c->dS1T = c->dS2 = c->dS1 = c->dS2T = nullptr;
+  c->obs_kind = obs->kind;
+  if (obs->kind == LRK_OBS_FULL) {
+    c->n_obs = (int)c->n_x;
+  } else if (obs->kind == LRK_OBS_SUBGRID) {
+    const int s1 = obs->n1, s2 = obs->n2;
+    if (s1 < 1 || s2 < 1) return fail(c, LRK_ERR_CONFIG, "empty sensor subgrid");
+    std::vector<double> S1T((size_t)n * s1), S2((size_t)s2 * n), S1((size_t)s1 * n),
+        S2T((size_t)n * s2);
+    const double f = std::sqrt(2.0 / (n + 1));
+    auto Sv = [&](int j, int k) { return f * std::sin(M_PI * (double)(j + 1) * (double)(k + 1) / (n + 1)); };
+    for (int a = 0; a < s1; ++a) {
+      const int i1 = obs->idx1[a];
+      if (i1 < 0 || i1 >= n) return fail(c, LRK_ERR_CONFIG, "sensor index out of range");
+      for (int k = 0; k < n; ++k) { S1T[(size_t)k * s1 + a] = Sv(k, i1); S1[(size_t)a * n + k] = Sv(i1, k); }
+    }
+    for (int b = 0; b < s2; ++b) {
+      const int i2 = obs->idx2[b];
+      if (i2 < 0 || i2 >= n) return fail(c, LRK_ERR_CONFIG, "sensor index out of range");
+      for (int k = 0; k < n; ++k) { S2[(size_t)b * n + k] = Sv(i2, k); S2T[(size_t)k * s2 + b] = Sv(k, i2); }
+    }
+    CK(cudaMalloc(&c->dS1T, S1T.size() * 8)); CK(cudaMalloc(&c->dS2, S2.size() * 8));
+    CK(cudaMalloc(&c->dS1, S1.size() * 8)); CK(cudaMalloc(&c->dS2T, S2T.size() * 8));
+    CK(cudaMemcpy(c->dS1T, S1T.data(), S1T.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dS2, S2.data(), S2.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dS1, S1.data(), S1.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dS2T, S2T.data(), S2T.size() * 8, cudaMemcpyHostToDevice));
+    c->s1 = s1; c->s2 = s2;
+    c->n_obs = s1 * s2;
+  } else if (obs->kind == LRK_OBS_LIST) {
+    if (obs->n_list < 0) return fail(c, LRK_ERR_CONFIG, "negative sensor count");
+    c->n_obs = obs->n_list;
+    if (obs->n_list > 0) {
+      for (int k = 0; k < obs->n_list; ++k)
+        if (obs->list[k] < 0 || obs->list[k] >= c->n_x)
+          return fail(c, LRK_ERR_CONFIG, "sensor dof out of range");
+      CK(cudaMalloc(&c->dList, obs->n_list * sizeof(int32_t)));
+      CK(cudaMemcpy(c->dList, obs->list, obs->n_list * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+  } else {
+    return fail(c, LRK_ERR_CONFIG, "unknown observation kind");
+  }
+  c->has_obs = true;
+  return LRK_OK;
+}
+
+int lrk_truncate(lrk_ctx* c, const lrk_lr* in, lrk_lr* out, double eps0, int r_max, int flags,
+                 int* r_out, void* stream) {
+  if (!c || !in || !out) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(eps0 > 0.0 && eps0 < 1.0)) return fail(c, LRK_ERR_SHAPE, "eps0 must lie in (0, 1)");
+  if (in->n_x != out->n_x || in->n_t != out->n_t) return fail(c, LRK_ERR_SHAPE, "shape mismatch");
+  if (in->r == 0) { out->r = 0; if (r_out) *r_out = 0; return LRK_OK; }
+  TruncOut to;
+  TRY(run_truncate(c, "tu_", in->n_x, in->n_t, in->W1, in->ld1, in->W2, in->ld2, in->r, nullptr,
+                   flags, eps0, r_max, out->W1, out->ld1, out->W2, out->ld2, out->cap, nullptr,
+                   nullptr, 0, to, s));
+  int info[8];
+  CK(cudaMemcpyAsync(info, to.info, sizeof(info), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (info[2] != 0) return fail(c, LRK_ERR_SHAPE, "output capacity too small for the truncated rank");
+  out->r = info[0];
+  if (r_out) *r_out = info[0];
+  return LRK_OK;
+}
+
+int lrk_singular_values(lrk_ctx* c, const lrk_lr* a, double* s_host, int cap, int* n_out,
+                        void* stream) {
+  if (!c || !a) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (a->r == 0) { if (n_out) *n_out = 0; return LRK_OK; }
+  const int R = a->r;
+  WS(double, o1, "sv_o1", a->n_x * (int64_t)R);
+  WS(double, o2, "sv_o2", (int64_t)a->n_t * R);
+  WS(double, sv, "sv_all", NMAX);
+  TruncOut to;
+  TRY(run_truncate(c, "sv_", a->n_x, a->n_t, a->W1, a->ld1, a->W2, a->ld2, R, nullptr, 0, 1e-300,
+                   -1, o1, a->n_x, o2, a->n_t, R, nullptr, sv, 1, to, s));
+  std::vector<double> h(R);
+  CK(cudaMemcpyAsync(h.data(), sv, R * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int n = std::min(R, cap);
+  for (int i = 0; i < n; ++i) s_host[i] = h[i];
+  if (n_out) *n_out = n;
+  return LRK_OK;
+}
+
+int lrk_dot(lrk_ctx* c, const lrk_lr* A, const lrk_lr* B, double* out, void* stream) {
+  if (!c || !A || !B || !out) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (A->n_x != B->n_x || A->n_t != B->n_t) return fail(c, LRK_ERR_SHAPE, "shape mismatch");
+  if (A->r == 0 || B->r == 0) { *out = 0.0; return LRK_OK; }
+  const int na = A->r, nb = B->r, nout = na * nb;
+  const int g1 = grid1(A->n_x, 4096, 2 * c->num_sms), g2 = grid1(A->n_t, 4096, 32);
+  WS(double, p1, "dot_p1", (int64_t)g1 * nout);
+  WS(double, p2, "dot_p2", (int64_t)g2 * nout);
+  WS(double, res, "dot_res", 1);
+  gram_partial_kernel<<<g1, NT, 0, s>>>(A->W1, A->ld1, na, B->W1, B->ld1, nb, A->n_x, p1);
+  CKL();
+  gram_partial_kernel<<<g2, NT, 0, s>>>(A->W2, A->ld2, na, B->W2, B->ld2, nb, A->n_t, p2);
+  CKL();
+  dot_finalize_kernel<<<1, 256, 0, s>>>(p1, g1, p2, g2, nout, res);
+  CKL();
+  CK(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return LRK_OK;
+}
+
+int lrk_step_solve(lrk_ctx* c, const double* B, int64_t ldb, int ncols, int adjoint, double* X,
+                   int64_t ldx, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  TRY(check_op(c));
+  (void)adjoint;  // heat: S is symmetric, S^{-T} = S^{-1}
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ncols <= 0) return LRK_OK;
+  const int64_t nx = c->n_x;
+  WS(double, T2, "ss_T2", nx * (int64_t)ncols);
+  TRY(dst2(c, B, ldb, T2, nx, ncols, nullptr, 1.0, s));
+  scale_rows_kernel<<<dim3(grid1(nx, 256, 1024), ncols), 256, 0, s>>>(T2, nx, c->dThetaM, nx,
+                                                                       ncols, nullptr, 1.0, T2, nx);
+  CKL();
+  TRY(dst2(c, T2, nx, X, ldx, ncols, nullptr, 1.0, s));
+  return LRK_OK;
+}
+
+int lrk_poisson_solve(lrk_ctx* c, const double* B, int64_t ldb, int ncols, double* X,
+                      int64_t ldx, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  TRY(check_op(c));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ncols <= 0) return LRK_OK;
+  const int64_t nx = c->n_x;
+  WS(double, T2, "ps_T2", nx * (int64_t)ncols);
+  TRY(dst2(c, B, ldb, T2, nx, ncols, nullptr, 1.0, s));
+  scale_rows_kernel<<<dim3(grid1(nx, 256, 1024), ncols), 256, 0, s>>>(T2, nx, c->dInvLam, nx,
+                                                                       ncols, nullptr, 1.0, T2, nx);
+  CKL();
+  TRY(dst2(c, T2, nx, X, ldx, ncols, nullptr, 1.0, s));
+  return LRK_OK;
+}
+
+int lrk_operator_apply(lrk_ctx* c, const lrk_lr* Y, int adjoint, lrk_lr* out, void* stream) {
+  if (!c || !Y || !out) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  if (!c->has_op) return fail(c, LRK_ERR_CONFIG, "no operator installed");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int r = Y->r;
+  if (out->cap < 2 * r) return fail(c, LRK_ERR_SHAPE, "output capacity must be >= 2r");
+  if (r == 0) { out->r = 0; return LRK_OK; }
+  const lrk_operator_desc& op = c->op;
+  const double h = op.h, ih2 = 1.0 / (h * h);
+  StencilArgs a{};
+  double cc, cw, ce, cs_, cn_;
+  if (op.kind == LRK_OP_HEAT) {
+    cc = 4.0 * ih2; cw = ce = cs_ = cn_ = -ih2;
+  } else {
+    cc = op.nu * 4.0 * ih2; cw = ce = cs_ = cn_ = -op.nu * ih2;
+    const double w1 = op.wind[0], w2 = op.wind[1];
+    if (w1 > 0) { cc += w1 / h; cw -= w1 / h; } else if (w1 < 0) { cc -= w1 / h; ce += w1 / h; }
+    if (w2 > 0) { cc += w2 / h; cs_ -= w2 / h; } else if (w2 < 0) { cc -= w2 / h; cn_ += w2 / h; }
+  }
+  if (adjoint) { std::swap(cw, ce); std::swap(cs_, cn_); }
+  a.X = Y->W1; a.ldx = Y->ld1; a.Y = out->W1; a.ldy = out->ld1; a.n = c->n; a.ncols = r;
+  a.cc = cc; a.cw = cw; a.ce = ce; a.cs = cs_; a.cn = cn_; a.m_scale = op.m_scale; a.tau = op.tau;
+  stencil_kernel<<<dim3(grid1(c->n_x, 256, 1 << 30), r), 256, 0, s>>>(a);
+  CKL();
+  // W2 copy into the first r columns; shift + (-M W1) into the second r
+  scale_cols_kernel<<<dim3(grid1(Y->n_t, 256, 64), r), 256, 0, s>>>(Y->W2, Y->ld2, Y->n_t, nullptr,
+                                                                     nullptr, r, 1.0, out->W2, out->ld2);
+  CKL();
+  shift_kernel<<<dim3(grid1(std::max<int64_t>(c->n_x, Y->n_t), 256, 1 << 30), r), 256, 0, s>>>(
+      Y->W2, Y->ld2, Y->n_t, r, adjoint, out->W2 + (int64_t)r * out->ld2, out->ld2, Y->W1, Y->ld1,
+      c->n_x, -op.m_scale, out->W1 + (int64_t)r * out->ld1, out->ld1);
+  CKL();
+  out->r = 2 * r;
+  return LRK_OK;
+}
+
+int lrk_st_solve_sweep(lrk_ctx* c, const lrk_lr* rhs, int adjoint, int compress_every,
+                       double eps0, int r_max, lrk_lr* out, int* trace, int trace_cap,
+                       int* trace_len, void* stream) {
+  if (!c || !rhs || !out) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  TRY(check_op(c));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (rhs->n_x != c->n_x || rhs->n_t != c->op.n_t)
+    return fail(c, LRK_ERR_SHAPE, "rhs shape does not match the operator");
+  if (trace_len) *trace_len = 0;
+  if (rhs->r == 0) { out->r = 0; return LRK_OK; }
+  const int64_t nx = c->n_x;
+  const int nt = c->op.n_t;
+  WS(double, Bh, "api_B", nx * (int64_t)rhs->r);
+  TRY(dst2(c, rhs->W1, rhs->ld1, Bh, nx, rhs->r, nullptr, 1.0, s));
+  SweepOut o;
+  TRY(run_sweep(c, "s0_", Bh, nx, rhs->r, nullptr, rhs->W2, rhs->ld2, adjoint, compress_every, eps0,
+                r_max, o, s));
+  int info[8];
+  CK(cudaMemcpyAsync(info, o.info, sizeof(info), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (info[2] != 0) return fail(c, LRK_ERR_NUMERICAL, "sweep rank exceeded the device core limit");
+  const int r = info[0];
+  if (r > out->cap) return fail(c, LRK_ERR_SHAPE, "output capacity too small for the pane rank");
+  if (r > 0) {
+    TRY(dst2(c, o.U, o.ldu, out->W1, out->ld1, r, nullptr, 1.0, s));
+    scale_cols_kernel<<<dim3(grid1(nt, 256, 64), r), 256, 0, s>>>(o.V, o.ldv, nt, o.sigma, nullptr,
+                                                                   r, 1.0, out->W2, out->ld2);
+    CKL();
+    TRY(flip(c, out->W1, out->ld1, nx, out->W2, out->ld2, nt, nullptr, r, s));
+  }
+  out->r = r;
+  if (trace) {
+    const int n = std::min(trace_cap, o.nflush + 1);
+    CK(cudaMemcpyAsync(trace, o.trace, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (trace_len) *trace_len = n;
+  }
+  return LRK_OK;
+}
+
+int lrk_hessian_apply_ic(lrk_ctx* c, const lrk_hessian_desc* hd, int nbatch, const double* V,
+                         int64_t ldv, double* OUT, int64_t ldo, int* max_rank, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  TRY(check_op(c));
+  TRY(hd_check(c, hd));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nx = c->n_x;
+  const int nt = c->op.n_t;
+  const double M = c->op.m_scale, sg = std::sqrt(hd->gamma_prior);
+  WS(double, Bv, "ic_B", nx);
+  WS(double, q, "ic_q", nx);
+  for (int b = 0; b < nbatch; ++b) {
+    const double* v = V + (int64_t)b * ldv;
+    double* out = OUT + (int64_t)b * ldo;
+    // inject: rhs = (M sqrt(g) v) e_0^T, spectral  (forward.py:108-109)
+    TRY(dst2(c, v, nx, Bv, nx, 1, nullptr, sg * M, s));
+    SweepOut fw, bw;
+    TRY(run_sweep(c, "f_", Bv, nx, 1, nullptr, c->dE0, nt, 0, hd->compress_every, hd->eps0,
+                  hd->r_max, fw, s));
+    double *Zh, *Z2;
+    int* zinfo;
+    int zcap;
+    TRY(obs_weight(c, fw, hd->obs_weight, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo, &zcap, s));
+    TRY(run_sweep(c, "b_", Zh, nx, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
+                  bw, s));
+    // extract: sqrt(g) M Q.column(0)  (forward.py:111-112)
+    column_eval_kernel<<<grid1(nx, 256, 1024), 256, 0, s>>>(bw.U, bw.ldu, nx, bw.sigma, bw.V,
+                                                              bw.ldv, 0, bw.info, q);
+    CKL();
+    TRY(dst2(c, q, nx, out, nx, 1, nullptr, sg * M, s));
+    if (max_rank) TRY(host_max_rank(c, fw, zinfo, bw, nullptr, &max_rank[b], s));
+  }
+  return LRK_OK;
+}
+
+int lrk_hessian_apply_st(lrk_ctx* c, const lrk_hessian_desc* hd, const lrk_lr* v, lrk_lr* out,
+                         int* max_rank, void* stream) {
+  if (!c || !v || !out) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  TRY(check_op(c));
+  TRY(hd_check(c, hd));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nx = c->n_x;
+  const int nt = c->op.n_t;
+  if (v->n_x != nx || v->n_t != nt) return fail(c, LRK_ERR_SHAPE, "field shape mismatch");
+  if (v->r == 0) { out->r = 0; if (max_rank) *max_rank = 0; return LRK_OK; }
+  const double M = c->op.m_scale, tau = c->op.tau, sg = std::sqrt(hd->gamma_prior);
+  WS(double, Bh, "st_B", nx * (int64_t)v->r);
+  // rhs = tau M sqrt(g) v  (forward.py:121-122, hessian.py:236)
+  TRY(dst2(c, v->W1, v->ld1, Bh, nx, v->r, nullptr, tau * M * sg, s));
+  SweepOut fw, bw;
+  TRY(run_sweep(c, "f_", Bh, nx, v->r, nullptr, v->W2, v->ld2, 0, hd->compress_every, hd->eps0,
+                hd->r_max, fw, s));
+  double *Zh, *Z2;
+  int* zinfo;
+  int zcap;
+  TRY(obs_weight(c, fw, hd->obs_weight, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo, &zcap, s));
+  TRY(run_sweep(c, "b_", Zh, nx, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
+                bw, s));
+  // out = truncate(sqrt(g) tau M Q)  (hessian.py:242)
+  const int cap = bw.ucap;
+  WS(double, Up, "st_Uphys", nx * (int64_t)cap);
+  WS(double, W2o, "st_W2o", (int64_t)nt * cap);
+  TRY(dst2(c, bw.U, bw.ldu, Up, nx, cap, bw.info, 1.0, s));
+  scale_cols_kernel<<<dim3(grid1(nt, 256, 64), cap), 256, 0, s>>>(bw.V, bw.ldv, nt, bw.sigma,
+                                                                   bw.info, cap, sg * tau * M, W2o, nt);
+  CKL();
+  TruncOut to;
+  TRY(run_truncate(c, "so_", nx, nt, Up, nx, W2o, nt, cap, bw.info,
+                   LRK_TRUNC_W1_ORTHO | LRK_TRUNC_W2_ORTHOSCALED, hd->eps0, hd->r_max, out->W1,
+                   out->ld1, out->W2, out->ld2, out->cap, nullptr, nullptr, 0, to, s));
+  int info[8];
+  CK(cudaMemcpyAsync(info, to.info, sizeof(info), cudaMemcpyDeviceToHost, s));
+  int mr = 0;
+  TRY(host_max_rank(c, fw, zinfo, bw, to.info, &mr, s));
+  if (info[2] != 0) return fail(c, LRK_ERR_SHAPE, "output capacity too small");
+  out->r = info[0];
+  if (max_rank) *max_rank = mr;
+  return LRK_OK;
+}
+
+int lrk_cgs2(lrk_ctx* c, const double* Q, int64_t ldq, int k, double* w, int n, double* h_host,
+             double* norm_out, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g = grid1(n, 4096, 2 * c->num_sms);
+  const int kk = std::max(k, 1);
+  WS(double, part, "cg_part", (int64_t)g * kk);
+  WS(double, hp, "cg_h", kk);
+  WS(double, hacc, "cg_hacc", kk + 1);
+  CK(cudaMemsetAsync(hacc, 0, (kk + 1) * sizeof(double), s));
+  for (int pass = 0; pass < 2 && k > 0; ++pass) {
+    gram_partial_kernel<<<g, NT, 0, s>>>(Q, ldq, k, w, n, 1, n, part);
+    CKL();
+    reduce_parts_kernel<<<grid1(k, 256, 64), 256, 0, s>>>(part, g, k, hp, hacc);
+    CKL();
+    sub_qh_kernel<<<grid1(n, 256, 2048), 256, 0, s>>>(Q, ldq, k, hp, w, n);
+    CKL();
+  }
+  gram_partial_kernel<<<g, NT, 0, s>>>(w, n, 1, w, n, 1, n, part);
+  CKL();
+  reduce_parts_kernel<<<1, 256, 0, s>>>(part, g, 1, hacc + kk, nullptr);
+  CKL();
+  std::vector<double> hh(kk + 1);
+  CK(cudaMemcpyAsync(hh.data(), hacc, (kk + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < k; ++i) h_host[i] = hh[i];
+  if (norm_out) *norm_out = std::sqrt(std::max(hh[kk], 0.0));
+  return LRK_OK;
+}
+
+int lrk_combine(lrk_ctx* c, const double* Q, int64_t ldq, int k, const double* c_host, int n,
+                double* y, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  WS(double, cf, "cb_cf", std::max(k, 1));
+  CK(cudaMemcpyAsync(cf, c_host, k * sizeof(double), cudaMemcpyHostToDevice, s));
+  combine_kernel<<<grid1(n, 256, 2048), 256, 0, s>>>(Q, ldq, k, cf, y, n);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  return LRK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,560 @@
+// lrk_device.cuh — device building blocks shared by the persistent kernels.
+//
+// Everything here runs inside cooperative kernels whose CTAs form "groups":
+// a group of `ncta` CTAs owns one problem (one sweep / one truncation) and
+// synchronises with a software grid barrier.  Rows of every tall factor
+// (n_x or n_t rows) are split into contiguous per-CTA ranges, so all
+// "row-local" work needs no synchronisation; only small r x p partial sums
+// cross CTAs, through L2 (ld.global.cg), reduced in a fixed order so every CTA
+// of a group sees bit-identical results and takes identical control flow.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrk {
+
+constexpr int NT = 512;            // threads per CTA of the persistent kernels
+constexpr int NWARP = NT / 32;
+constexpr int PMAX = 16;           // max columns appended per block (compress_every)
+constexpr int JMAX_SMEM = 80;      // Jacobi SVD kept in SMEM up to this order
+constexpr int NMAX = 160;          // absolute max order of a core matrix
+constexpr double DEPS = 2.220446049250313e-16;
+constexpr double NOISE_FLOOR = 1e-15;   // lowrank.py:20-22
+
+// ------------------------------------------------------------------ barrier
+// Sense-free generation barrier for the `ncta` CTAs of one group.
+// bar[0] = arrival count, bar[1] = generation.
+__device__ __forceinline__ void group_barrier(unsigned* bar, int ncta) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    unsigned gen = *vgen;
+    __threadfence();
+    unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == (unsigned)ncta - 1u) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) { __nanosleep(20); }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum K per-thread values over the whole CTA; every thread gets the sums in
+// out[0..K).  red must hold NWARP*K doubles; fixed order -> deterministic.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* red, double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) red[w * K + i] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int ww = 0; ww < NWARP; ++ww) s += red[ww * K + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < K; ++i) v[i] = out[i];
+  __syncthreads();
+}
+
+// Runtime-length variant: per-thread values live in a per-thread stripe of
+// `vals` (vals[k*NT + tid], k < K); results to out[0..K).  red: NWARP*K.
+__device__ inline void block_sum_rt(double* vals, int K, double* red, double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < K; ++k) {
+    double s = warp_sum(vals[k * NT + threadIdx.x]);
+    if (lane == 0) red[w * K + k] = s;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += NT) {
+    double s = 0.0;
+    for (int ww = 0; ww < NWARP; ++ww) s += red[ww * K + k];
+    out[k] = s;
+  }
+  __syncthreads();
+}
+
+// Reduce per-CTA partials written by the ncta CTAs of a group:
+// out[o] = sum_c part[c*stride + o], o < len.  Reads through L2 (.cg) because
+// other SMs wrote the data.  Every CTA computes the same sums in the same
+// order.  out is shared memory.
+__device__ inline void reduce_partials(const double* part, int64_t stride, int ncta,
+                                       int len, double* out) {
+  int lp = 1;
+  while (lp < 32 && lp * 2 * len <= NT) lp *= 2;
+  const int tid = threadIdx.x;
+  if (lp > 1) {
+    const int o = tid / lp, sub = tid % lp;
+    double acc = 0.0;
+    if (o < len)
+      for (int c = sub; c < ncta; c += lp) acc += __ldcg(part + (int64_t)c * stride + o);
+    for (int m = lp >> 1; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (o < len && sub == 0) out[o] = acc;
+  } else {
+    for (int o = tid; o < len; o += NT) {
+      double acc = 0.0;
+      for (int c = 0; c < ncta; ++c) acc += __ldcg(part + (int64_t)c * stride + o);
+      out[o] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// CTA-partial of A^T B over `nrows` rows: out[i*nb + j] = sum_t A[t + i*lda] *
+// B[t + j*ldb].  scratch: NT doubles of shared memory; out: shared.
+__device__ inline void cta_tn(const double* A, int64_t lda, int na, const double* B,
+                              int64_t ldb, int nb, int nrows, double* out, double* scratch) {
+  const int nout = na * nb;
+  const int tid = threadIdx.x;
+  if (nout == 0) return;
+  if (nout <= NT) {
+    const int nslice = NT / nout;
+    const int o = tid % nout, s = tid / nout;
+    double acc = 0.0;
+    if (s < nslice) {
+      const int i = o / nb, j = o % nb;
+      const double* a = A + (int64_t)i * lda;
+      const double* b = B + (int64_t)j * ldb;
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      int t = s;
+      for (; t + 3 * nslice < nrows; t += 4 * nslice) {
+        a0 += a[t] * b[t];
+        a1 += a[t + nslice] * b[t + nslice];
+        a2 += a[t + 2 * nslice] * b[t + 2 * nslice];
+        a3 += a[t + 3 * nslice] * b[t + 3 * nslice];
+      }
+      for (; t < nrows; t += nslice) a0 += a[t] * b[t];
+      acc = (a0 + a1) + (a2 + a3);
+    }
+    if (s < nslice) scratch[s * nout + o] = acc;
+    __syncthreads();
+    if (tid < nout) {
+      double v = 0.0;
+      for (int q = 0; q < nslice; ++q) v += scratch[q * nout + tid];
+      out[tid] = v;
+    }
+    __syncthreads();
+  } else {
+    for (int o = tid; o < nout; o += NT) {
+      const int i = o / nb, j = o % nb;
+      const double* a = A + (int64_t)i * lda;
+      const double* b = B + (int64_t)j * ldb;
+      double acc = 0.0;
+      for (int t = 0; t < nrows; ++t) acc += a[t] * b[t];
+      out[o] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Row-local update X[:, 0..nx) -= A[:, 0..na) * Cm, Cm is na x nx row-major
+// in shared memory (Cm[i*nx + j]).
+__device__ inline void rows_sub_gemm(double* X, int64_t ldx, int nx, const double* A,
+                                     int64_t lda, int na, const double* Cm, int nrows) {
+  for (int t = threadIdx.x; t < nrows; t += NT) {
+    double acc[PMAX];
+#pragma unroll
+    for (int j = 0; j < PMAX; ++j) acc[j] = 0.0;
+    for (int i = 0; i < na; ++i) {
+      const double a = A[t + (int64_t)i * lda];
+#pragma unroll
+      for (int j = 0; j < PMAX; ++j)
+        if (j < nx) acc[j] += a * Cm[i * nx + j];
+    }
+#pragma unroll
+    for (int j = 0; j < PMAX; ++j)
+      if (j < nx) X[t + (int64_t)j * ldx] -= acc[j];
+  }
+}
+
+// ------------------------------------------------- block Householder QR
+// In-place Householder QR of the CTA-local block X (m x q, col-major, ldx),
+// q <= PMAX.  Reflector vectors overwrite X below the diagonal (unit leading
+// entry implicit), tau[j] saved; R (q x q, row-major, zero-padded when m < q)
+// is written to Rout.  red: NWARP*PMAX doubles, tmp: PMAX doubles (shared).
+__device__ inline void block_householder_qr(double* X, int64_t ldx, int m, int q,
+                                            double* tau, double* Rout, double* red,
+                                            double* tmp) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < q * q; i += NT) Rout[i] = 0.0;
+  __syncthreads();
+  const int kmax = m < q ? m : q;
+  for (int j = 0; j < kmax; ++j) {
+    double v1[1];
+    {
+      double s = 0.0;
+      for (int i = j + 1 + tid; i < m; i += NT) {
+        double x = X[i + (int64_t)j * ldx];
+        s += x * x;
+      }
+      v1[0] = s;
+    }
+    block_sum<1>(v1, red, tmp);
+    const double sig = v1[0];
+    const double alpha = X[j + (int64_t)j * ldx];
+    double beta, t, scale;
+    if (sig == 0.0) {
+      t = 0.0; beta = alpha; scale = 0.0;
+    } else {
+      double nrm = sqrt(alpha * alpha + sig);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    __syncthreads();  // everyone has read alpha before row j changes
+    if (tid == 0) tau[j] = t;
+    // v_i = X[i,j]*scale for i>j (stored in place)
+    for (int i = j + 1 + tid; i < m; i += NT) X[i + (int64_t)j * ldx] *= scale;
+    __syncthreads();
+    // w_k = x_jk + sum_{i>j} v_i x_ik for k in (j, q)
+    double w[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) w[k] = 0.0;
+    for (int i = j + 1 + tid; i < m; i += NT) {
+      const double vi = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int k = 0; k < PMAX; ++k)
+        if (k > j && k < q) w[k] += vi * X[i + (int64_t)k * ldx];
+    }
+    block_sum<PMAX>(w, red, tmp);
+    // apply: x_ik -= tau * v_i * w_k (row j: v_j = 1)
+    for (int k = j + 1; k < q; ++k) {
+      const double wk = w[k] + X[j + (int64_t)k * ldx];
+      const double f = t * wk;
+      for (int i = j + 1 + tid; i < m; i += NT) X[i + (int64_t)k * ldx] -= f * X[i + (int64_t)j * ldx];
+      __syncthreads();
+      if (tid == 0) {
+        X[j + (int64_t)k * ldx] -= f;
+        Rout[j * q + k] = X[j + (int64_t)k * ldx];
+      }
+    }
+    if (tid == 0) { Rout[j * q + j] = beta; X[j + (int64_t)j * ldx] = beta; }
+    __syncthreads();
+  }
+  for (int j = kmax + tid; j < q; j += NT) tau[j] = 0.0;
+  __syncthreads();
+}
+
+// Y (m x q) = H_0 H_1 ... H_{kmax-1} [G; 0], G (q x q row-major, shared),
+// reflectors from block_householder_qr stored in X.  Y is written fresh.
+__device__ inline void block_householder_apply_q(const double* X, int64_t ldx, int m, int q,
+                                                 const double* tau, const double* G,
+                                                 double* Y, int64_t ldy, double* red,
+                                                 double* tmp) {
+  const int tid = threadIdx.x;
+  for (int c = 0; c < q; ++c)
+    for (int i = tid; i < m; i += NT) Y[i + (int64_t)c * ldy] = (i < q) ? G[i * q + c] : 0.0;
+  __syncthreads();
+  const int kmax = m < q ? m : q;
+  for (int j = kmax - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;  // uniform across the CTA
+    double w[PMAX];
+#pragma unroll
+    for (int c = 0; c < PMAX; ++c) w[c] = 0.0;
+    for (int i = j + 1 + tid; i < m; i += NT) {
+      const double vi = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int c = 0; c < PMAX; ++c)
+        if (c < q) w[c] += vi * Y[i + (int64_t)c * ldy];
+    }
+    block_sum<PMAX>(w, red, tmp);
+    for (int c = 0; c < q; ++c) {
+      const double f = t * (w[c] + Y[j + (int64_t)c * ldy]);
+      for (int i = j + 1 + tid; i < m; i += NT) Y[i + (int64_t)c * ldy] -= f * X[i + (int64_t)j * ldx];
+      __syncthreads();
+      if (tid == 0) Y[j + (int64_t)c * ldy] -= f;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------ small dense helpers
+// Single-thread column-pivoted Householder QR of a q x q matrix A (row-major,
+// in place): A*P = X*Rt.  Writes X (q x q row-major, orthogonal), Rt (upper,
+// row-major, in A) and perm (Rt column k corresponds to A column perm[k]).
+__device__ inline void small_pivoted_qr(double* A, int q, double* X, int* perm, double* cn) {
+  for (int k = 0; k < q; ++k) {
+    perm[k] = k;
+    double s = 0;
+    for (int i = 0; i < q; ++i) s += A[i * q + k] * A[i * q + k];
+    cn[k] = s;
+  }
+  for (int i = 0; i < q * q; ++i) X[i] = (i / q == i % q) ? 1.0 : 0.0;
+  for (int j = 0; j < q; ++j) {
+    // pivot: largest remaining column norm (recomputed exactly)
+    int best = j; double bv = -1.0;
+    for (int k = j; k < q; ++k) {
+      double s = 0;
+      for (int i = j; i < q; ++i) s += A[i * q + k] * A[i * q + k];
+      cn[k] = s;
+      if (s > bv) { bv = s; best = k; }
+    }
+    if (best != j) {
+      for (int i = 0; i < q; ++i) { double t = A[i * q + j]; A[i * q + j] = A[i * q + best]; A[i * q + best] = t; }
+      int t = perm[j]; perm[j] = perm[best]; perm[best] = t;
+    }
+    double sig = 0;
+    for (int i = j + 1; i < q; ++i) sig += A[i * q + j] * A[i * q + j];
+    if (sig == 0.0) continue;
+    double alpha = A[j * q + j];
+    double nrm = sqrt(alpha * alpha + sig);
+    double beta = alpha >= 0 ? -nrm : nrm;
+    double tau = (beta - alpha) / beta;
+    double sc = 1.0 / (alpha - beta);
+    double v[PMAX];
+    v[j] = 1.0;
+    for (int i = j + 1; i < q; ++i) v[i] = A[i * q + j] * sc;
+    // A <- H A on columns j..q-1
+    for (int k = j; k < q; ++k) {
+      double w = 0;
+      for (int i = j; i < q; ++i) w += v[i] * A[i * q + k];
+      w *= tau;
+      for (int i = j; i < q; ++i) A[i * q + k] -= w * v[i];
+    }
+    // X <- X H (accumulate Q = H_0 H_1 ...)
+    for (int i = 0; i < q; ++i) {
+      double w = 0;
+      for (int l = j; l < q; ++l) w += X[i * q + l] * v[l];
+      w *= tau;
+      for (int l = j; l < q; ++l) X[i * q + l] -= w * v[l];
+    }
+    for (int i = j + 1; i < q; ++i) A[i * q + j] = 0.0;
+  }
+}
+
+// _rank_cut (lowrank.py:98-111) on descending s[0..n); single thread.
+__device__ inline int rank_cut_dev(const double* s, int n, double eps0, int r_max) {
+  if (n == 0 || !(s[0] > 0.0)) return 0;
+  const double floor_v = NOISE_FLOOR * s[0];
+  // tail[r] = sqrt(sum_{i>=r} s_i^2) accumulated from the end (as np.cumsum on
+  // the reversed array); keep = smallest r with tail[r] <= eps0*tail[0].
+  double tail[NMAX + 1];
+  double acc = 0.0;
+  int nnz = 0;
+  tail[n] = 0.0;
+  for (int i = n - 1; i >= 0; --i) {
+    double si = s[i] < floor_v ? 0.0 : s[i];
+    if (si != 0.0) ++nnz;
+    acc += si * si;
+    tail[i] = sqrt(acc);
+  }
+  const double thr = eps0 * tail[0];
+  int keep = n;  // searchsorted(-tail, -thr, 'left') over indices 0..n-1
+  for (int i = 0; i < n; ++i) {
+    if (!(tail[i] > thr)) { keep = i; break; }
+  }
+  if (keep > nnz) keep = nnz;
+  if (r_max >= 0 && keep > r_max) keep = r_max;
+  return keep;
+}
+
+// --------------------------------------------------- one-sided Jacobi SVD
+// SVD of the n x n matrix held in A (col-major, lda) by cyclic one-sided
+// (Hestenes) Jacobi with a round-robin parallel ordering; one warp per
+// column pair.  On exit: V (col-major, ldv) holds right singular vectors
+// (unsorted), columns of A hold U*diag(s) (unsorted), s_sorted[k] the k-th
+// largest singular value, perm[k] its column.  nrm: n doubles, flag: 1 int
+// (all shared).
+__device__ inline void jacobi_svd(double* A, int lda, double* V, int ldv, int n,
+                                  double* s_sorted, int* perm, double* nrm, int* flag) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int idx = tid; idx < n * n; idx += NT) {
+    int i = idx % n, j = idx / n;
+    V[i + j * ldv] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int ne = n + (n & 1);
+  const double tol = DEPS * (n > 16 ? sqrt((double)n) : 4.0);
+  for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
+    // exact column norms
+    for (int c = w; c < n; c += NWARP) {
+      double s = 0.0;
+      for (int i = lane; i < n; i += 32) { double a = A[i + c * lda]; s += a * a; }
+      s = warp_sum(s);
+      if (lane == 0) nrm[c] = s;
+    }
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < ne - 1; ++rnd) {
+      for (int k = w; k < ne / 2; k += NWARP) {
+        int i, j;
+        if (k == 0) { i = ne - 1; j = rnd; }
+        else { i = (rnd + k) % (ne - 1); j = (rnd - k + ne - 1) % (ne - 1); }
+        if (i >= n || j >= n) continue;
+        if (i > j) { int t = i; i = j; j = t; }
+        const double al = nrm[i], be = nrm[j];
+        double g = 0.0;
+        for (int l = lane; l < n; l += 32) g += A[l + i * lda] * A[l + j * lda];
+        g = warp_sum(g);
+        if (!(al > 0.0) || !(be > 0.0)) continue;
+        if (fabs(g) <= tol * sqrt(al) * sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * g);
+        double t;
+        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+        else t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int l = lane; l < n; l += 32) {
+          const double ai = A[l + i * lda], aj = A[l + j * lda];
+          A[l + i * lda] = c * ai - s * aj;
+          A[l + j * lda] = s * ai + c * aj;
+          const double vi = V[l + i * ldv], vj = V[l + j * ldv];
+          V[l + i * ldv] = c * vi - s * vj;
+          V[l + j * ldv] = s * vi + c * vj;
+        }
+        if (lane == 0) {
+          nrm[i] = al - t * g;
+          nrm[j] = be + t * g;
+          *flag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) break;
+    __syncthreads();
+  }
+  // final exact norms -> singular values
+  for (int c = w; c < n; c += NWARP) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) { double a = A[i + c * lda]; s += a * a; }
+    s = warp_sum(s);
+    if (lane == 0) nrm[c] = sqrt(s);
+  }
+  __syncthreads();
+  // stable descending order (ties by index)
+  for (int i = tid; i < n; i += NT) {
+    const double si = nrm[i];
+    int rk = 0;
+    for (int j = 0; j < n; ++j) {
+      const double sj = nrm[j];
+      if (sj > si || (sj == si && j < i)) ++rk;
+    }
+    perm[rk] = i;
+    s_sorted[rk] = si;
+  }
+  __syncthreads();
+}
+
+// Row range owned by CTA `cta` of `ncta` over `n` rows.
+__device__ __forceinline__ void row_range(int64_t n, int cta, int ncta, int64_t& r0, int64_t& r1) {
+  const int64_t per = (n + ncta - 1) / ncta;
+  r0 = per * cta;
+  r1 = r0 + per;
+  if (r0 > n) r0 = n;
+  if (r1 > n) r1 = n;
+}
+
+}  // namespace lrk
+
+namespace lrk {
+
+// ---------------------------------------------- warp-level Householder QR
+// Same contract as block_householder_qr, executed by ONE warp (no CTA
+// barriers).  Used for the small stacked-R level of the TSQR.
+__device__ inline void warp_householder_qr(double* X, int64_t ldx, int m, int q,
+                                           double* tau, double* Rout) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < q * q; i += 32) Rout[i] = 0.0;
+  __syncwarp();
+  const int kmax = m < q ? m : q;
+  for (int j = 0; j < kmax; ++j) {
+    double s = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) { double x = X[i + (int64_t)j * ldx]; s += x * x; }
+    const double sig = warp_sum(s);
+    const double alpha = X[j + (int64_t)j * ldx];
+    double beta, t, scale;
+    if (sig == 0.0) { t = 0.0; beta = alpha; scale = 0.0; }
+    else {
+      const double nrm = sqrt(alpha * alpha + sig);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    __syncwarp();
+    for (int i = j + 1 + lane; i < m; i += 32) X[i + (int64_t)j * ldx] *= scale;
+    __syncwarp();
+    double w[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) w[k] = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) {
+      const double vi = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int k = 0; k < PMAX; ++k)
+        if (k > j && k < q) w[k] += vi * X[i + (int64_t)k * ldx];
+    }
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k)
+      if (k > j && k < q) w[k] = warp_sum(w[k]);
+    for (int k = j + 1; k < q; ++k) {
+      const double f = t * (w[k] + X[j + (int64_t)k * ldx]);
+      for (int i = j + 1 + lane; i < m; i += 32) X[i + (int64_t)k * ldx] -= f * X[i + (int64_t)j * ldx];
+      __syncwarp();
+      if (lane == 0) { X[j + (int64_t)k * ldx] -= f; Rout[j * q + k] = X[j + (int64_t)k * ldx]; }
+      __syncwarp();
+    }
+    if (lane == 0) { Rout[j * q + j] = beta; X[j + (int64_t)j * ldx] = beta; tau[j] = t; }
+    __syncwarp();
+  }
+  for (int j = kmax + lane; j < q; j += 32) tau[j] = 0.0;
+  __syncwarp();
+}
+
+// Rows [row0, row0+nrow) of H_0 ... H_{kmax-1} [G; 0] (m x q), one warp,
+// G (q x q row-major).  Y: scratch m x q col-major (ldy); result rows copied
+// to out (nrow x q row-major).
+__device__ inline void warp_householder_q_rows(const double* X, int64_t ldx, int m, int q,
+                                               const double* tau, const double* G,
+                                               double* Y, int64_t ldy, int row0, int nrow,
+                                               double* out) {
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < q; ++c)
+    for (int i = lane; i < m; i += 32) Y[i + (int64_t)c * ldy] = (i < q) ? G[i * q + c] : 0.0;
+  __syncwarp();
+  const int kmax = m < q ? m : q;
+  for (int j = kmax - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;
+    double w[PMAX];
+#pragma unroll
+    for (int c = 0; c < PMAX; ++c) w[c] = 0.0;
+    for (int i = j + 1 + lane; i < m; i += 32) {
+      const double vi = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int c = 0; c < PMAX; ++c)
+        if (c < q) w[c] += vi * Y[i + (int64_t)c * ldy];
+    }
+#pragma unroll
+    for (int c = 0; c < PMAX; ++c)
+      if (c < q) w[c] = warp_sum(w[c]);
+    for (int c = 0; c < q; ++c) {
+      const double f = t * (w[c] + Y[j + (int64_t)c * ldy]);
+      for (int i = j + 1 + lane; i < m; i += 32) Y[i + (int64_t)c * ldy] -= f * X[i + (int64_t)j * ldx];
+      __syncwarp();
+      if (lane == 0) Y[j + (int64_t)c * ldy] -= f;
+      __syncwarp();
+    }
+  }
+  for (int idx = lane; idx < nrow * q; idx += 32) {
+    const int i = idx / q, c = idx % q;
+    out[idx] = Y[(row0 + i) + (int64_t)c * ldy];
+  }
+  __syncwarp();
+}
+
+}  // namespace lrk

@@ -1,0 +1,90 @@
+// lrk_kernels.h — host-visible kernel argument blocks and launchers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace lrk {
+
+// One low-rank sweep (forward.py:133-188) in the operator's eigenbasis.
+struct SweepArgs {
+  int64_t n_x;
+  int n_t;
+  int adjoint;
+  int p;            // compress_every
+  int r_max;        // < 0: none
+  double eps0;
+  const double* theta;     // n_x: eigenvalues of S^{-1} M
+  const double* rowscale;  // n_x or NULL: B~ = rowscale .* B
+  const double* B;         // n_x x rb (rhs spatial factor, eigenbasis)
+  int64_t ldb;
+  int rb;
+  const int* rb_dev;       // optional device rank of the rhs (rb = min(rb, *rb_dev))
+  const double* W2;        // n_t x rb (rhs time factor)
+  int64_t ldw2;
+  double* U0; double* U1; int64_t ldu;   // ping-pong pane bases, n_x x ucap
+  double* V0; double* V1; int64_t ldv;   // ping-pong time bases, n_t x ucap
+  int ucap;
+  double* sigma;           // ucap, output singular values
+  int* info;               // [0]=final rank, [1]=which buffer, [2]=error code
+  int* trace;              // nflush+1 ranks
+  double* ybuf; int64_t ldy;   // n_x x p
+  double* qbuf; int64_t ldq;   // n_x x p
+  double* yprev;               // n_x
+  double* part; int64_t pstride;  // 3 * ncta * pstride
+  double* scratch; int64_t scratch_stride;  // per-CTA
+  unsigned* bar;           // 2 unsigned per group
+  int ncta;
+};
+
+size_t sweep_smem_bytes();
+int64_t sweep_scratch_stride(int ncta);
+int64_t sweep_part_stride();
+cudaError_t launch_sweep(const SweepArgs* d_args, int ngroups, int ncta, cudaStream_t s);
+
+// General lr_truncate (lowrank.py:124-144) of W1 (n_x x R) W2^T (n_t x R).
+struct TruncArgs {
+  int64_t n_x;
+  int n_t;
+  int R;
+  const int* R_dev;  // optional device column count (R = min(R, *R_dev))
+  int flags;         // LRK_TRUNC_* bits
+  int r_max;
+  double eps0;
+  const double* W1; int64_t ld1;
+  const double* W2; int64_t ld2;
+  double* Q1; int64_t ldq1;   // workspace n_x x R
+  double* Q2; int64_t ldq2;   // workspace n_t x R
+  double* tmpw; int64_t ldtmp;  // workspace max(n_x,n_t) x PMAX
+  double* out1; int64_t ldo1; // n_x x cap
+  double* out2; int64_t ldo2; // n_t x cap
+  int cap;
+  double* sigma;              // cap (output singular values), may be NULL
+  double* sv_all;             // all R singular values (may be NULL)
+  int* info;                  // [0]=rank, [2]=error
+  double* part; int64_t pstride;
+  double* scratch; int64_t scratch_stride;
+  unsigned* bar;
+  int ncta;
+  int no_flip;                // skip _svd_flip
+};
+size_t trunc_smem_bytes();
+int64_t trunc_scratch_stride(int ncta);
+int64_t trunc_part_stride();
+cudaError_t launch_truncate(const TruncArgs* d_args, int ncta, cudaStream_t s);
+
+// fp64 batched GEMM: C[b] = alpha * A[b] B[b] + beta * C[b], all row-major.
+struct GemmArgs {
+  int M, N, K;
+  const double* A; int64_t lda; int64_t sA;
+  const double* B; int64_t ldb; int64_t sB;
+  double* C; int64_t ldc; int64_t sC;
+  double alpha, beta;
+  int batch;
+  const int* batch_dev;    // optional: batch = min(batch, *batch_dev)
+  const int* m_dev;        // optional: M = min(M, *m_dev * m_mult)
+  int m_mult;
+};
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s);
+
+}  // namespace lrk

@@ -1,0 +1,51 @@
+// lrk_misc.h — declarations of the streaming kernels in lrk_misc.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lrk {
+
+struct StencilArgs {
+  const double* X; int64_t ldx;
+  double* Y; int64_t ldy;
+  int n;          // n_side
+  int ncols;
+  double cc, cw, ce, cs, cn;  // (L x)_i coefficients (already transposed for adjoint)
+  double m_scale, tau;
+};
+
+__global__ void stencil_kernel(StencilArgs a);
+__global__ void shift_kernel(const double* W2, int64_t ld2, int n_t, int ncols, int adjoint,
+                             double* out, int64_t ldo, const double* W1, int64_t ld1,
+                             int64_t n_x, double neg_m, double* out1, int64_t ldo1);
+__global__ void scale_rows_kernel(const double* X, int64_t ldx, const double* s, int64_t n,
+                                  int ncols, const int* ncols_dev, double alpha, double* Y,
+                                  int64_t ldy);
+__global__ void scale_cols_kernel(const double* X, int64_t ldx, int64_t n, const double* colscale,
+                                  const int* ncols_dev, int ncols, double alpha, double* Y,
+                                  int64_t ldy);
+__global__ void column_eval_kernel(const double* U, int64_t ldu, int64_t n, const double* sigma,
+                                   const double* V, int64_t ldv, int row, const int* r_dev,
+                                   double* y);
+__global__ void gather_rows_kernel(const double* X, int64_t ldx, const int32_t* idx, int nidx,
+                                   const int* ncols_dev, int ncols, double* Y, int64_t ldy);
+__global__ void scatter_rows_kernel(const double* X, int64_t ldx, const int32_t* idx, int nidx,
+                                    const int* ncols_dev, int ncols, double* Y, int64_t ldy);
+__global__ void fill_kernel(double* X, int64_t ldx, int64_t n, int ncols, double v);
+__global__ void flip_partial_kernel(const double* U, int64_t ldu, int64_t n, const int* r_dev,
+                                    int rcap, double* part);
+__global__ void flip_apply_kernel(double* U, int64_t ldu, int64_t n_x, double* V, int64_t ldv,
+                                  int n_t, const int* r_dev, int rcap, const double* part,
+                                  int nparts);
+__global__ void gram_partial_kernel(const double* A, int64_t lda, int na, const double* B,
+                                    int64_t ldb, int nb, int64_t n, double* part);
+__global__ void dot_finalize_kernel(const double* p1, int n1, const double* p2, int n2, int nout,
+                                    double* out);
+__global__ void reduce_parts_kernel(const double* p, int nparts, int nout, double* out,
+                                    double* acc_out);
+__global__ void sub_qh_kernel(const double* Q, int64_t ldq, int k, const double* h, double* w,
+                              int64_t n);
+__global__ void combine_kernel(const double* Q, int64_t ldq, int k, const double* cf, double* y,
+                               int64_t n);
+
+}  // namespace lrk

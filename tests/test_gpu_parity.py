@@ -1,0 +1,313 @@
+"""GPU parity: the sm_100a path through the C ABI vs the reference's golden
+outputs (tests/golden) and the CPU oracle, on the same seeded inputs.
+
+Tolerances: floating point fp64.  The reference itself agrees with the dense
+brute force to 1e-8 (test_hessian.py:117-127); the device path computes the
+same truncations in an orthogonally equivalent basis, so we require much
+tighter agreement (1e-10 relative) where the inputs are identical and
+identical rank decisions.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1703_05638_b200 as lp  # noqa: E402
+from oracle import lrk_oracle as O  # noqa: E402
+
+POL = lp.TruncationPolicy(1e-8)
+
+
+def _dense(A):
+    return lp.lr_to_dense(A)
+
+
+def _rmax(v):
+    return None if v < 0 else int(v)
+
+
+# ------------------------------------------------------------ factor algebra
+@pytest.mark.parametrize("name", ["trunc_a", "trunc_b", "trunc_c", "trunc_d"])
+def test_truncate_vs_reference(golden, name):
+    eps0, rmax = golden[f"{name}_meta"]
+    A = lp.LowRankMat(golden[f"{name}_W1"], golden[f"{name}_W2"])
+    B = lp.lr_truncate(A, lp.TruncationPolicy(eps0, _rmax(rmax)))
+    U, V = golden[f"{name}_U"], golden[f"{name}_V"]
+    assert B.r == U.shape[1]
+    ref = U @ V.T
+    assert np.linalg.norm(_dense(B) - ref) <= 1e-12 * np.linalg.norm(ref)
+    # canonical form: same factors as the reference (sign convention included)
+    np.testing.assert_allclose(B.W1.cpu().numpy(), U, atol=1e-9)
+
+
+def test_truncate_contract_and_canonical_form():
+    rng = np.random.default_rng(2)
+    for eps0 in (1e-2, 1e-5, 1e-8):
+        for n, m, r in [(200, 150, 40), (60, 200, 25), (35, 35, 35)]:
+            W1 = rng.standard_normal((n, r)) * np.logspace(0, -9, r)
+            A = lp.LowRankMat(W1, rng.standard_normal((m, r)))
+            out = lp.lr_truncate(A, lp.TruncationPolicy(eps0))
+            err = np.linalg.norm(_dense(A) - _dense(out))
+            assert err <= eps0 * lp.lr_norm(A) * (1 + 1e-12)
+            Q = out.W1.cpu().numpy()
+            np.testing.assert_allclose(Q.T @ Q, np.eye(out.r), atol=1e-13)
+
+
+def test_truncate_edge_cases():
+    z = lp.LowRankMat(np.zeros((10, 2)), np.zeros((8, 2)))
+    assert lp.lr_truncate(z, POL).r == 0
+    rng = np.random.default_rng(7)
+    A = lp.LowRankMat(rng.standard_normal((20, 2)), rng.standard_normal((15, 2)))
+    assert lp.lr_truncate(lp.lr_add(A, lp.lr_scale(A, -1.0)), POL).r == 0
+    w = rng.standard_normal((20, 1))
+    B = lp.lr_add(lp.LowRankMat(w, rng.standard_normal((15, 1))),
+                  lp.LowRankMat(w, rng.standard_normal((15, 1))))
+    assert lp.lr_truncate(B, POL).r == 1
+    C = lp.LowRankMat(rng.standard_normal((30, 10)), rng.standard_normal((30, 10)))
+    assert lp.lr_truncate(C, lp.TruncationPolicy(1e-12, 4)).r == 4
+    # u vᵀ + 1e-12 p qᵀ: exactly one survivor (test_lowrank.py:47-57)
+    u = np.zeros((12, 2)); u[0, 0] = 1; u[1, 1] = 1e-12
+    v = np.zeros((9, 2)); v[0, 0] = 1; v[1, 1] = 1
+    assert lp.lr_truncate(lp.LowRankMat(u, v), POL).r == 1
+
+
+def test_dot_norm_singular_values_vs_oracle():
+    rng = np.random.default_rng(9)
+    for (n, m, ra, rb) in [(30, 22, 2, 2), (4097, 33, 5, 7), (65536, 512, 12, 16)]:
+        A = (rng.standard_normal((n, ra)), rng.standard_normal((m, ra)))
+        B = (rng.standard_normal((n, rb)), rng.standard_normal((m, rb)))
+        got = lp.lr_dot(lp.LowRankMat(*A), lp.LowRankMat(*B))
+        ref = O.dot(A, B)
+        assert abs(got - ref) <= 1e-12 * (abs(ref) + O.norm(A) * O.norm(B))
+    A = (rng.standard_normal((26, 5)), rng.standard_normal((19, 5)))
+    np.testing.assert_allclose(lp.lr_singular_values(lp.LowRankMat(*A)), O.singular_values(A),
+                               rtol=1e-11)
+
+
+# ------------------------------------------------------------ space-time operator
+def _heat(n_side, n_t):
+    grid = lp.build_grid(n_side)
+    return grid, lp.SpaceTimeOperator(lp.assemble_heat(grid), lp.build_time_grid(n_t))
+
+
+def test_stencil_apply_is_the_dense_operator():
+    """test_forward.py:104-116 on the device SpMM (heat and convdiff)."""
+    rng = np.random.default_rng(4)
+    for op in (lp.assemble_heat(lp.build_grid(7)),
+               lp.assemble_convdiff(lp.build_grid(9), 1e-2, (0.3, -1.0))):
+        K = lp.SpaceTimeOperator(op, lp.build_time_grid(5))
+        Y = lp.LowRankMat(rng.standard_normal((op.grid.n_x, 3)), rng.standard_normal((5, 3)))
+        Yd = _dense(Y)
+        A = K.step_matrix.toarray()
+        ref = A @ Yd
+        ref[:, 1:] -= op.grid.m_scale * Yd[:, :-1]
+        assert np.abs(_dense(K.apply(Y)) - ref).max() < 1e-12 * np.abs(ref).max()
+        ref_t = A.T @ Yd
+        ref_t[:, :-1] -= op.grid.m_scale * Yd[:, 1:]
+        assert np.abs(_dense(K.apply_adjoint(Y)) - ref_t).max() < 1e-12 * np.abs(ref_t).max()
+
+
+def test_step_solve_vs_superlu():
+    grid, K = _heat(31, 8)
+    L, h, m = O.fd_operator(31)
+    solver = O.StepSolver(L, m, 1.0 / 8, 8)
+    B = np.random.default_rng(3).standard_normal((grid.n_x, 4))
+    np.testing.assert_allclose(K.solve_step(B), solver.solve(B), rtol=1e-11,
+                               atol=1e-11 * np.abs(solver.solve(B)).max())
+
+
+@pytest.mark.parametrize("name", ["sweep_a", "sweep_b", "sweep_c", "sweep_d"])
+def test_sweep_vs_reference(golden, name):
+    n_side, n_t, adjoint = (int(x) for x in golden[f"{name}_meta"])
+    _, K = _heat(n_side, n_t)
+    rhs = lp.LowRankMat(golden[f"{name}_R1"], golden[f"{name}_R2"])
+    tr = []
+    Y = lp.st_solve_sweep(K, rhs, POL, adjoint=bool(adjoint), trace=tr)
+    assert tr == golden[f"{name}_trace"].tolist()
+    ref = golden[f"{name}_Y1"] @ golden[f"{name}_Y2"].T
+    assert np.linalg.norm(_dense(Y) - ref) <= 1e-11 * np.linalg.norm(ref)
+    np.testing.assert_allclose(Y.W1.cpu().numpy(), golden[f"{name}_Y1"], atol=1e-8)
+
+
+def test_sweep_eigvec_decay_at_config_scale():
+    """Size-independent closed form (test_forward.py:40-48) at the C2 grid: y_k = θ^k v."""
+    n_side, n_t = 256, 512
+    grid, K = _heat(n_side, n_t)
+    v = lp.eigvec_dense(3, 2, grid)
+    Y = lp.st_solve_sweep(K, v, POL)
+    assert Y.r == 1
+    theta = 1.0 / (1.0 + K.time.tau * lp.discrete_fd_eig(3, 2, grid))
+    W2 = Y.W2.cpu().numpy()[:, 0]
+    W1 = Y.W1.cpu().numpy()[:, 0]
+    expect = theta ** np.arange(1, n_t + 1)
+    s = np.dot(W1, v)
+    np.testing.assert_allclose(W2 * s, expect, rtol=1e-10, atol=1e-14)
+
+
+def test_sweep_zero_rhs_and_shape_errors():
+    grid, K = _heat(7, 5)
+    assert lp.st_solve_sweep(K, lp.LowRankMat.zeros(grid.n_x, 5), POL).r == 0
+    with pytest.raises(ValueError):
+        lp.st_solve_sweep(K, lp.LowRankMat.zeros(grid.n_x, 6), POL)
+
+
+def test_adjoint_consistency_random_fields():
+    """test_forward.py:78-85."""
+    grid, K = _heat(15, 9)
+    rng = np.random.default_rng(2)
+    a = lp.lr_truncate(lp.LowRankMat(rng.standard_normal((grid.n_x, 2)), rng.standard_normal((9, 2))), POL)
+    b = lp.lr_truncate(lp.LowRankMat(rng.standard_normal((grid.n_x, 2)), rng.standard_normal((9, 2))), POL)
+    lhs = lp.lr_dot(lp.st_solve_sweep(K, a, POL), b)
+    rhs = lp.lr_dot(a, lp.st_solve_adjoint_sweep(K, b, POL))
+    assert abs(lhs - rhs) <= 1e-8 * abs(rhs)
+
+
+def test_gmres_vs_reference(golden):
+    _, K = _heat(15, 10)
+    rhs = lp.LowRankMat(golden["gmres_R1"], golden["gmres_R2"])
+    tr = []
+    Y = lp.st_solve_krylov(K, rhs, POL, trace=tr)
+    assert abs(len(tr) - int(golden["gmres_iters"][0])) <= 1  # north_star: iterations +-1
+    ref = golden["gmres_Y"]
+    assert np.linalg.norm(_dense(Y) - ref) <= 1e-8 * np.linalg.norm(ref)
+
+
+# ------------------------------------------------------------------ Hessian
+def _ic_ctx(meta, mask, pol=None):
+    n_side, n_t, bn, bp, g, rmax = meta
+    grid, K = _heat(int(n_side), int(n_t))
+    cov = lp.CovarianceSpec(bn, bp, g)
+    layout = lp.SensorLayout(patches=(), mask=mask.astype(bool))
+    pol = pol or lp.TruncationPolicy(1e-8, _rmax(rmax))
+    return lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=pol)
+
+
+@pytest.mark.parametrize("name", ["hic_a", "hic_b", "hic_c", "hic_d"])
+def test_hessian_ic_vs_reference(golden, name):
+    ctx = _ic_ctx(golden[f"{name}_meta"], golden[f"{name}_mask"])
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    for j in range(V.shape[1]):
+        out = ctx.apply(V[:, j])
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-10 * np.linalg.norm(Oref[:, j])
+    assert ctx.rank_trace == golden[f"{name}_ranks"].tolist()
+
+
+def test_hessian_ic_batch_equals_single(golden):
+    ctx = _ic_ctx(golden["hic_b_meta"], golden["hic_b_mask"])
+    V = golden["hic_b_V"]
+    out = ctx.apply_batch(V).cpu().numpy()
+    for j in range(V.shape[1]):
+        assert np.linalg.norm(out[:, j] - golden["hic_b_O"][:, j]) <= 1e-10 * np.linalg.norm(out[:, j])
+
+
+def test_hessian_source_vs_reference(golden):
+    n_side, n_t, bn, bp, g = golden["hst_meta"]
+    grid, K = _heat(int(n_side), int(n_t))
+    ctx = lp.HessianContext(mode="source", operator=K, layout=lp.full_observation(grid),
+                            cov=lp.CovarianceSpec(bn, bp, g), pol=POL)
+    out = ctx.apply(lp.LowRankMat(golden["hst_V1"], golden["hst_V2"]))
+    ref = golden["hst_O"]
+    assert np.linalg.norm(_dense(out) - ref) <= 1e-10 * np.linalg.norm(ref)
+    assert ctx.rank_trace == golden["hst_ranks"].tolist()
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 1), (5, 3)])
+def test_full_obs_ic_eigenpairs_at_config_scale(m, n):
+    """μ = γ β τ M Σθ^{2k} (test_hessian.py:129-139) at the C2 grid (256², n_t 512)."""
+    n_side, n_t = 256, 512
+    grid, K = _heat(n_side, n_t)
+    cov = lp.CovarianceSpec.from_gamma(0.05, 1e6, grid)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.full_observation(grid), cov=cov, pol=POL)
+    v = lp.eigvec_dense(m, n, grid)
+    out = ctx.apply(v)
+    mu = O.ic_eigenvalue_full_obs(m, n, n_side, n_t, cov.beta_noise, cov.gamma_prior)
+    assert np.linalg.norm(out - mu * v) <= 1e-8 * mu
+
+
+def test_hessian_ic_subgrid_vs_oracle_mid_size():
+    """C2-shaped operator at reduced size (64², n_t 128, 8x8 point sensors)."""
+    n_side, n_t = 64, 128
+    grid, K = _heat(n_side, n_t)
+    layout = lp.make_sensor_subgrid(grid, 8)
+    cov = lp.CovarianceSpec.from_gamma(0.05, 1e6, grid)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=POL)
+    P = O.Problem(n_side, n_t, layout.mask, cov.beta_noise, cov.gamma_prior)
+    rng = np.random.default_rng(11)
+    for _ in range(2):
+        v = rng.standard_normal(grid.n_x)
+        ref, r = O.hessian_ic(P, v)
+        out = ctx.apply(v)
+        assert np.linalg.norm(out - ref) <= 1e-10 * np.linalg.norm(ref)
+        assert ctx.rank_trace[-1] == r
+
+
+def test_hessian_self_adjoint_psd_and_zero():
+    grid, K = _heat(15, 10)
+    cov = lp.CovarianceSpec.from_gamma(10.0, 1e4, grid)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.make_sensor_layout_3x3(grid),
+                            cov=cov, pol=POL)
+    rng = np.random.default_rng(6)
+    u, w = rng.standard_normal((2, grid.n_x))
+    Hu, Hw = ctx.apply(u), ctx.apply(w)
+    assert abs(Hu @ w - u @ Hw) <= 1e-6 * np.linalg.norm(Hu) * np.linalg.norm(w)
+    assert u @ Hu >= -1e-10 * (u @ u)
+    assert np.linalg.norm(ctx.apply(np.zeros(grid.n_x))) == 0.0
+    empty = lp.HessianContext(mode="ic", operator=K, layout=lp.SensorLayout((), np.zeros(grid.n_x, bool)),
+                              cov=cov, pol=POL)
+    assert np.linalg.norm(empty.apply(u)) == 0.0
+
+
+def test_steady_poisson_eigenpair():
+    grid = lp.build_grid(15)
+    op = lp.assemble_heat(grid)
+    cov = lp.CovarianceSpec(beta_noise=1e4, beta_prior=1.0, gamma_prior=1.0)
+    for m, n in [(1, 1), (3, 2)]:
+        v = lp.eigvec_dense(m, n, grid)
+        mu = 1e-4 / lp.discrete_fd_eig(m, n, grid) ** 2
+        out = lp.steady_poisson_apply(v, cov, op)
+        assert np.linalg.norm(out - mu * v) <= 1e-10 * mu
+
+
+# ------------------------------------------------------------- Arnoldi / posterior
+def test_arnoldi_and_variance_vs_reference(golden):
+    n_side, n_t, bn, bp, g, m_a = golden["arn_meta"]
+    grid, K = _heat(int(n_side), int(n_t))
+    ctx = lp.HessianContext(mode="ic", operator=K,
+                            layout=lp.SensorLayout((), golden["arn_mask"].astype(bool)),
+                            cov=lp.CovarianceSpec(bn, bp, g), pol=POL)
+    res = lp.lr_arnoldi(ctx.apply, golden["arn_v1"], POL, lp.StopRule(m_a=int(m_a), eps_eig=1e-1),
+                        rank_source=ctx.rank_trace)
+    assert abs(res.iterations - int(golden["arn_iters"][0])) <= 1
+    ref = golden["arn_ritz"]
+    lead = ref >= 1e-1
+    got = res.ritz_values.real[: lead.sum()]
+    np.testing.assert_allclose(got, ref[lead], rtol=1e-6)  # north_star: eigenvalues 1e-6
+    summ = lp.build_summary(res.ritz_values, res.ritz_vectors, g, 1e-1)
+    np.testing.assert_allclose(summ.variance_field, golden["arn_var"], rtol=1e-5)  # variance 1e-5
+    assert res.gram_defect() <= 1e-6
+
+
+def test_arnoldi_low_rank_mode_orthogonality():
+    grid, K = _heat(9, 6)
+    cov = lp.CovarianceSpec.from_gamma(10.0, 1e4, grid)
+    ctx = lp.HessianContext(mode="source", operator=K, layout=lp.full_observation(grid), cov=cov, pol=POL)
+    v1 = lp.LowRankMat(np.ones((grid.n_x, 1)), np.ones((6, 1)))
+    res = lp.lr_arnoldi(ctx.apply, v1, POL, lp.StopRule(m_a=10, eps_eig=1e-14, check_every=100),
+                        rank_source=ctx.rank_trace)
+    assert res.gram_defect() <= 1e-6
+    for v in res.basis:
+        assert abs(lp.lr_norm(v) - 1.0) <= 1e-7
+
+
+def test_diagonal_operator_arnoldi_numpy_callable():
+    d = np.array([3.0, 2.0, 1.0, 0.5, 0.25])
+    res = lp.lr_arnoldi(lambda x: d * x, np.ones(5) / np.sqrt(5), POL,
+                        lp.StopRule(m_a=5, eps_eig=1e-12, check_every=100))
+    np.testing.assert_allclose(np.sort(res.ritz_values.real)[::-1], d, rtol=1e-10)

@@ -1,0 +1,114 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden) and
+the reference's closed-form known answers.  CPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import lrk_oracle as O
+
+
+def _rmax(v):
+    return None if v < 0 else int(v)
+
+
+@pytest.mark.parametrize("name", ["trunc_a", "trunc_b", "trunc_c", "trunc_d"])
+def test_truncate_matches_reference(golden, name):
+    eps0, rmax = golden[f"{name}_meta"]
+    U, V = O.truncate(golden[f"{name}_W1"], golden[f"{name}_W2"], eps0, _rmax(rmax))
+    assert U.shape == golden[f"{name}_U"].shape
+    np.testing.assert_allclose(U, golden[f"{name}_U"], atol=1e-12)
+    np.testing.assert_allclose(V, golden[f"{name}_V"], rtol=1e-12, atol=1e-12 * np.abs(V).max())
+
+
+@pytest.mark.parametrize("name", ["sweep_a", "sweep_b", "sweep_c", "sweep_d"])
+def test_sweep_matches_reference(golden, name):
+    n_side, n_t, adjoint = (int(x) for x in golden[f"{name}_meta"])
+    L, h, m = O.fd_operator(n_side)
+    solver = O.StepSolver(L, m, 1.0 / n_t, n_t)
+    Y1, Y2, tr = O.sweep(solver, golden[f"{name}_R1"], golden[f"{name}_R2"], 1e-8, None,
+                         bool(adjoint))
+    assert tr == golden[f"{name}_trace"].tolist()
+    ref = golden[f"{name}_Y1"] @ golden[f"{name}_Y2"].T
+    assert np.linalg.norm(Y1 @ Y2.T - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_gmres_matches_reference(golden):
+    L, h, m = O.fd_operator(15)
+    solver = O.StepSolver(L, m, 0.1, 10)
+    (Y1, Y2), iters, tr = O.gmres(solver, golden["gmres_R1"], golden["gmres_R2"], 1e-8)
+    assert iters == int(golden["gmres_iters"][0])
+    ref = golden["gmres_Y"]
+    assert np.linalg.norm(Y1 @ Y2.T - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("name", ["hic_a", "hic_b", "hic_c", "hic_d"])
+def test_hessian_ic_matches_reference(golden, name):
+    n_side, n_t, bn, bp, g, rmax = golden[f"{name}_meta"]
+    P = O.Problem(int(n_side), int(n_t), golden[f"{name}_mask"], bn, g, 1e-8, _rmax(rmax))
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    ranks = []
+    for j in range(V.shape[1]):
+        out, r = O.hessian_ic(P, V[:, j])
+        ranks.append(r)
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-12 * np.linalg.norm(Oref[:, j])
+    assert ranks == golden[f"{name}_ranks"].tolist()
+
+
+def test_hessian_source_matches_reference(golden):
+    n_side, n_t, bn, bp, g = golden["hst_meta"]
+    P = O.Problem(int(n_side), int(n_t), np.ones(int(n_side) ** 2, bool), bn, g)
+    (W1, W2), r = O.hessian_st(P, golden["hst_V1"], golden["hst_V2"])
+    ref = golden["hst_O"]
+    assert np.linalg.norm(W1 @ W2.T - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert r == int(golden["hst_ranks"][0])
+
+
+def test_arnoldi_and_variance_match_reference(golden):
+    n_side, n_t, bn, bp, g, m_a = golden["arn_meta"]
+    P = O.Problem(int(n_side), int(n_t), golden["arn_mask"], bn, g)
+    H, basis, vals, iters = O.arnoldi_dense(lambda x: O.hessian_ic(P, x)[0], golden["arn_v1"],
+                                            int(m_a))
+    assert iters == int(golden["arn_iters"][0])
+    ref = golden["arn_ritz"]
+    lead = ref >= 1e-1
+    np.testing.assert_allclose(vals.real[lead], ref[lead], rtol=1e-10)
+    rv, vecs = O.ritz_vectors(H, basis)
+    var = O.posterior_variance(rv, vecs, g, 1e-1)
+    np.testing.assert_allclose(var, golden["arn_var"], rtol=1e-10)
+
+
+# ---- closed-form known answers used by the reference's own tests
+def test_eigvec_injection_geometric_decay():
+    """test_forward.py:40-48: y_k = θ^k v for an FD eigenvector."""
+    n_side, n_t = 7, 5
+    L, h, m = O.fd_operator(n_side)
+    solver = O.StepSolver(L, m, 1.0 / n_t, n_t)
+    v = O.fd_eigvec(1, 1, n_side)
+    e0 = np.zeros((n_t, 1)); e0[0] = 1
+    Y1, Y2, _ = O.sweep(solver, (m * v)[:, None], e0, 1e-8)
+    theta = 1.0 / (1.0 + O.fd_eig(1, 1, n_side) / n_t)
+    expect = np.column_stack([theta ** k * v for k in range(1, n_t + 1)])
+    assert np.abs(Y1 @ Y2.T - expect).max() <= 1e-10
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 1), (3, 3)])
+def test_full_observation_ic_eigenvalue(m, n):
+    """test_hessian.py:129-139: μ = γ β τ M Σ θ^{2k}."""
+    n_side, n_t = 7, 5
+    h = 1.0 / (n_side + 1)
+    gamma, ratio = 10.0, 1e4
+    beta_prior = 1.0 / (gamma * h * h)
+    P = O.Problem(n_side, n_t, np.ones(n_side ** 2, bool), ratio * beta_prior, gamma)
+    v = O.fd_eigvec(m, n, n_side)
+    out, _ = O.hessian_ic(P, v)
+    mu = O.ic_eigenvalue_full_obs(m, n, n_side, n_t, ratio * beta_prior, gamma)
+    assert np.linalg.norm(out - mu * v) <= 1e-8 * mu
+
+
+def test_rank_cut_semantics():
+    assert O.rank_cut(np.array([1.0, 1e-12]), 1e-8) == 1
+    assert O.rank_cut(np.array([1.0, 0.5, 0.1]), 1e-8, r_max=2) == 2
+    assert O.rank_cut(np.zeros(3), 1e-8) == 0
+    assert O.rank_cut(np.array([1.0, 1e-16]), 1e-20) == 1  # noise floor
