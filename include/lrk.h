@@ -171,6 +171,17 @@ int lrk_combine(lrk_ctx* ctx, const double* Q, int64_t ldq, int k,
 /* Number of device kernels this context has launched (instrumentation). */
 int64_t lrk_launch_count(const lrk_ctx* ctx);
 
+/* Instrumentation for the roofline: when enabled, every sweep launch is
+ * bracketed by CUDA events on its stream and its algorithmic bytes (DESIGN.md
+ * §Roofline) are accumulated once the apply's ranks are known. */
+int lrk_profile_enable(lrk_ctx* ctx, int enable);
+int lrk_profile_read(lrk_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,
+                     double* sweep_alg_bytes, int reset);
+/* Rank traces of the last Hessian apply: forward and adjoint sweeps (pane
+ * rank after every flush + final) and the observation rank. */
+int lrk_last_traces(lrk_ctx* ctx, int* fwd, int* bwd, int cap, int* n_fwd,
+                    int* n_bwd, int* obs_rank);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,11 @@ _SIGNATURES = {
     "lrk_ctx_destroy": (None, [c_void_p]),
     "lrk_last_error": (c_char_p, [c_void_p]),
     "lrk_launch_count": (c_int64, [c_void_p]),
+    "lrk_profile_enable": (c_int, [c_void_p, c_int]),
+    "lrk_profile_read": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), POINTER(c_double),
+                                 c_int]),
+    "lrk_last_traces": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), c_int, POINTER(c_int),
+                                POINTER(c_int), POINTER(c_int)]),
     "lrk_set_operator": (c_int, [c_void_p, POINTER(lrk_operator_desc)]),
     "lrk_set_observation": (c_int, [c_void_p, POINTER(lrk_obs_desc)]),
     "lrk_truncate": (c_int, [c_void_p, POINTER(lrk_lr), POINTER(lrk_lr), c_double, c_int, c_int,

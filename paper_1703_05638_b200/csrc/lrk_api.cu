@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -29,6 +30,7 @@ struct Buf {
 struct lrk_ctx {
   int device = 0;
   int num_sms = 148;
+  int smem_optin = 227 * 1024;
   std::string err;
   int64_t launches = 0;
   // operator
@@ -48,7 +50,15 @@ struct lrk_ctx {
   int32_t* dList = nullptr;
   double *dS1T = nullptr, *dS2 = nullptr, *dS1 = nullptr, *dS2T = nullptr;
   std::map<std::string, Buf> ws;
+  // instrumentation
+  bool prof = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double prof_ms = 0.0, prof_bytes = 0.0;
+  int64_t prof_n = 0;
+  std::vector<int> last_fwd, last_bwd;
+  int last_obs = 0;
   ~lrk_ctx() {
+    for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (auto& kv : ws) cudaFree(kv.second.p);
     cudaFree(dS); cudaFree(dTheta); cudaFree(dThetaM); cudaFree(dE0); cudaFree(dInvLam);
     cudaFree(dList); cudaFree(dS1T); cudaFree(dS2); cudaFree(dS1); cudaFree(dS2T);
@@ -186,6 +196,7 @@ struct SweepOut {
   int ucap = 0;
   int nflush = 0;
   int64_t ldu = 0, ldv = 0;
+  long long* dbg = nullptr;
 };
 
 int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, int rb,
@@ -213,8 +224,9 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   const int64_t sst = sweep_scratch_stride(ncta);
   WS(double, scratch, "sw_scratch", (int64_t)ncta * sst);
   WS(unsigned, bar, "sw_bar", 4);
-  WS(SweepArgs, dargs, tag + "args", 1);
-  SweepArgs a{};
+  SweepBatch batch{};
+  batch.ngroups = 1;
+  SweepArgs& a = batch.g[0];
   a.n_x = nx; a.n_t = nt; a.adjoint = adjoint; a.p = p; a.r_max = r_max; a.eps0 = eps0;
   a.theta = c->dTheta; a.rowscale = c->dThetaM;
   a.B = B; a.ldb = ldb; a.rb = rb; a.rb_dev = rb_dev;
@@ -224,9 +236,16 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   a.ybuf = ybuf; a.ldy = nx; a.qbuf = qbuf; a.ldq = nx; a.yprev = yprev;
   a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
   a.bar = bar; a.ncta = ncta;
-  CK(cudaMemcpyAsync(dargs, &a, sizeof(a), cudaMemcpyHostToDevice, s));
+  sweep_plan(a, nx, ncta, ucap, p, (size_t)c->smem_optin);
+  a.ftz = std::getenv("LRK_FTZ") ? std::atof(std::getenv("LRK_FTZ")) : 0.0;
+  WS(long long, dbg, tag + "dbg", 16);
+  a.dbg = std::getenv("LRK_DEBUG") ? dbg : nullptr;
+  o.dbg = dbg;
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
-  CK(launch_sweep(dargs, 1, ncta, s));
+  const int slot = adjoint ? 1 : 0;
+  if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
+  CK(launch_sweep(batch, s));
+  if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
   ++c->launches;
   o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
   o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
@@ -257,7 +276,6 @@ int run_truncate(lrk_ctx* c, const std::string& tag, int64_t n_x, int n_t, const
   WS(double, scratch, "tr_scratch", (int64_t)ncta * sst);
   WS(unsigned, bar, "tr_bar", 4);
   WS(int, info, tag + "info", 8);
-  WS(TruncArgs, dargs, tag + "args", 1);
   TruncArgs a{};
   a.n_x = n_x; a.n_t = n_t; a.R = R; a.R_dev = R_dev; a.flags = flags; a.r_max = r_max; a.eps0 = eps0;
   a.W1 = W1; a.ld1 = ld1; a.W2 = W2; a.ld2 = ld2;
@@ -267,9 +285,8 @@ int run_truncate(lrk_ctx* c, const std::string& tag, int64_t n_x, int n_t, const
   a.sigma = sigma; a.sv_all = sv_all; a.info = info;
   a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
   a.bar = bar; a.ncta = ncta; a.no_flip = no_flip;
-  CK(cudaMemcpyAsync(dargs, &a, sizeof(a), cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
-  CK(launch_truncate(dargs, ncta, s));
+  CK(launch_truncate(a, s));
   ++c->launches;
   o.info = info;
   return LRK_OK;
@@ -360,8 +377,28 @@ int hd_check(lrk_ctx* c, const lrk_hessian_desc* hd) {
   return LRK_OK;
 }
 
+// Algorithmic (compulsory) bytes of one sweep, from its rank trace (DESIGN.md
+// §Roofline): per step 16 n_x for the recurrence + 16 n_x for
+// one ideal pass of the spatial solve + 8 n_x r_B where the rhs time factor
+// is nonzero; per flush 8 n_x R (Gram) + 8 n_x R + 8 n_x r' (basis update),
+// R = r_prev + pc.
+double sweep_alg_bytes(int64_t n_x, int n_t, int p, const std::vector<int>& tr, int rb,
+                       int nnz_steps) {
+  double b = 32.0 * n_x * n_t + 8.0 * n_x * rb * nnz_steps;
+  const int nflush = (n_t + p - 1) / p;
+  for (int f = 0; f < nflush && f < (int)tr.size(); ++f) {
+    const int rprev = f ? tr[f - 1] : 0;
+    const int pc = std::min(p, n_t - f * p);
+    const int R = rprev + pc;
+    b += 8.0 * n_x * (2.0 * R + tr[f]);
+  }
+  return b;
+}
+
+// Reads back the ranks of one apply (the only sync of an apply), derives
+// max_rank (hessian.py:225) and, when profiling, the sweep timings/bytes.
 int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOut& g,
-                  const int* extra_info, int* out, cudaStream_t s) {
+                  const int* extra_info, int* out, int p, int rb_f, int nnz_f, cudaStream_t s) {
   std::vector<int> t1(f.nflush + 1), t2(g.nflush + 1);
   int zr[8] = {0}, er[8] = {0};
   CK(cudaMemcpyAsync(t1.data(), f.trace, t1.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -374,6 +411,37 @@ int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOu
   for (int v : t2) m = std::max(m, v);
   if (extra_info) m = std::max(m, er[0]);
   *out = m;
+  c->last_fwd = t1;
+  c->last_bwd = t2;
+  c->last_obs = zr[0];
+  if (std::getenv("LRK_DEBUG")) {
+    int fi[8], gi[8];
+    CK(cudaMemcpy(fi, f.info, sizeof(fi), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(gi, g.info, sizeof(gi), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[lrk] apply: ranks fwd %d obs %d bwd %d; jacobi sweeps fwd %d bwd %d over %d+%d flushes\n",
+                 fi[0], zr[0], gi[0], fi[3], gi[3], f.nflush, g.nflush);
+    long long fd[16], gd[16];
+    CK(cudaMemcpy(fd, f.dbg, sizeof(fd), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(gd, g.dbg, sizeof(gd), cudaMemcpyDeviceToHost));
+    const char* names[13] = {"gen+proj1", "barrier1", "reduce2+sub2", "hh_local", "barrier3",
+                             "stackQR", "apply_q", "core+jacobi", "update", "reduce1",
+                             "sub1+tn2", "barrier2", "rankcut"};
+    std::fprintf(stderr, "[lrk] cycles/flush (fwd | bwd):");
+    for (int k = 0; k < 13; ++k)
+      std::fprintf(stderr, " %s %lld|%lld", names[k], fd[k] / std::max(1, f.nflush),
+                   gd[k] / std::max(1, g.nflush));
+    std::fprintf(stderr, "\n");
+  }
+  if (c->prof) {
+    float ms0 = 0.f, ms1 = 0.f;
+    CK(cudaEventElapsedTime(&ms0, c->ev[0], c->ev[1]));
+    CK(cudaEventElapsedTime(&ms1, c->ev[2], c->ev[3]));
+    c->prof_ms += (double)ms0 + (double)ms1;
+    c->prof_n += 2;
+    const int nt = c->op.n_t;
+    c->prof_bytes += sweep_alg_bytes(c->n_x, nt, p, t1, rb_f, nnz_f) +
+                     sweep_alg_bytes(c->n_x, nt, p, t2, zr[0], nt);
+  }
   return LRK_OK;
 }
 
@@ -391,6 +459,7 @@ int lrk_ctx_create(int device, lrk_ctx** out) {
   lrk_ctx* c = new lrk_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   *out = c;
   return LRK_OK;
 }
@@ -405,6 +474,38 @@ void lrk_ctx_destroy(lrk_ctx* c) {
 const char* lrk_last_error(const lrk_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int64_t lrk_launch_count(const lrk_ctx* c) { return c ? c->launches : 0; }
+
+int lrk_profile_enable(lrk_ctx* c, int enable) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  if (enable && !c->ev[0])
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  c->prof = enable != 0;
+  return LRK_OK;
+}
+
+int lrk_profile_read(lrk_ctx* c, double* sweep_ms, int64_t* sweep_launches,
+                     double* sweep_alg_bytes_out, int reset) {
+  if (!c) return LRK_ERR_CONFIG;
+  if (sweep_ms) *sweep_ms = c->prof_ms;
+  if (sweep_launches) *sweep_launches = c->prof_n;
+  if (sweep_alg_bytes_out) *sweep_alg_bytes_out = c->prof_bytes;
+  if (reset) { c->prof_ms = 0.0; c->prof_n = 0; c->prof_bytes = 0.0; }
+  return LRK_OK;
+}
+
+int lrk_last_traces(lrk_ctx* c, int* fwd, int* bwd, int cap, int* n_fwd, int* n_bwd,
+                    int* obs_rank) {
+  if (!c) return LRK_ERR_CONFIG;
+  const int nf = std::min<int>(cap, (int)c->last_fwd.size());
+  const int nb = std::min<int>(cap, (int)c->last_bwd.size());
+  for (int i = 0; i < nf; ++i) fwd[i] = c->last_fwd[i];
+  for (int i = 0; i < nb; ++i) bwd[i] = c->last_bwd[i];
+  if (n_fwd) *n_fwd = nf;
+  if (n_bwd) *n_bwd = nb;
+  if (obs_rank) *obs_rank = c->last_obs;
+  return LRK_OK;
+}
 
 int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
   if (!c || !op) return LRK_ERR_CONFIG;
@@ -715,7 +816,9 @@ int lrk_hessian_apply_ic(lrk_ctx* c, const lrk_hessian_desc* hd, int nbatch, con
                                                               bw.ldv, 0, bw.info, q);
     CKL();
     TRY(dst2(c, q, nx, out, nx, 1, nullptr, sg * M, s));
-    if (max_rank) TRY(host_max_rank(c, fw, zinfo, bw, nullptr, &max_rank[b], s));
+    int mr = 0;
+    TRY(host_max_rank(c, fw, zinfo, bw, nullptr, &mr, hd->compress_every, 1, 1, s));
+    if (max_rank) max_rank[b] = mr;
   }
   return LRK_OK;
 }
@@ -759,7 +862,7 @@ int lrk_hessian_apply_st(lrk_ctx* c, const lrk_hessian_desc* hd, const lrk_lr* v
   int info[8];
   CK(cudaMemcpyAsync(info, to.info, sizeof(info), cudaMemcpyDeviceToHost, s));
   int mr = 0;
-  TRY(host_max_rank(c, fw, zinfo, bw, to.info, &mr, s));
+  TRY(host_max_rank(c, fw, zinfo, bw, to.info, &mr, hd->compress_every, v->r, nt, s));
   if (info[2] != 0) return fail(c, LRK_ERR_SHAPE, "output capacity too small");
   out->r = info[0];
   if (max_rank) *max_rank = mr;

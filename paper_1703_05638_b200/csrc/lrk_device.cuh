@@ -13,7 +13,7 @@
 
 namespace lrk {
 
-constexpr int NT = 512;            // threads per CTA of the persistent kernels
+constexpr int NT = 256;            // threads per CTA of the persistent kernels
 constexpr int NWARP = NT / 32;
 constexpr int PMAX = 16;           // max columns appended per block (compress_every)
 constexpr int JMAX_SMEM = 80;      // Jacobi SVD kept in SMEM up to this order
@@ -94,7 +94,7 @@ __device__ inline void block_sum_rt(double* vals, int K, double* red, double* ou
 // out[o] = sum_c part[c*stride + o], o < len.  Reads through L2 (.cg) because
 // other SMs wrote the data.  Every CTA computes the same sums in the same
 // order.  out is shared memory.
-__device__ inline void reduce_partials(const double* part, int64_t stride, int ncta,
+__device__ __forceinline__ void reduce_partials(const double* part, int64_t stride, int ncta,
                                        int len, double* out) {
   int lp = 1;
   while (lp < 32 && lp * 2 * len <= NT) lp *= 2;
@@ -118,7 +118,7 @@ __device__ inline void reduce_partials(const double* part, int64_t stride, int n
 
 // CTA-partial of A^T B over `nrows` rows: out[i*nb + j] = sum_t A[t + i*lda] *
 // B[t + j*ldb].  scratch: NT doubles of shared memory; out: shared.
-__device__ inline void cta_tn(const double* A, int64_t lda, int na, const double* B,
+__device__ __forceinline__ void cta_tn(const double* A, int64_t lda, int na, const double* B,
                               int64_t ldb, int nb, int nrows, double* out, double* scratch) {
   const int nout = na * nb;
   const int tid = threadIdx.x;
@@ -289,7 +289,7 @@ __device__ inline void block_householder_apply_q(const double* X, int64_t ldx, i
 // Single-thread column-pivoted Householder QR of a q x q matrix A (row-major,
 // in place): A*P = X*Rt.  Writes X (q x q row-major, orthogonal), Rt (upper,
 // row-major, in A) and perm (Rt column k corresponds to A column perm[k]).
-__device__ inline void small_pivoted_qr(double* A, int q, double* X, int* perm, double* cn) {
+__device__ __forceinline__ void small_pivoted_qr(double* A, int q, double* X, int* perm, double* cn) {
   for (int k = 0; k < q; ++k) {
     perm[k] = k;
     double s = 0;
@@ -340,7 +340,7 @@ __device__ inline void small_pivoted_qr(double* A, int q, double* X, int* perm, 
 }
 
 // _rank_cut (lowrank.py:98-111) on descending s[0..n); single thread.
-__device__ inline int rank_cut_dev(const double* s, int n, double eps0, int r_max) {
+__device__ __forceinline__ int rank_cut_dev(const double* s, int n, double eps0, int r_max) {
   if (n == 0 || !(s[0] > 0.0)) return 0;
   const double floor_v = NOISE_FLOOR * s[0];
   // tail[r] = sqrt(sum_{i>=r} s_i^2) accumulated from the end (as np.cumsum on
@@ -372,17 +372,33 @@ __device__ inline int rank_cut_dev(const double* s, int n, double eps0, int r_ma
 // (unsorted), columns of A hold U*diag(s) (unsorted), s_sorted[k] the k-th
 // largest singular value, perm[k] its column.  nrm: n doubles, flag: 1 int
 // (all shared).
-__device__ inline void jacobi_svd(double* A, int lda, double* V, int ldv, int n,
-                                  double* s_sorted, int* perm, double* nrm, int* flag) {
+__device__ inline int jacobi_svd(double* A, int lda, double* V, int ldv, int n,
+                                 double* s_sorted, int* perm, double* nrm, int* flag,
+                                 double* fro) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int nsweep = 0;
+  // columns below 1e-16 ||M||_F are rounding noise (far under the 1e-15
+  // noise floor of _rank_cut): rotating them never converges and cannot
+  // change any retained singular triplet, so such pairs are skipped
+  if (w == 0) {
+    double s = 0.0;
+    for (int idx = lane; idx < n * n; idx += 32) {
+      const double x = A[(idx % n) + (idx / n) * lda];
+      s += x * x;
+    }
+    s = warp_sum(s);
+    if (lane == 0) *fro = s * 1e-32;
+  }
   for (int idx = tid; idx < n * n; idx += NT) {
     int i = idx % n, j = idx / n;
     V[i + j * ldv] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   const int ne = n + (n & 1);
-  const double tol = DEPS * (n > 16 ? sqrt((double)n) : 4.0);
-  for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
+  // rotate only when the cosine between two columns exceeds the rounding
+  // floor of an n-term dot product (a tighter test never terminates)
+  const double tol = 2.0 * DEPS * (double)(n > 8 ? n : 8);
+  for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
     // exact column norms
     for (int c = w; c < n; c += NWARP) {
       double s = 0.0;
@@ -403,7 +419,7 @@ __device__ inline void jacobi_svd(double* A, int lda, double* V, int ldv, int n,
         double g = 0.0;
         for (int l = lane; l < n; l += 32) g += A[l + i * lda] * A[l + j * lda];
         g = warp_sum(g);
-        if (!(al > 0.0) || !(be > 0.0)) continue;
+        if (!(al > *fro) || !(be > *fro)) continue;
         if (fabs(g) <= tol * sqrt(al) * sqrt(be)) continue;
         const double zeta = (be - al) / (2.0 * g);
         double t;
@@ -426,6 +442,7 @@ __device__ inline void jacobi_svd(double* A, int lda, double* V, int ldv, int n,
       }
       __syncthreads();
     }
+    ++nsweep;
     if (*flag == 0) break;
     __syncthreads();
   }
@@ -449,6 +466,114 @@ __device__ inline void jacobi_svd(double* A, int lda, double* V, int ldv, int n,
     s_sorted[rk] = si;
   }
   __syncthreads();
+  return nsweep;
+}
+
+// ------------------------------------------- single-warp Jacobi (n <= 32)
+// One-sided Jacobi executed by ONE warp with no CTA barrier: lane j owns
+// column j of the matrix and of the accumulated rotations.  Columns live in
+// two shared-memory ping-pong copies (A0/A1, V0/V1; leading dimension ld,
+// odd so the 32 lanes hit distinct banks); each round a lane reads its own
+// and its partner's column from the current copy and writes its rotated
+// column to the other, so the only synchronisation is __syncwarp().
+// Round-robin pairing: lanes a, b with a + b = 2*rnd (mod ne-1), lane ne-1
+// paired with rnd.  On exit: Uo[:, k] (ld ldo) = k-th left singular vector,
+// Vo[:, k] = right singular vector, s_sorted[k] descending, perm[k] source
+// column.  A0 holds the input on entry.  Returns the number of sweeps.
+__device__ inline int warp_jacobi_svd(double* A0, double* A1, double* V0, double* V1, int ld,
+                                      int n, double* Uo, double* Vo, int ldo, double* s_sorted,
+                                      int* perm) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const bool own = lane < n;
+  if (own)
+    for (int i = 0; i < n; ++i) V0[i + lane * ld] = (i == lane) ? 1.0 : 0.0;
+  double nrm = 0.0;
+  if (own)
+    for (int i = 0; i < n; ++i) { const double x = A0[i + lane * ld]; nrm += x * x; }
+  const double tiny = warp_sum(nrm) * 1e-32;  // (1e-16 ||M||_F)^2, see jacobi_svd
+  const double tol = 2.0 * DEPS * (double)(n > 8 ? n : 8);
+  const int ne = n + (n & 1);
+  double *Ac = A0, *An = A1, *Vc = V0, *Vn = V1;
+  int nsweep = 0;
+  __syncwarp();
+  for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
+    bool rotated = false;
+    if (own) {
+      nrm = 0.0;
+      for (int i = 0; i < n; ++i) { const double x = Ac[i + lane * ld]; nrm += x * x; }
+    }
+    for (int rnd = 0; rnd < ne - 1; ++rnd) {
+      int p;
+      if (lane == ne - 1) p = rnd;
+      else if (lane == rnd) p = ne - 1;
+      else { p = 2 * rnd - lane; p %= (ne - 1); if (p < 0) p += ne - 1; }
+      const double np = __shfl_sync(full, nrm, p & 31);
+      const bool act = own && p < n;
+      double c = 1.0, s = 0.0, t = 0.0, g = 0.0;
+      bool rot = false;
+      const bool lo = lane < p;
+      const double al = lo ? nrm : np, be = lo ? np : nrm;
+      if (act) {
+        const double* me = Ac + lane * ld;
+        const double* pa = Ac + p * ld;
+        for (int i = 0; i < n; ++i) g += me[i] * pa[i];
+        if (al > tiny && be > tiny && fabs(g) > tol * sqrt(al * be)) {
+          const double d = be - al;
+          t = 2.0 * g / (fabs(d) + sqrt(d * d + 4.0 * g * g));
+          if (d < 0.0) t = -t;
+          c = rsqrt(1.0 + t * t);
+          s = c * t;
+          rot = true;
+        }
+      }
+      if (own) {
+        const double* me = Ac + lane * ld;
+        const double* pa = Ac + (act ? p : lane) * ld;
+        const double* vm = Vc + lane * ld;
+        const double* vp = Vc + (act ? p : lane) * ld;
+        double* mo = An + lane * ld;
+        double* vo = Vn + lane * ld;
+        if (!rot) {
+          for (int i = 0; i < n; ++i) { mo[i] = me[i]; vo[i] = vm[i]; }
+        } else if (lo) {  // I am column i: a_i' = c a_i - s a_j
+          for (int i = 0; i < n; ++i) { mo[i] = c * me[i] - s * pa[i]; vo[i] = c * vm[i] - s * vp[i]; }
+          nrm = al - t * g;
+        } else {          // I am column j: a_j' = s a_i + c a_j
+          for (int i = 0; i < n; ++i) { mo[i] = s * pa[i] + c * me[i]; vo[i] = s * vp[i] + c * vm[i]; }
+          nrm = be + t * g;
+        }
+      }
+      rotated |= rot;
+      { double* tp = Ac; Ac = An; An = tp; }
+      { double* tp = Vc; Vc = Vn; Vn = tp; }
+      __syncwarp();
+    }
+    ++nsweep;
+    if (!__any_sync(full, rotated)) break;
+  }
+  // singular values, stable descending order, normalised outputs
+  double sv = 0.0;
+  if (own) {
+    for (int i = 0; i < n; ++i) { const double x = Ac[i + lane * ld]; sv += x * x; }
+    sv = sqrt(sv);
+  }
+  int rk = 0;
+  for (int j = 0; j < n; ++j) {
+    const double sj = __shfl_sync(full, sv, j);
+    if (sj > sv || (sj == sv && j < lane)) ++rk;
+  }
+  if (own) {
+    perm[rk] = lane;
+    s_sorted[rk] = sv;
+    const double inv = sv > 0.0 ? 1.0 / sv : 0.0;
+    for (int i = 0; i < n; ++i) {
+      Uo[i + rk * ldo] = Ac[i + lane * ld] * inv;
+      Vo[i + rk * ldo] = Vc[i + lane * ld];
+    }
+  }
+  __syncwarp();
+  return nsweep;
 }
 
 // Row range owned by CTA `cta` of `ncta` over `n` rows.

@@ -14,6 +14,7 @@ struct SweepArgs {
   int p;            // compress_every
   int r_max;        // < 0: none
   double eps0;
+  double ftz;              // |y| below this is flushed to zero (0 = off)
   const double* theta;     // n_x: eigenvalues of S^{-1} M
   const double* rowscale;  // n_x or NULL: B~ = rowscale .* B
   const double* B;         // n_x x rb (rhs spatial factor, eigenbasis)
@@ -35,12 +36,32 @@ struct SweepArgs {
   double* scratch; int64_t scratch_stride;  // per-CTA
   unsigned* bar;           // 2 unsigned per group
   int ncta;
+  long long* dbg;          // optional per-phase cycle counters (10), CTA 0
+  // shared-memory plan (offsets in doubles, computed by sweep_plan)
+  int resident;            // 1: CTA row blocks of U/Y/Q~ live in shared memory
+  int mp;                  // padded rows per CTA (leading dim of resident blocks)
+  int tp;                  // padded time rows per CTA (resident V block)
+  int off_V, off_U, off_Y, off_Q, off_yp, off_th, off_rs;
+  int off_small, off_scr;  // small matrices; phase-4 scratch (stack QR / Jacobi)
+  int stack_smem;          // stacked-R QR in shared memory
+  int smem_doubles;
+};
+
+// Shared-memory plan for a sweep over n_x rows with ncta CTAs per group.
+void sweep_plan(SweepArgs& a, int64_t n_x, int ncta, int ucap, int p, size_t smem_limit);
+
+// Independent sweeps launched together, one group of ncta CTAs each (passed
+// by value as a __grid_constant__ kernel parameter: no host->device copy).
+constexpr int SWEEP_MAXG = 16;
+struct SweepBatch {
+  SweepArgs g[SWEEP_MAXG];
+  int ngroups;
 };
 
 size_t sweep_smem_bytes();
 int64_t sweep_scratch_stride(int ncta);
 int64_t sweep_part_stride();
-cudaError_t launch_sweep(const SweepArgs* d_args, int ngroups, int ncta, cudaStream_t s);
+cudaError_t launch_sweep(const SweepBatch& batch, cudaStream_t s);
 
 // General lr_truncate (lowrank.py:124-144) of W1 (n_x x R) W2^T (n_t x R).
 struct TruncArgs {
@@ -71,7 +92,7 @@ struct TruncArgs {
 size_t trunc_smem_bytes();
 int64_t trunc_scratch_stride(int ncta);
 int64_t trunc_part_stride();
-cudaError_t launch_truncate(const TruncArgs* d_args, int ncta, cudaStream_t s);
+cudaError_t launch_truncate(const TruncArgs& args, cudaStream_t s);
 
 // fp64 batched GEMM: C[b] = alpha * A[b] B[b] + beta * C[b], all row-major.
 struct GemmArgs {

@@ -1,0 +1,606 @@
+// lrk_small.cuh — latency-oriented building blocks for the persistent sweep,
+// specialised at compile time on the flush width Q (columns appended per
+// truncation) so no loop runs over unused padding.
+//
+// All row-local routines take raw pointers that the sweep resolves either to
+// a CTA's shared-memory block or to global rows; loads are issued before any
+// dependent store (explicit register staging) so generic-pointer aliasing
+// never serialises the loops.
+#pragma once
+#include "lrk_device.cuh"
+
+namespace lrk {
+
+// Householder QR of X (m x q, col-major) by the whole CTA, one fused block
+// reduction per column: sums[0] = ||x_j below diag||^2, sums[k] = x_j . x_k.
+// Reflectors overwrite X below the diagonal, tau[j] saved, R (q x q
+// row-major, zero padded) to Rout.  red: NWARP*Q, tmp: Q (shared).
+template <int Q>
+__device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, int m, int q,
+                           double* __restrict__ tau, double* __restrict__ Rout,
+                           double* __restrict__ red, double* __restrict__ tmp) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < q * q; i += NT) Rout[i] = 0.0;
+  const int kmax = m < q ? m : q;
+  for (int j = 0; j < kmax; ++j) {
+    double s[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) s[k] = 0.0;
+    for (int i = j + 1 + tid; i < m; i += NT) {
+      const double xj = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int k = 0; k < Q; ++k)
+        if (k >= j && k < q) s[k] += xj * X[i + (int64_t)k * ldx];
+    }
+    // s[j] = ||x_j||^2 below the diagonal, s[k>j] = x_j . x_k (below the diagonal)
+    block_sum<Q>(s, red, tmp);
+    double xr[Q];  // row j before the update (all threads read it)
+#pragma unroll
+    for (int k = 0; k < Q; ++k) xr[k] = (k > j && k < q) ? X[j + (int64_t)k * ldx] : 0.0;
+    const double alpha = X[j + (int64_t)j * ldx];
+    double sig = 0.0;
+#pragma unroll
+    for (int k = 0; k < Q; ++k)
+      if (k == j) sig = s[k];
+    double beta, t, scale;
+    if (sig == 0.0) {
+      t = 0.0; beta = alpha; scale = 0.0;
+    } else {
+      const double nrm = sqrt(alpha * alpha + sig);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    // w_k = x_jk + scale * (x_j . x_k)  for k > j  (v_i = scale x_ij, v_j = 1)
+    double f[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) f[k] = (k > j && k < q) ? t * (xr[k] + scale * s[k]) : 0.0;
+    __syncthreads();  // row j read by everyone before it changes
+    for (int i = j + 1 + tid; i < m; i += NT) {
+      const double vi = X[i + (int64_t)j * ldx] * scale;
+      double x[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) x[k] = (k > j && k < q) ? X[i + (int64_t)k * ldx] : 0.0;
+      X[i + (int64_t)j * ldx] = vi;
+#pragma unroll
+      for (int k = 0; k < Q; ++k)
+        if (k > j && k < q) X[i + (int64_t)k * ldx] = x[k] - f[k] * vi;
+    }
+    if (tid == 0) {
+      tau[j] = t;
+#pragma unroll
+      for (int k = 0; k < Q; ++k)
+        if (k > j && k < q) {
+          const double v = xr[k] - f[k];
+          X[j + (int64_t)k * ldx] = v;
+          Rout[j * q + k] = v;
+        }
+      Rout[j * q + j] = beta;
+      X[j + (int64_t)j * ldx] = beta;
+    }
+    __syncthreads();
+  }
+  for (int j = kmax + tid; j < q; j += NT) tau[j] = 0.0;
+  __syncthreads();
+}
+
+// Y (m x q) = H_0 ... H_{kmax-1} [G; 0]  (G q x q row-major), whole CTA.
+template <int Q>
+__device__ __forceinline__ void block_apply_q_t(const double* __restrict__ X, int64_t ldx, int m, int q,
+                                const double* __restrict__ tau, const double* __restrict__ G,
+                                double* __restrict__ Y, int64_t ldy, double* __restrict__ red,
+                                double* __restrict__ tmp) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < m; i += NT) {
+#pragma unroll
+    for (int c = 0; c < Q; ++c)
+      if (c < q) Y[i + (int64_t)c * ldy] = (i < q) ? G[i * q + c] : 0.0;
+  }
+  __syncthreads();
+  const int kmax = m < q ? m : q;
+  for (int j = kmax - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t == 0.0) continue;  // uniform
+    double w[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) w[c] = 0.0;
+    for (int i = j + 1 + tid; i < m; i += NT) {
+      const double vi = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int c = 0; c < Q; ++c)
+        if (c < q) w[c] += vi * Y[i + (int64_t)c * ldy];
+    }
+    block_sum<Q>(w, red, tmp);
+    double f[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) f[c] = (c < q) ? t * (w[c] + Y[j + (int64_t)c * ldy]) : 0.0;
+    __syncthreads();
+    for (int i = j + 1 + tid; i < m; i += NT) {
+      const double vi = X[i + (int64_t)j * ldx];
+#pragma unroll
+      for (int c = 0; c < Q; ++c)
+        if (c < q) Y[i + (int64_t)c * ldy] -= f[c] * vi;
+    }
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < Q; ++c)
+        if (c < q) Y[j + (int64_t)c * ldy] -= f[c];
+    }
+    __syncthreads();
+  }
+}
+
+// X[:, 0..nx) -= A[:, 0..na) Cm, Cm na x nx row-major (shared); nx <= Q.
+template <int Q>
+__device__ __forceinline__ void rows_sub_t(double* __restrict__ X, int64_t ldx, int nx,
+                           const double* __restrict__ A, int64_t lda, int na,
+                           const double* __restrict__ Cm, int nrows) {
+  for (int t = threadIdx.x; t < nrows; t += NT) {
+    double acc[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) acc[j] = 0.0;
+    for (int i = 0; i < na; ++i) {
+      const double a = A[t + (int64_t)i * lda];
+#pragma unroll
+      for (int j = 0; j < Q; ++j)
+        if (j < nx) acc[j] += a * Cm[i * nx + j];
+    }
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+      if (j < nx) X[t + (int64_t)j * ldx] -= acc[j];
+  }
+}
+
+// One-sided Jacobi SVD of an n x n matrix (n <= NJ <= 32) by ONE warp with
+// the columns in registers: lane j holds column j of A and of V (zero padded
+// to NJ, which leaves the arithmetic unchanged).  The partner column of a
+// round arrives by shuffles, so there is no shared-memory traffic and no CTA
+// barrier.  Rotation test: cosine above the rounding floor of an n-term dot
+// product; columns under 1e-16 ||M||_F are noise (see jacobi_svd).  Stops
+// after a sweep whose largest cosine was <= 1e-8: the next sweep could only
+// change the result at the 1e-16 level (quadratic convergence).
+// Output (lanes < n): Uo[:, k] (ld ldo) k-th left singular vector, Vo[:, k]
+// right singular vector, s_sorted[k] descending, perm[k] source column.
+template <int NJ, bool KEEP = (NJ <= 24)>
+__device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, int lda, int n,
+                               double* __restrict__ Uo, double* __restrict__ Vo, int ldo,
+                               double* __restrict__ s_sorted, int* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const bool own = lane < n;
+  double a[NJ], v[NJ];
+#pragma unroll
+  for (int i = 0; i < NJ; ++i) {
+    a[i] = (own && i < n) ? Ain[i + lane * lda] : 0.0;
+    v[i] = (i == lane) ? 1.0 : 0.0;
+  }
+  auto colnorm = [&]() {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < NJ; i += 4) {
+      s0 += a[i] * a[i];
+      if (i + 1 < NJ) s1 += a[i + 1] * a[i + 1];
+      if (i + 2 < NJ) s2 += a[i + 2] * a[i + 2];
+      if (i + 3 < NJ) s3 += a[i + 3] * a[i + 3];
+    }
+    return (s0 + s1) + (s2 + s3);
+  };
+  double nrm = colnorm();
+  const double tiny = warp_sum(nrm) * 1e-32;
+  const double tol = 2.0 * DEPS * (double)(n > 8 ? n : 8);
+  const double tol2 = tol * tol;
+  const int ne = n + (n & 1);
+  const int m1 = ne - 1;
+  int nsweep = 0;
+  for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
+    nrm = colnorm();
+    double maxcos2 = 0.0;
+    bool rotated = false;
+    // partner of lane for round rnd: (2 rnd - lane) mod (ne-1), kept
+    // incrementally; lane ne-1 meets rnd, lane rnd meets ne-1
+    int pf = (lane < m1) ? (m1 - lane) % m1 : 0;
+    for (int rnd = 0; rnd < m1; ++rnd) {
+      int p = pf;
+      if (lane == m1) p = rnd;
+      else if (lane == rnd) p = m1;
+      if (lane >= ne) p = lane;
+      pf += 2;
+      if (pf >= m1) pf -= m1;
+      const bool act = own && p < n;
+      const bool lo = lane < p;
+      const double np = __shfl_sync(full, nrm, p & 31);
+      double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+      double ap[KEEP ? NJ : 1];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        const double x = __shfl_sync(full, a[i], p & 31);
+        if (KEEP) ap[KEEP ? i : 0] = x;
+        if ((i & 3) == 0) g0 += a[i] * x;
+        else if ((i & 3) == 1) g1 += a[i] * x;
+        else if ((i & 3) == 2) g2 += a[i] * x;
+        else g3 += a[i] * x;
+      }
+      // identical summation order on both lanes of a pair: products commute
+      const double g = (g0 + g1) + (g2 + g3);
+      const double al = lo ? nrm : np, be = lo ? np : nrm;
+      double c = 1.0, s = 0.0, t = 0.0;
+      bool rot = false;
+      if (act && al > tiny && be > tiny) {
+        const double g2 = g * g, ab = al * be;
+        if (g2 > 1e-16 * ab) maxcos2 = 1.0;  // a cosine above 1e-8 this sweep
+        if (g2 > tol2 * ab) {
+          // tangent of the rotation angle: only its convergence effect depends
+          // on its accuracy, so it is formed in fp32 after an exact power-of-two
+          // rescale; c (and so c^2 + s^2 = 1) is then computed in fp64.
+          const double d = be - al;
+          const double m = fmax(fabs(d), fabs(g));
+          const int e = ((int)(__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+          const double sc = __longlong_as_double((long long)(1023 - e) << 52);
+          const float df = (float)(d * sc), gf = (float)(g * sc);
+          float tf;
+          if (fabsf(gf) < 1e-4f * fabsf(df)) tf = __fdividef(gf, df);  // t ~ g/d
+          else {
+            tf = __fdividef(2.0f * gf, fabsf(df) + sqrtf(df * df + 4.0f * gf * gf));
+            if (df < 0.0f) tf = -tf;
+          }
+          t = (double)tf;
+          const double t2 = t * t;
+          c = (t2 < 1e-8) ? 1.0 - t2 * (0.5 - 0.375 * t2) : rsqrt(1.0 + t2);
+          s = c * t;
+          rot = true;
+        }
+      }
+      const bool any = __any_sync(full, rot);
+      if (any) {
+        const double sl = lo ? -s : s;  // lo: a' = c a - s ap ; hi: a' = c a + s ap
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) {
+          // both lanes of a pair shuffle index i before either updates it
+          const double xp = KEEP ? ap[KEEP ? i : 0] : __shfl_sync(full, a[i], p & 31);
+          a[i] = rot ? (c * a[i] + sl * xp) : a[i];
+          const double vp = __shfl_sync(full, v[i], p & 31);
+          v[i] = rot ? (c * v[i] + sl * vp) : v[i];
+        }
+        if (rot) nrm = lo ? (al - t * g) : (be + t * g);
+        rotated = true;
+      }
+    }
+    ++nsweep;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxcos2 = fmax(maxcos2, __shfl_xor_sync(full, maxcos2, o));
+    if (!rotated || maxcos2 <= 1e-16) break;
+  }
+  double sv = own ? sqrt(colnorm()) : 0.0;
+  int rk = 0;
+  for (int j = 0; j < n; ++j) {
+    const double sj = __shfl_sync(full, sv, j);
+    if (sj > sv || (sj == sv && j < lane)) ++rk;
+  }
+  if (own) {
+    perm[rk] = lane;
+    s_sorted[rk] = sv;
+    const double inv = sv > 0.0 ? 1.0 / sv : 0.0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i)
+      if (i < n) {
+        Uo[i + rk * ldo] = a[i] * inv;
+        Vo[i + rk * ldo] = v[i];
+      }
+  }
+  __syncwarp();
+  return nsweep;
+}
+
+// Householder QR (optionally with column pivoting) of an n x n matrix held by
+// ONE warp in registers, lane j = column j (a[i] = entry i, zero padded to
+// NJ).  On exit a[] holds column `lane` of R; the reflector of step j is
+// stored in Vh[i + j*ldv] (i > j, unit leading entry implicit) with tau[j];
+// colid returns the original column index of the lane (pivot permutation).
+template <int NJ, bool PIVOT>
+__device__ __forceinline__ void warp_qr_cols(double (&a)[NJ], int n, double* __restrict__ Vh,
+                                             int ldv, double* __restrict__ tau, int& colid) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  colid = lane;
+  for (int j = 0; j < n - 1; ++j) {
+    if (PIVOT) {
+      double tn = 0.0;
+#pragma unroll
+      for (int i = 0; i < NJ; ++i)
+        if (i >= j) tn += a[i] * a[i];
+      if (lane < j || lane >= n) tn = -1.0;
+      int idx = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ot = __shfl_xor_sync(full, tn, o);
+        const int oi = __shfl_xor_sync(full, idx, o);
+        if (ot > tn || (ot == tn && oi < idx)) { tn = ot; idx = oi; }
+      }
+      if (idx != j) {  // uniform: swap columns j and idx
+        const int src = (lane == j) ? idx : ((lane == idx) ? j : lane);
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) a[i] = __shfl_sync(full, a[i], src);
+        colid = __shfl_sync(full, colid, src);
+      }
+    }
+    double x[NJ];
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) x[i] = __shfl_sync(full, a[i], j);
+    double sig = 0.0, alpha = 0.0;
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) {
+      if (i > j) sig += x[i] * x[i];
+      if (i == j) alpha = x[i];
+    }
+    double beta = alpha, t = 0.0, scale = 0.0;
+    if (sig != 0.0) {
+      const double nrm = sqrt(alpha * alpha + sig);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    // v_i = x_i * scale (i > j), v_j = 1
+    if (lane > j && lane < n) {
+      double w = 0.0;
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        if (i == j) w += a[i];
+        else if (i > j) w += x[i] * scale * a[i];
+      }
+      const double f = t * w;
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        if (i == j) a[i] -= f;
+        else if (i > j) a[i] -= f * x[i] * scale;
+      }
+    } else if (lane == j) {
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) {
+        if (i > j) {
+          Vh[i + j * ldv] = x[i] * scale;
+          a[i] = 0.0;
+        }
+        if (i == j) a[i] = beta;
+      }
+      tau[j] = t;
+    }
+  }
+  if (lane == 0) tau[n - 1] = 0.0;
+  __syncwarp();
+}
+
+// Same algorithm as warp_jacobi_reg, executed by JW warps (threads
+// [0, 32*JW)): lane j still owns column j, warp w holds rows
+// [w*NR, (w+1)*NR) of every column (NR = NJ/JW).  Per round each warp forms
+// its partial of the column dot product from its rows; the partials meet in
+// shared memory behind a named barrier (bar 1) and are summed in a fixed
+// order, so every warp derives bit-identical rotations.  gbuf: 2*JW*32
+// doubles (double-buffered by round parity).
+template <int NJ, int JW>
+__device__ __forceinline__ int multi_warp_jacobi(const double* __restrict__ Ain, int lda, int n,
+                                                 double* __restrict__ Uo, double* __restrict__ Vo,
+                                                 int ldo, double* __restrict__ s_sorted,
+                                                 int* __restrict__ perm, double* __restrict__ gbuf) {
+  constexpr int NR = NJ / JW;
+  static_assert(NR * JW == NJ, "NJ must be a multiple of JW");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned full = 0xffffffffu;
+  const bool own = lane < n;
+  const int row0 = w * NR;
+  double a[NR], v[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const int i = row0 + k;
+    a[k] = (own && i < n) ? Ain[i + lane * lda] : 0.0;
+    v[k] = (i == lane) ? 1.0 : 0.0;
+  }
+  int buf = 0;
+  auto xsum = [&](double part) {  // sum a per-lane value over the JW warps
+    gbuf[(buf * JW + w) * 32 + lane] = part;
+    asm volatile("bar.sync 1, %0;" ::"r"(JW * 32));
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < JW; ++ww) s += gbuf[(buf * JW + ww) * 32 + lane];
+    buf ^= 1;
+    return s;
+  };
+  auto colnorm_part = [&]() {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      if (k & 1) s1 += a[k] * a[k];
+      else s0 += a[k] * a[k];
+    }
+    return s0 + s1;
+  };
+  double nrm = xsum(colnorm_part());
+  const double tiny = warp_sum(nrm) * 1e-32;
+  const double tol = 2.0 * DEPS * (double)(n > 8 ? n : 8);
+  const double tol2 = tol * tol;
+  const int ne = n + (n & 1);
+  const int m1 = ne - 1;
+  int nsweep = 0;
+  for (int sweep = 0; sweep < 40 && n > 1; ++sweep) {
+    nrm = xsum(colnorm_part());
+    bool big = false, rotated = false;
+    int pf = (lane < m1) ? (m1 - lane) % m1 : 0;
+    for (int rnd = 0; rnd < m1; ++rnd) {
+      int p = pf;
+      if (lane == m1) p = rnd;
+      else if (lane == rnd) p = m1;
+      if (lane >= ne) p = lane;
+      pf += 2;
+      if (pf >= m1) pf -= m1;
+      const bool act = own && p < n;
+      const bool lo = lane < p;
+      const double np = __shfl_sync(full, nrm, p & 31);
+      double ap[NR];
+      double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {
+        ap[k] = __shfl_sync(full, a[k], p & 31);
+        if (k & 1) g1 += a[k] * ap[k];
+        else g0 += a[k] * ap[k];
+      }
+      // partial products are symmetric in (lane, p): both lanes of a pair
+      // reduce identical values in the same order
+      const double g = xsum(g0 + g1);
+      const double al = lo ? nrm : np, be = lo ? np : nrm;
+      double c = 1.0, sl = 0.0, t = 0.0;
+      bool rot = false;
+      if (act && al > tiny && be > tiny) {
+        const double g2 = g * g, ab = al * be;
+        if (g2 > 1e-16 * ab) big = true;
+        if (g2 > tol2 * ab) {
+          const double d = be - al;
+          const double m = fmax(fabs(d), fabs(g));
+          const int e = ((int)(__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+          const double sc = __longlong_as_double((long long)(1023 - e) << 52);
+          const float df = (float)(d * sc), gf = (float)(g * sc);
+          float tf;
+          if (fabsf(gf) < 1e-4f * fabsf(df)) tf = __fdividef(gf, df);
+          else {
+            tf = __fdividef(2.0f * gf, fabsf(df) + sqrtf(df * df + 4.0f * gf * gf));
+            if (df < 0.0f) tf = -tf;
+          }
+          t = (double)tf;
+          const double t2 = t * t;
+          c = (t2 < 1e-8) ? 1.0 - t2 * (0.5 - 0.375 * t2) : rsqrt(1.0 + t2);
+          sl = lo ? -c * t : c * t;
+          rot = true;
+        }
+      }
+      if (__any_sync(full, rot)) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          a[k] = c * a[k] + sl * ap[k];
+          const double vp = __shfl_sync(full, v[k], p & 31);
+          v[k] = c * v[k] + sl * vp;
+        }
+        if (rot) nrm = lo ? (al - t * g) : (be + t * g);
+        rotated = true;
+      }
+    }
+    ++nsweep;
+    if (!__any_sync(full, rotated) || !__any_sync(full, big)) break;
+  }
+  const double nfin = xsum(colnorm_part());  // every lane takes part in the barrier
+  const double sv = own ? sqrt(nfin) : 0.0;
+  int rk = 0;
+  for (int j = 0; j < n; ++j) {
+    const double sj = __shfl_sync(full, sv, j);
+    if (sj > sv || (sj == sv && j < lane)) ++rk;
+  }
+  if (own) {
+    if (w == 0) {
+      perm[rk] = lane;
+      s_sorted[rk] = sv;
+    }
+    const double inv = sv > 0.0 ? 1.0 / sv : 0.0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      const int i = row0 + k;
+      if (i < n) {
+        Uo[i + rk * ldo] = a[k] * inv;
+        Vo[i + rk * ldo] = v[k];
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(JW * 32));
+  return nsweep;
+}
+
+// Preconditioned one-sided Jacobi SVD of the n x n core (n <= NJ <= 32):
+//   M P = Q1 R1 (Householder QR with column pivoting),
+//   R1^T = Q2 R2 (unpivoted QR),
+//   X = R2^T,  X W = U_X diag(s)  (multi-warp Jacobi, typically ~2 sweeps
+//   instead of ~6 on the raw core),
+// so M = (Q1 U_X) diag(s) (P Q2 W)^T.  Executed by warps 0..3 (threads
+// [0,128)); the caller synchronises the CTA afterwards.  Outputs as
+// warp_jacobi_reg: Uo[:, k], Vo[:, k] (ld ldo), s_sorted (descending).
+// scr: PRECOND_SCR doubles of shared memory.
+constexpr int PRECOND_SCR = 5 * 32 * 33 + 2 * 32 + 2 * 4 * 32 + 32;
+template <int NJ>
+__device__ __forceinline__ int precond_svd(const double* __restrict__ core, int ldm, int n,
+                                           double* __restrict__ Uo, double* __restrict__ Vo,
+                                           int ldo, double* __restrict__ s_sorted,
+                                           int* __restrict__ perm, double* __restrict__ scr) {
+  constexpr int L = 33;
+  double* V1 = scr;
+  double* V2 = V1 + 32 * L;
+  double* X = V2 + 32 * L;
+  double* Uj = X + 32 * L;
+  double* Wj = Uj + 32 * L;
+  double* t1 = Wj + 32 * L;
+  double* t2 = t1 + 32;
+  double* gbuf = t2 + 32;
+  int* P = reinterpret_cast<int*>(gbuf + 2 * 4 * 32);
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {
+    double a[NJ];
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) a[i] = (lane < n && i < n) ? core[i + lane * ldm] : 0.0;
+    int colid;
+    warp_qr_cols<NJ, true>(a, n, V1, L, t1, colid);
+    if (lane < n) P[lane] = colid;
+    // X = R1^T (column i of X = row i of R1)
+#pragma unroll
+    for (int i = 0; i < NJ; ++i)
+      if (lane < n && i < n) X[lane + i * L] = a[i];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NJ; ++i) a[i] = (lane < n && i < n) ? X[i + lane * L] : 0.0;
+    __syncwarp();
+    int dummy;
+    warp_qr_cols<NJ, false>(a, n, V2, L, t2, dummy);
+    // X = R2^T
+#pragma unroll
+    for (int i = 0; i < NJ; ++i)
+      if (lane < n && i < n) X[lane + i * L] = a[i];
+  }
+  int nsw = 0;
+  if (tid < 128) {
+    asm volatile("bar.sync 1, 128;");
+    nsw = multi_warp_jacobi<NJ, 4>(X, L, n, Uj, Wj, L, s_sorted, perm, gbuf);
+    // back-transforms: U = Q1 U_X (threads [0,32)), V = P Q2 W (threads [32,64))
+    const bool isU = tid < 32;
+    const int k = isU ? tid : tid - 32;
+    if (tid < 64 && k < n) {
+      const double* src = isU ? Uj : Wj;
+      const double* Vh = isU ? V1 : V2;
+      const double* th = isU ? t1 : t2;
+      double u[NJ];
+#pragma unroll
+      for (int i = 0; i < NJ; ++i) u[i] = (i < n) ? src[i + k * L] : 0.0;
+      for (int j = n - 2; j >= 0; --j) {
+        const double tj = th[j];
+        if (tj == 0.0) continue;
+        double w = 0.0;
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) {
+          if (i == j) w += u[i];
+          else if (i > j && i < n) w += Vh[i + j * L] * u[i];
+        }
+        const double f = tj * w;
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) {
+          if (i == j) u[i] -= f;
+          else if (i > j && i < n) u[i] -= f * Vh[i + j * L];
+        }
+      }
+      if (isU) {
+#pragma unroll
+        for (int i = 0; i < NJ; ++i)
+          if (i < n) Uo[i + k * ldo] = u[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < NJ; ++i)
+          if (i < n) Vo[P[i] + k * ldo] = u[i];
+      }
+    }
+    asm volatile("bar.sync 1, 128;");
+  }
+  return nsw;
+}
+
+}  // namespace lrk

@@ -19,334 +19,529 @@
 // those of the reference; the pane is returned in the eigenbasis and mapped
 // back by the caller.
 //
+// Latency design (the sweep is a chain of n_t/p dependent truncations):
+//  * every CTA keeps its block of U, Y, Q~, the carried column and the
+//    eigenvalues resident in shared memory for the whole sweep when they fit
+//    (sweep_plan), so row-local passes never touch L2;
+//  * three grid barriers per flush; the small algebra (stacked-R QR, pivoted
+//    fix-up, core SVD, rank cut) is computed redundantly by every CTA from the
+//    same reduced partials, so no broadcast barrier is needed;
+//  * the core SVD is a register-resident single-warp Jacobi (no CTA barrier);
+//  * all loops are specialised on the flush width Q (template) and the basis
+//    update runs in place with register accumulators.
+//
 // Grid: ngroups x ncta CTAs (one group per independent sweep), NT threads,
 // one CTA per SM, launched cooperatively so all CTAs are co-resident.
+#include <algorithm>
+
 #include "lrk_device.cuh"
 #include "lrk_kernels.h"
+#include "lrk_small.cuh"
 
 namespace lrk {
 
 namespace {
-struct SweepSmem {
-  // offsets in doubles
-  static constexpr int off_C = 0;                         // NMAX*PMAX
-  static constexpr int off_Yn = off_C + NMAX * PMAX;      // PMAX
-  static constexpr int off_R = off_Yn + PMAX;             // PMAX^2
-  static constexpr int off_Rp = off_R + PMAX * PMAX;      // PMAX^2
-  static constexpr int off_X = off_Rp + PMAX * PMAX;      // PMAX^2
-  static constexpr int off_G = off_X + PMAX * PMAX;       // PMAX^2
-  static constexpr int off_I = off_G + PMAX * PMAX;       // PMAX^2
-  static constexpr int off_Q = off_I + PMAX * PMAX;       // PMAX^2
-  static constexpr int off_Rb = off_Q + PMAX * PMAX;      // PMAX^2
-  static constexpr int off_tau = off_Rb + PMAX * PMAX;    // PMAX
-  static constexpr int off_taut = off_tau + PMAX;         // PMAX
-  static constexpr int off_cn = off_taut + PMAX;          // PMAX
-  static constexpr int off_sig = off_cn + PMAX;           // NMAX
-  static constexpr int off_s = off_sig + NMAX;            // NMAX
-  static constexpr int off_inv = off_s + NMAX;            // NMAX
-  static constexpr int off_nrm = off_inv + NMAX;          // NMAX
-  static constexpr int off_red = off_nrm + NMAX;          // NWARP*PMAX
-  static constexpr int off_tmp = off_red + NWARP * PMAX;  // PMAX
-  static constexpr int off_scr = off_tmp + PMAX;          // NT
-  static constexpr int off_part = off_scr + NT;           // NMAX*PMAX + PMAX
-  static constexpr int off_jac = off_part + NMAX * PMAX + PMAX;  // 2*JMAX^2
-  static constexpr int n_double = off_jac + 2 * JMAX_SMEM * JMAX_SMEM;
-  static constexpr int n_int = NMAX + PMAX + 8;
-  static constexpr size_t bytes = n_double * sizeof(double) + n_int * sizeof(int);
+constexpr int NINT = NMAX + PMAX + 8;
+
+struct Small {  // offsets inside the small region, sized by (cap, pc)
+  int C, Part, Yn, R, Rp, X, G, I, Qs, Rb, Tau, TauT, Cn, Sig, S, Red, Tmp, Scr, Uc, Vc, Core, Int,
+      total;
+  __host__ __device__ Small(int cap, int pc) {
+    int o = 0;
+    C = o; o += cap * pc;
+    Part = o; o += cap * pc + pc + 8;
+    Yn = o; o += pc;
+    R = o; o += pc * pc;
+    Rp = o; o += pc * pc;
+    X = o; o += pc * pc;
+    G = o; o += pc * pc;
+    I = o; o += pc * pc;
+    Qs = o; o += pc * pc;
+    Rb = o; o += pc * pc;
+    Tau = o; o += pc;
+    TauT = o; o += pc;
+    Cn = o; o += pc;
+    Sig = o; o += NMAX;
+    S = o; o += NMAX;
+    Red = o; o += NWARP * PMAX;
+    Tmp = o; o += PMAX;
+    Scr = o; o += NT;
+    Uc = o; o += 32 * 32;
+    Vc = o; o += 32 * 32;
+    Core = o; o += 32 * 33;
+    Int = o; o += (NINT + 1) / 2;
+    total = o;
+  }
 };
+
+// Rows i in [0, m) of X = [A (na cols), B (nb cols)] times W (n x rn, ld ldw),
+// written in place into A's first rn columns (accumulators in registers;
+// every read of a row happens before its write).  rn <= RA.
+template <int RA>
+__device__ __forceinline__ void update_rows(double* __restrict__ A, int64_t lda, int na, const double* __restrict__ B,
+                            int64_t ldb, int nb, const double* __restrict__ W, int ldw, int rn, int m) {
+  const int n = na + nb;
+  for (int i = threadIdx.x; i < m; i += NT) {
+    double acc[RA];
+#pragma unroll
+    for (int c = 0; c < RA; ++c) acc[c] = 0.0;
+    for (int k = 0; k < n; ++k) {
+      const double x = (k < na) ? A[i + (int64_t)k * lda] : B[i + (int64_t)(k - na) * ldb];
+      const double* w = W + k;
+#pragma unroll
+      for (int c = 0; c < RA; ++c)
+        if (c < rn) acc[c] += x * w[c * ldw];
+    }
+#pragma unroll
+    for (int c = 0; c < RA; ++c)
+      if (c < rn) A[i + (int64_t)c * lda] = acc[c];
+  }
+}
+
+// Time rows: V'[t] = V[t, :r] W[:r, :rn] + [t visited at slot s] W[r+s, :rn]
+// (V points at this CTA's first time row t0; local row index tl = t - t0.)
+template <int RA>
+__device__ __forceinline__ void update_time_rows(double* __restrict__ V, int64_t ldv, int r, const double* __restrict__ W,
+                                 int ldw, int rn, int64_t t0, int64_t t1, int adjoint, int n_t,
+                                 int start, int pc) {
+  for (int64_t t = t0 + threadIdx.x; t < t1; t += NT) {
+    const int64_t tl = t - t0;
+    int sel = adjoint ? (n_t - 1 - start) - (int)t : (int)t - start;
+    double acc[RA];
+#pragma unroll
+    for (int c = 0; c < RA; ++c) acc[c] = (sel >= 0 && sel < pc && c < rn) ? W[(r + sel) + c * ldw] : 0.0;
+    for (int k = 0; k < r; ++k) {
+      const double x = V[tl + (int64_t)k * ldv];
+#pragma unroll
+      for (int c = 0; c < RA; ++c)
+        if (c < rn) acc[c] += x * W[k + c * ldw];
+    }
+#pragma unroll
+    for (int c = 0; c < RA; ++c)
+      if (c < rn) V[tl + (int64_t)c * ldv] = acc[c];
+  }
+}
 }  // namespace
 
-size_t sweep_smem_bytes() { return SweepSmem::bytes; }
+void sweep_plan(SweepArgs& a, int64_t n_x, int ncta, int ucap, int p, size_t smem_limit) {
+  const int64_t mloc = (n_x + ncta - 1) / ncta;
+  const int mp = (int)(mloc | 1);
+  Small sm(ucap, p);
+  const int stack = 2 * ncta * p * p;
+  const int64_t limit = (int64_t)(smem_limit / sizeof(double)) - 64;
+  int scr = 0;
+  int stack_smem = 0;
+  if (sm.total + stack <= limit) { scr = stack; stack_smem = 1; }
+  const int tp = (int)(((int64_t)a.n_t + ncta - 1) / ncta) | 1;
+  const int64_t resident_rows = (int64_t)mp * (ucap + 2 * p + 3) + (int64_t)tp * ucap;
+  // resident mode keeps the stacked-R QR in shared memory too
+  const bool resident = stack_smem && sm.total + scr + resident_rows <= limit;
+  int o = 0;
+  a.resident = resident ? 1 : 0;
+  a.mp = resident ? mp : 0;
+  a.tp = resident ? tp : 0;
+  if (resident) {
+    a.off_V = o; o += tp * ucap;
+    a.off_U = o; o += mp * ucap;
+    a.off_Y = o; o += mp * p;
+    a.off_Q = o; o += mp * p;
+    a.off_yp = o; o += mp;
+    a.off_th = o; o += mp;
+    a.off_rs = o; o += mp;
+  } else {
+    a.off_U = a.off_Y = a.off_Q = a.off_yp = a.off_th = a.off_rs = 0;
+  }
+  a.off_small = o; o += sm.total;
+  a.off_scr = o; o += scr;
+  a.stack_smem = stack_smem;
+  a.smem_doubles = o;
+}
+
+size_t sweep_smem_bytes() { return 227 * 1024; }
 int64_t sweep_scratch_stride(int ncta) {
-  return 2 * (int64_t)ncta * PMAX * PMAX + 2 * (int64_t)NMAX * NMAX;
+  return 2 * (int64_t)ncta * PMAX * PMAX + 4 * (int64_t)NMAX * NMAX;
 }
 int64_t sweep_part_stride() { return NMAX * PMAX + PMAX + 8; }
 
-__global__ void __launch_bounds__(NT, 1) sweep_kernel(const SweepArgs* __restrict__ all_args) {
+template <int Q, bool RES>
+__global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ SweepBatch batch) {
   extern __shared__ double sm[];
-  const int ncta = all_args[0].ncta;
-  const SweepArgs& a = all_args[blockIdx.x / ncta];
+  const int ncta = batch.g[0].ncta;
+  const SweepArgs& a = batch.g[blockIdx.x / ncta];
   const int cta = blockIdx.x % ncta;
-  const int tid = threadIdx.x;
-
-  double* sC = sm + SweepSmem::off_C;
-  double* sYn = sm + SweepSmem::off_Yn;
-  double* sR = sm + SweepSmem::off_R;
-  double* sRp = sm + SweepSmem::off_Rp;
-  double* sX = sm + SweepSmem::off_X;
-  double* sG = sm + SweepSmem::off_G;
-  double* sI = sm + SweepSmem::off_I;
-  double* sQ = sm + SweepSmem::off_Q;
-  double* sRb = sm + SweepSmem::off_Rb;
-  double* sTau = sm + SweepSmem::off_tau;
-  double* sTauT = sm + SweepSmem::off_taut;
-  double* sCn = sm + SweepSmem::off_cn;
-  double* sSig = sm + SweepSmem::off_sig;
-  double* sS = sm + SweepSmem::off_s;
-  double* sInv = sm + SweepSmem::off_inv;
-  double* sNrm = sm + SweepSmem::off_nrm;
-  double* sRed = sm + SweepSmem::off_red;
-  double* sTmp = sm + SweepSmem::off_tmp;
-  double* sScr = sm + SweepSmem::off_scr;
-  double* sPart = sm + SweepSmem::off_part;
-  double* sJac = sm + SweepSmem::off_jac;
-  int* iPerm = reinterpret_cast<int*>(sm + SweepSmem::n_double);
-  int* iPiv = iPerm + NMAX;
-  int* iFlag = iPiv + PMAX;  // [0] jacobi flag, [1] new rank, [2] error
+  const int tid = threadIdx.x, warp = tid >> 5;
 
   const int64_t n_x = a.n_x;
   const int n_t = a.n_t;
   const int p = a.p;
+  const int cap = a.ucap;
   const int rb = a.rb_dev ? min(a.rb, *a.rb_dev) : a.rb;
   int64_t r0, r1, t0, t1;
   row_range(n_x, cta, ncta, r0, r1);
   row_range(n_t, cta, ncta, t0, t1);
   const int m_loc = (int)(r1 - r0);
 
-  double* Ucur = a.U0;
-  double* Ualt = a.U1;
-  double* Vcur = a.V0;
-  double* Valt = a.V1;
-  int r = 0;
+  // ---- storage: resident shared-memory blocks or global rows.  RES is a
+  // template parameter so every pointer has a single, provable address space
+  // (the compiler emits LDS/STS for the resident blocks, not generic LD/ST).
+  constexpr bool res = RES;
+  double* Ul;
+  double* Yl;
+  double* Ql;
+  double* Vl;
+  double* yp;
+  const double* th;
+  const double* rsc;
+  int64_t ldu, ldy, ldq, ldvl;
+  if constexpr (RES) {
+    Ul = sm + a.off_U; Yl = sm + a.off_Y; Ql = sm + a.off_Q; Vl = sm + a.off_V;
+    yp = sm + a.off_yp; th = sm + a.off_th; rsc = sm + a.off_rs;
+    ldu = ldy = ldq = a.mp;
+    ldvl = a.tp;
+    for (int i = tid; i < m_loc; i += NT) {
+      sm[a.off_yp + i] = 0.0;
+      sm[a.off_th + i] = a.theta[r0 + i];
+      sm[a.off_rs + i] = a.rowscale ? a.rowscale[r0 + i] : 1.0;
+    }
+  } else {
+    Ul = a.U0 + r0; Yl = a.ybuf + r0; Ql = a.qbuf + r0; Vl = a.V0 + t0;
+    yp = a.yprev + r0; th = a.theta + r0; rsc = a.rowscale ? a.rowscale + r0 : nullptr;
+    ldu = a.ldu; ldy = a.ldy; ldq = a.ldq; ldvl = a.ldv;
+    for (int i = tid; i < m_loc; i += NT) yp[i] = 0.0;
+  }
 
-  double* stack = a.scratch + (int64_t)cta * a.scratch_stride;
-  double* stackY = stack + (int64_t)ncta * PMAX * PMAX;
-  double* jacG = stackY + (int64_t)ncta * PMAX * PMAX;
+  Small L(cap, p);
+  double* small = sm + a.off_small;
+  double* sC = small + L.C;
+  double* sPart = small + L.Part;
+  double* sYn = small + L.Yn;
+  double* sR = small + L.R;
+  double* sRp = small + L.Rp;
+  double* sX = small + L.X;
+  double* sG = small + L.G;
+  double* sI = small + L.I;
+  double* sQs = small + L.Qs;
+  double* sRb = small + L.Rb;
+  double* sTau = small + L.Tau;
+  double* sTauT = small + L.TauT;
+  double* sCn = small + L.Cn;
+  double* sSig = small + L.Sig;
+  double* sS = small + L.S;
+  double* sRed = small + L.Red;
+  double* sTmp = small + L.Tmp;
+  double* sScr = small + L.Scr;
+  double* sCore = small + L.Core;
+  int* iPerm = reinterpret_cast<int*>(small + L.Int);
+  int* iPiv = iPerm + NMAX;
+  int* iFlag = iPiv + PMAX;
 
+  double* gscr = a.scratch + (int64_t)cta * a.scratch_stride;  // global per-CTA scratch
   double* part1 = a.part;
   double* part2 = a.part + (int64_t)ncta * a.pstride;
   double* part3 = a.part + 2 * (int64_t)ncta * a.pstride;
-
-  for (int64_t i = r0 + tid; i < r1; i += NT) a.yprev[i] = 0.0;
-  for (int i = tid; i < PMAX * PMAX; i += NT) sI[i] = 0.0;
   __syncthreads();
 
+  const bool timing = a.dbg != nullptr && cta == 0 && tid == 0;
+  long long tacc[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = timing ? clock64() : 0;
+#define LRK_TSTAMP(k)               \
+  if (timing) {                     \
+    const long long t_ = clock64(); \
+    tacc[k] += t_ - tprev;          \
+    tprev = t_;                     \
+  }
+
+  int r = 0;
+  int jac_sweeps = 0;
   const int nflush = (n_t + p - 1) / p;
   for (int f = 0; f < nflush; ++f) {
     const int start = f * p;
     const int pc = (n_t - start) < p ? (n_t - start) : p;
-    if (tid < pc) sI[tid * pc + tid] = 1.0;  // identity pc x pc (row-major)
-    // ---------------- phase 1: generate the buffered columns (row-local)
-    for (int64_t row = r0 + tid; row < r1; row += NT) {
-      double acc[PMAX];
+    // ---------------- phase 1: buffered columns (row-local) + projections
+    {
+      int ks[Q];
 #pragma unroll
-      for (int s = 0; s < PMAX; ++s) acc[s] = 0.0;
-      for (int j = 0; j < rb; ++j) {
-        const double b = a.B[row + (int64_t)j * a.ldb];
-        const double* w2 = a.W2 + (int64_t)j * a.ldw2;
+      for (int s = 0; s < Q; ++s) ks[s] = a.adjoint ? (n_t - 1 - (start + s)) : (start + s);
+      for (int i = tid; i < m_loc; i += NT) {
+        double acc[Q];
 #pragma unroll
-        for (int s = 0; s < PMAX; ++s) {
+        for (int s = 0; s < Q; ++s) acc[s] = 0.0;
+        for (int j = 0; j < rb; ++j) {
+          const double b = a.B[r0 + i + (int64_t)j * a.ldb];
+          const double* w2 = a.W2 + (int64_t)j * a.ldw2;
+#pragma unroll
+          for (int s = 0; s < Q; ++s)
+            if (s < pc) acc[s] += b * w2[ks[s]];
+        }
+        const double tv = th[i];
+        const double rs = rsc ? rsc[i] : 1.0;
+        double y = yp[i];
+#pragma unroll
+        for (int s = 0; s < Q; ++s) {
           if (s < pc) {
-            const int k = a.adjoint ? (n_t - 1 - (start + s)) : (start + s);
-            acc[s] += b * w2[k];
+            y = tv * y + rs * acc[s];
+            if (fabs(y) < a.ftz) y = 0.0;
+            Yl[i + (int64_t)s * ldy] = y;
           }
         }
+        yp[i] = y;
       }
-      const double th = a.theta[row];
-      const double rs = a.rowscale ? a.rowscale[row] : 1.0;
-      double y = a.yprev[row];
-#pragma unroll
-      for (int s = 0; s < PMAX; ++s) {
-        if (s < pc) {
-          y = th * y + rs * acc[s];
-          a.ybuf[row + (int64_t)s * a.ldy] = y;
-        }
-      }
-      a.yprev[row] = y;
     }
     __syncthreads();
-    double* Yl = a.ybuf + r0;
-    const double* Ul = Ucur + r0;
-    // partial: [U^T Y (r x pc) | ||Y_s||^2 (pc)]
-    if (r > 0) cta_tn(Ul, a.ldu, r, Yl, a.ldy, pc, m_loc, sPart, sScr);
+    if (r > 0) cta_tn(Ul, ldu, r, Yl, ldy, pc, m_loc, sPart, sScr);
     {
-      double v[PMAX];
+      double v[Q];
 #pragma unroll
-      for (int s = 0; s < PMAX; ++s) v[s] = 0.0;
+      for (int s = 0; s < Q; ++s) v[s] = 0.0;
       for (int i = tid; i < m_loc; i += NT) {
 #pragma unroll
-        for (int s = 0; s < PMAX; ++s)
-          if (s < pc) { const double y = Yl[i + (int64_t)s * a.ldy]; v[s] += y * y; }
+        for (int s = 0; s < Q; ++s)
+          if (s < pc) { const double y = Yl[i + (int64_t)s * ldy]; v[s] += y * y; }
       }
-      block_sum<PMAX>(v, sRed, sTmp);
-      if (tid < pc) sPart[r * pc + tid] = v[tid];
+      block_sum<Q>(v, sRed, sTmp);
+      if (tid < pc) sPart[r * pc + tid] = sTmp[tid];
     }
     __syncthreads();
     for (int i = tid; i < r * pc + pc; i += NT) part1[(int64_t)cta * a.pstride + i] = sPart[i];
+    LRK_TSTAMP(0);
     group_barrier(a.bar, ncta);
+    LRK_TSTAMP(1);
     // ---------------- phase 2: block CGS2 against the orthonormal pane
     reduce_partials(part1, a.pstride, ncta, r * pc + pc, sPart);
     for (int i = tid; i < pc; i += NT) sYn[i] = sPart[r * pc + i];
     for (int i = tid; i < r * pc; i += NT) sC[i] = sPart[i];
     __syncthreads();
+    LRK_TSTAMP(9);
     if (r > 0) {
-      rows_sub_gemm(Yl, a.ldy, pc, Ul, a.ldu, r, sC, m_loc);
+      rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
       __syncthreads();
-      cta_tn(Ul, a.ldu, r, Yl, a.ldy, pc, m_loc, sPart, sScr);
+      cta_tn(Ul, ldu, r, Yl, ldy, pc, m_loc, sPart, sScr);
       for (int i = tid; i < r * pc; i += NT) part2[(int64_t)cta * a.pstride + i] = sPart[i];
+      LRK_TSTAMP(10);
       group_barrier(a.bar, ncta);
+      LRK_TSTAMP(11);
       reduce_partials(part2, a.pstride, ncta, r * pc, sPart);
-      rows_sub_gemm(Yl, a.ldy, pc, Ul, a.ldu, r, sPart, m_loc);
+      rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sPart, m_loc);
       for (int i = tid; i < r * pc; i += NT) sC[i] += sPart[i];
       __syncthreads();
     }
+    LRK_TSTAMP(2);
     // ---------------- phase 3: local Householder QR of the remainder
-    block_householder_qr(Yl, a.ldy, m_loc, pc, sTau, sR, sRed, sTmp);
+    block_qr_t<Q>(Yl, ldy, m_loc, pc, sTau, sR, sRed, sTmp);
     for (int i = tid; i < pc * pc; i += NT) part3[(int64_t)cta * a.pstride + i] = sR[i];
+    LRK_TSTAMP(3);
     group_barrier(a.bar, ncta);
-    // ---------------- phase 4 (every CTA, redundantly): finish TSQR + SVD
+    LRK_TSTAMP(4);
+    // ---------------- phase 4 (every CTA, redundantly): finish the TSQR
     const int ms = ncta * pc;
-    if (tid < 32) {
-      for (int idx = tid; idx < ms * pc; idx += 32) {
-        const int c = idx / ms, rr = idx % ms;
-        const int owner = rr / pc, lr = rr % pc;
-        stack[rr + (int64_t)c * ms] = __ldcg(part3 + (int64_t)owner * a.pstride + lr * pc + c);
-      }
-      __syncwarp();
-      warp_householder_qr(stack, ms, ms, pc, sTauT, sRp);
-      // rows of the stacked Q that belong to this CTA
-      warp_householder_q_rows(stack, ms, ms, pc, sTauT, sI, stackY, ms, cta * pc, pc, sQ);
-      if (tid == 0) {
-        // rank-revealing fix-up: Rp P = X Rt (column pivoting)
-        for (int i = 0; i < pc * pc; ++i) sRb[i] = sRp[i];
-        small_pivoted_qr(sRb, pc, sX, iPiv, sCn);
-        double ysq = 0.0;
-        for (int s = 0; s < pc; ++s) ysq += sYn[s];
-        const double delta = 16.0 * DEPS * sqrt(ysq);
-        for (int j = 0; j < pc; ++j) {
-          if (fabs(sRb[j * pc + j]) <= delta) {
-            for (int k = 0; k < pc; ++k) { sRb[j * pc + k] = 0.0; sX[k * pc + j] = 0.0; }
+    double* stack;
+    if constexpr (RES) stack = sm + a.off_scr;
+    else stack = a.stack_smem ? sm + a.off_scr : gscr;
+    double* stackY = stack + ms * pc;
+    {
+      // all loads of the stacked R's are issued before any store
+      constexpr int BATCH = 8;
+      for (int base = 0; base < ms * pc; base += BATCH * NT) {
+        double v[BATCH];
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int idx = base + u * NT + tid;
+          v[u] = 0.0;
+          if (idx < ms * pc) {
+            const int c = idx / ms, rr = idx % ms;
+            v[u] = __ldcg(part3 + (int64_t)(rr / pc) * a.pstride + (rr % pc) * pc + c);
           }
         }
-        // Rblock (original column order) into sRp; G = Qrows * X into sG
-        for (int j = 0; j < pc; ++j)
-          for (int kk = 0; kk < pc; ++kk) sRp[j * pc + iPiv[kk]] = sRb[j * pc + kk];
-        for (int i = 0; i < pc; ++i)
-          for (int j = 0; j < pc; ++j) {
-            double acc = 0.0;
-            for (int k = 0; k < pc; ++k) acc += sQ[i * pc + k] * sX[k * pc + j];
-            sG[i * pc + j] = acc;
-          }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int idx = base + u * NT + tid;
+          if (idx < ms * pc) stack[(idx % ms) + (idx / ms) * ms] = v[u];
+        }
       }
     }
+    for (int i = tid; i < pc * pc; i += NT) sI[i] = (i / pc == i % pc) ? 1.0 : 0.0;
     __syncthreads();
-    // explicit Q~ rows of this CTA: Q_loc * G  -> qbuf
-    block_householder_apply_q(Yl, a.ldy, m_loc, pc, sTau, sG, a.qbuf + r0, a.ldq, sRed, sTmp);
-    // core matrix (n x n, col-major) = [[diag(sig), C], [0, Rblock]]
+    block_qr_t<Q>(stack, ms, ms, pc, sTauT, sRp, sRed, sTmp);
+    block_apply_q_t<Q>(stack, ms, ms, pc, sTauT, sI, stackY, ms, sRed, sTmp);
+    if (tid == 0) {
+      // rows of the stacked Q that belong to this CTA; rank-revealing fix-up
+      // Rp P = X Rt (column pivoting); drop rows at the block's rounding floor
+      for (int i = 0; i < pc; ++i)
+        for (int c = 0; c < pc; ++c) sQs[i * pc + c] = stackY[(cta * pc + i) + c * ms];
+      for (int i = 0; i < pc * pc; ++i) sRb[i] = sRp[i];
+      small_pivoted_qr(sRb, pc, sX, iPiv, sCn);
+      double ysq = 0.0;
+      for (int s = 0; s < pc; ++s) ysq += sYn[s];
+      const double delta = 16.0 * DEPS * sqrt(ysq);
+      for (int j = 0; j < pc; ++j)
+        if (fabs(sRb[j * pc + j]) <= delta)
+          for (int k = 0; k < pc; ++k) { sRb[j * pc + k] = 0.0; sX[k * pc + j] = 0.0; }
+      for (int j = 0; j < pc; ++j)
+        for (int kk = 0; kk < pc; ++kk) sRp[j * pc + iPiv[kk]] = sRb[j * pc + kk];
+      for (int i = 0; i < pc; ++i)
+        for (int j = 0; j < pc; ++j) {
+          double acc = 0.0;
+          for (int k = 0; k < pc; ++k) acc += sQs[i * pc + k] * sX[k * pc + j];
+          sG[i * pc + j] = acc;
+        }
+    }
+    __syncthreads();
+    LRK_TSTAMP(5);
+    // explicit Q~ rows of this CTA: Q_loc * G
+    block_apply_q_t<Q>(Yl, ldy, m_loc, pc, sTau, sG, Ql, ldq, sRed, sTmp);
+    LRK_TSTAMP(6);
+    // ---------------- core SVD: [[diag(sig), C], [0, Rblock]]
     const int n = r + pc;
     if (n > NMAX) {  // uniform across the group; report and stop
       if (tid == 0 && cta == 0) a.info[2] = 1;
       return;
     }
-    double* Aj = (n <= JMAX_SMEM) ? sJac : jacG;
-    double* Vj = Aj + n * n;
-    const int lda = n;
-    for (int idx = tid; idx < n * n; idx += NT) {
-      const int i = idx % n, j = idx / n;
-      double v = 0.0;
-      if (i < r) {
-        if (j < r) v = (i == j) ? sSig[i] : 0.0;
-        else v = sC[i * pc + (j - r)];
-      } else if (j >= r) {
-        v = sRp[(i - r) * pc + (j - r)];
+    double* const Ucs = small + L.Uc;  // compact singular vectors (shared, n <= 32)
+    double* const Vcs = small + L.Vc;
+    double* Ucg = nullptr;             // (global, wide cores)
+    double* Vcg = nullptr;
+    const int ldc = n;
+    if (n <= 32) {
+      double* Uc = Ucs;
+      double* Vc = Vcs;
+      for (int idx = tid; idx < n * n; idx += NT) {
+        const int i = idx % n, j = idx / n;
+        double v = 0.0;
+        if (i < r) v = (j < r) ? (i == j ? sSig[i] : 0.0) : sC[i * pc + (j - r)];
+        else if (j >= r) v = sRp[(i - r) * pc + (j - r)];
+        sCore[i + j * 33] = v;
       }
-      Aj[i + j * lda] = v;
+      __syncthreads();
+      if (warp < 4) {  // 4-warp register Jacobi (named barrier 1), sScr = gbuf
+        if (n <= 8) jac_sweeps += multi_warp_jacobi<8, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
+        else if (n <= 16) jac_sweeps += multi_warp_jacobi<16, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
+        else if (n <= 24) jac_sweeps += multi_warp_jacobi<24, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
+        else jac_sweeps += multi_warp_jacobi<32, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
+      }
+      __syncthreads();
+    } else {
+      double* Aj = gscr + 2 * (int64_t)ncta * PMAX * PMAX;
+      double* Vj = Aj + (int64_t)NMAX * NMAX;
+      for (int idx = tid; idx < n * n; idx += NT) {
+        const int i = idx % n, j = idx / n;
+        double v = 0.0;
+        if (i < r) v = (j < r) ? (i == j ? sSig[i] : 0.0) : sC[i * pc + (j - r)];
+        else if (j >= r) v = sRp[(i - r) * pc + (j - r)];
+        Aj[i + j * n] = v;
+      }
+      __syncthreads();
+      jac_sweeps += jacobi_svd(Aj, n, Vj, n, n, sS, iPerm, sScr, iFlag, sTmp);
+      Ucg = Vj + (int64_t)n * n;
+      Vcg = Ucg + (int64_t)n * n;
+      for (int idx = tid; idx < n * n; idx += NT) {
+        const int i = idx % n, k = idx / n;
+        const double sv = sS[k];
+        Ucg[i + k * ldc] = sv > 0.0 ? Aj[i + iPerm[k] * n] / sv : 0.0;
+        Vcg[i + k * ldc] = Vj[i + iPerm[k] * n];
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    jacobi_svd(Aj, lda, Vj, lda, n, sS, iPerm, sNrm, iFlag);
+    LRK_TSTAMP(7);
     if (tid == 0) {
       double ysq = 0.0, ssq = 0.0;
       for (int s = 0; s < pc; ++s) ysq += sYn[s];
       for (int i = 0; i < r; ++i) ssq += sSig[i] * sSig[i];
       const double fs = sqrt((double)r + ysq) * sqrt(ssq + (double)pc);
       int rn;
-      if (n == 0 || sS[0] <= NOISE_FLOOR * fs) rn = 0;
+      if (sS[0] <= NOISE_FLOOR * fs) rn = 0;
       else rn = rank_cut_dev(sS, n, a.eps0, a.r_max);
-      if (rn > a.ucap) { rn = a.ucap; if (cta == 0) a.info[2] = 2; }
+      if (rn > cap) { rn = cap; if (cta == 0) a.info[2] = 2; }
       iFlag[1] = rn;
-      for (int k = 0; k < rn; ++k) sInv[k] = 1.0 / sS[k];
     }
     __syncthreads();
     const int rn = iFlag[1];
-    // ---------------- basis update (row-local): U' = [U, Q~] Uc[:, :rn]
-    for (int c0 = 0; c0 < rn; c0 += 8) {
-      const int cn = (rn - c0) < 8 ? (rn - c0) : 8;
-      for (int64_t row = r0 + tid; row < r1; row += NT) {
-        double acc[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-        for (int i = 0; i < n; ++i) {
-          const double x = (i < r) ? Ucur[row + (int64_t)i * a.ldu]
-                                   : a.qbuf[row + (int64_t)(i - r) * a.ldq];
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            if (c < cn) acc[c] += x * Aj[i + iPerm[c0 + c] * lda];
+    LRK_TSTAMP(12);
+    // ---------------- basis update in place: U' = [U, Q~] Uc[:, :rn]
+    if (n <= 32 && rn <= 16) {
+      update_rows<16>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      update_time_rows<16>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
+    } else if (n <= 32) {
+      update_rows<32>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      update_time_rows<32>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
+    } else {
+      // wide core: out of place through the global alternates, then copy back
+      const double* Uc = Ucg;
+      const double* Vc = Vcg;
+      for (int c = 0; c < rn; ++c) {
+        for (int i = tid; i < m_loc; i += NT) {
+          double acc = 0.0;
+          for (int k = 0; k < n; ++k)
+            acc += ((k < r) ? Ul[i + (int64_t)k * ldu] : Ql[i + (int64_t)(k - r) * ldq]) * Uc[k + c * ldc];
+          a.U1[r0 + i + (int64_t)c * a.ldu] = acc;
         }
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < cn) Ualt[row + (int64_t)(c0 + c) * a.ldu] = acc[c] * sInv[c0 + c];
+        for (int64_t t = t0 + tid; t < t1; t += NT) {
+          int sel = a.adjoint ? (n_t - 1 - start) - (int)t : (int)t - start;
+          double acc = (sel >= 0 && sel < pc) ? Vc[(r + sel) + c * ldc] : 0.0;
+          for (int k = 0; k < r; ++k) acc += Vl[(t - t0) + (int64_t)k * ldvl] * Vc[k + c * ldc];
+          a.V1[t + (int64_t)c * a.ldv] = acc;
+        }
       }
-      // time basis: V' = [V, E] Vc[:, :rn]
-      for (int64_t t = t0 + tid; t < t1; t += NT) {
-        int sel = a.adjoint ? (n_t - 1 - start) - (int)t : (int)t - start;
-        if (sel < 0 || sel >= pc) sel = -1;
-        double acc[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] = 0.0;
-        for (int i = 0; i < r; ++i) {
-          const double x = Vcur[t + (int64_t)i * a.ldv];
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            if (c < cn) acc[c] += x * Vj[i + iPerm[c0 + c] * lda];
-        }
-        if (sel >= 0) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            if (c < cn) acc[c] += Vj[(r + sel) + iPerm[c0 + c] * lda];
-        }
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c < cn) Valt[t + (int64_t)(c0 + c) * a.ldv] = acc[c];
+      __syncthreads();
+      for (int c = 0; c < rn; ++c) {
+        for (int i = tid; i < m_loc; i += NT) Ul[i + (int64_t)c * ldu] = a.U1[r0 + i + (int64_t)c * a.ldu];
+        for (int64_t t = t0 + tid; t < t1; t += NT) Vl[(t - t0) + (int64_t)c * ldvl] = a.V1[t + (int64_t)c * a.ldv];
       }
     }
     for (int k = tid; k < rn; k += NT) sSig[k] = sS[k];
     if (tid == 0 && cta == 0) a.trace[f] = rn;
     __syncthreads();
     r = rn;
-    { double* t = Ucur; Ucur = Ualt; Ualt = t; }
-    { double* t = Vcur; Vcur = Valt; Valt = t; }
-    if (tid < pc) sI[tid * pc + tid] = 0.0;
-    __syncthreads();
+    LRK_TSTAMP(8);
   }
-  // leave the result in slot 0 (row-local copies, no barrier needed)
-  if (Ucur != a.U0) {
+  if (timing)
+    for (int k = 0; k < 14; ++k) a.dbg[k] = tacc[k];
+#undef LRK_TSTAMP
+  // the pane: resident U rows go back to global slot 0
+  if (res)
     for (int c = 0; c < r; ++c) {
-      for (int64_t i = r0 + tid; i < r1; i += NT) a.U0[i + (int64_t)c * a.ldu] = Ucur[i + (int64_t)c * a.ldu];
-      for (int64_t t = t0 + tid; t < t1; t += NT) a.V0[t + (int64_t)c * a.ldv] = Vcur[t + (int64_t)c * a.ldv];
+      for (int i = tid; i < m_loc; i += NT) a.U0[r0 + i + (int64_t)c * a.ldu] = Ul[i + (int64_t)c * ldu];
+      for (int64_t t = t0 + tid; t < t1; t += NT)
+        a.V0[t + (int64_t)c * a.ldv] = Vl[(t - t0) + (int64_t)c * ldvl];
     }
-  }
   if (cta == 0) {
     for (int k = tid; k < r; k += NT) a.sigma[k] = sSig[k];
     if (tid == 0) {
       a.info[0] = r;
       a.info[1] = 0;
+      a.info[3] = jac_sweeps;
       a.trace[nflush] = r;
     }
   }
 }
 
-cudaError_t launch_sweep(const SweepArgs* d_args, int ngroups, int ncta, cudaStream_t s) {
-  static bool attr_set = false;
-  const size_t smem = SweepSmem::bytes;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+template <int Q, bool RES>
+static cudaError_t launch_q(const SweepBatch& batch, cudaStream_t s) {
+  static int attr_bytes = 0;
+  const int smem = batch.g[0].smem_doubles * (int)sizeof(double);
+  if (smem > attr_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<Q, RES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_bytes = smem;
   }
-  void* params[] = {(void*)&d_args};
-  return cudaLaunchCooperativeKernel((const void*)sweep_kernel, dim3(ngroups * ncta), dim3(NT),
-                                     params, smem, s);
+  void* params[] = {(void*)&batch};
+  return cudaLaunchCooperativeKernel((const void*)sweep_kernel<Q, RES>,
+                                     dim3(batch.ngroups * batch.g[0].ncta), dim3(NT), params,
+                                     (size_t)smem, s);
+}
+
+template <bool RES>
+static cudaError_t launch_r(const SweepBatch& batch, cudaStream_t s) {
+  const int p = batch.g[0].p;
+  if (p <= 1) return launch_q<1, RES>(batch, s);
+  if (p <= 2) return launch_q<2, RES>(batch, s);
+  if (p <= 4) return launch_q<4, RES>(batch, s);
+  if (p <= 8) return launch_q<8, RES>(batch, s);
+  return launch_q<16, RES>(batch, s);
+}
+
+cudaError_t launch_sweep(const SweepBatch& batch, cudaStream_t s) {
+  return batch.g[0].resident ? launch_r<true>(batch, s) : launch_r<false>(batch, s);
 }
 
 }  // namespace lrk

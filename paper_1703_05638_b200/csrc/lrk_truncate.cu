@@ -169,9 +169,8 @@ __device__ void group_blocked_qr(const double* X, int64_t ldx, int64_t N, int R,
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) truncate_kernel(const TruncArgs* __restrict__ pa) {
+__global__ void __launch_bounds__(NT, 1) truncate_kernel(const __grid_constant__ TruncArgs a) {
   extern __shared__ double sm[];
-  const TruncArgs& a = *pa;
   const int ncta = a.ncta, cta = blockIdx.x, tid = threadIdx.x;
   TS s;
   s.C = sm + TruncSmem::off_C; s.Yn = sm + TruncSmem::off_Yn; s.R = sm + TruncSmem::off_R;
@@ -257,7 +256,7 @@ __global__ void __launch_bounds__(NT, 1) truncate_kernel(const TruncArgs* __rest
     if (tid == 0) s.misc[0] = sqrt(v[0]) * sqrt(v[1]);
   }
   __syncthreads();
-  jacobi_svd(Aj, n, Vj, n, n, s.s, s.perm, s.nrm, s.flag);
+  jacobi_svd(Aj, n, Vj, n, n, s.s, s.perm, s.nrm, s.flag, s.tmp);
   if (tid == 0) {
     int rn;
     if (n == 0 || s.s[0] <= NOISE_FLOOR * s.misc[0]) rn = 0;
@@ -350,7 +349,7 @@ __global__ void __launch_bounds__(NT, 1) truncate_kernel(const TruncArgs* __rest
   if (cta == 0 && tid == 0) a.info[0] = rn;
 }
 
-cudaError_t launch_truncate(const TruncArgs* d_args, int ncta, cudaStream_t st) {
+cudaError_t launch_truncate(const TruncArgs& args, cudaStream_t st) {
   static bool attr_set = false;
   const size_t smem = TruncSmem::bytes;
   if (!attr_set) {
@@ -359,8 +358,8 @@ cudaError_t launch_truncate(const TruncArgs* d_args, int ncta, cudaStream_t st) 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  void* params[] = {(void*)&d_args};
-  return cudaLaunchCooperativeKernel((const void*)truncate_kernel, dim3(ncta), dim3(NT), params,
+  void* params[] = {(void*)&args};
+  return cudaLaunchCooperativeKernel((const void*)truncate_kernel, dim3(args.ncta), dim3(NT), params,
                                      smem, st);
 }
 
