@@ -423,11 +423,12 @@ int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOu
     long long fd[16], gd[16];
     CK(cudaMemcpy(fd, f.dbg, sizeof(fd), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(gd, g.dbg, sizeof(gd), cudaMemcpyDeviceToHost));
-    const char* names[13] = {"gen+proj1", "barrier1", "reduce2+sub2", "hh_local", "barrier3",
-                             "stackQR", "apply_q", "core+jacobi", "update", "reduce1",
-                             "sub1+tn2", "barrier2", "rankcut"};
+    const char* names[16] = {"gen+proj1", "barrier1", "reduce2+sub2", "hh_local", "barrier3",
+                             "stack_tail", "apply_q", "core+jacobi", "update", "reduce1",
+                             "sub1+tn2", "barrier2", "rankcut", "stack_copy", "stack_qr",
+                             "stack_q"};
     std::fprintf(stderr, "[lrk] cycles/flush (fwd | bwd):");
-    for (int k = 0; k < 13; ++k)
+    for (int k = 0; k < 16; ++k)
       std::fprintf(stderr, " %s %lld|%lld", names[k], fd[k] / std::max(1, f.nflush),
                    gd[k] / std::max(1, g.nflush));
     std::fprintf(stderr, "\n");

@@ -97,13 +97,25 @@ __device__ inline void block_sum_rt(double* vals, int K, double* red, double* ou
 __device__ __forceinline__ void reduce_partials(const double* part, int64_t stride, int ncta,
                                        int len, double* out) {
   int lp = 1;
-  while (lp < 32 && lp * 2 * len <= NT) lp *= 2;
+  while (lp < 32 && lp * 2 * len <= NT) lp *= 2;  // keeps lp * len <= NT
   const int tid = threadIdx.x;
   if (lp > 1) {
     const int o = tid / lp, sub = tid % lp;
     double acc = 0.0;
-    if (o < len)
-      for (int c = sub; c < ncta; c += lp) acc += __ldcg(part + (int64_t)c * stride + o);
+    if (o < len) {
+      // issue a batch of independent L2 loads before summing (latency-bound)
+      constexpr int B = 16;
+      for (int c0 = sub; c0 < ncta; c0 += B * lp) {
+        double v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int c = c0 + u * lp;
+          v[u] = (c < ncta) ? __ldcg(part + (int64_t)c * stride + o) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) acc += v[u];
+      }
+    }
     for (int m = lp >> 1; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
     if (o < len && sub == 0) out[o] = acc;
   } else {

@@ -291,6 +291,83 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
   return nsweep;
 }
 
+// Column-pivoted Householder QR of the q x q (q <= Q) matrix A held in
+// registers by one thread (compile-time unrolled, no local memory):
+// A P = X Rt.  On exit A = Rt (upper), X orthogonal, perm[k] = source column
+// of Rt's column k.  Used for the rank-revealing fix-up of the TSQR's R.
+template <int Q>
+__device__ __forceinline__ void pivoted_qr_reg(double (&A)[Q][Q], int q, double (&X)[Q][Q],
+                                               int (&perm)[Q]) {
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    perm[i] = i;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) X[i][k] = (i == k) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    if (j >= q) break;
+    // pivot: largest trailing column norm (exact)
+    double best = -1.0;
+    int piv = j;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      if (k < j || k >= q) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+        if (i >= j && i < q) s += A[i][k] * A[i][k];
+      if (s > best) { best = s; piv = k; }
+    }
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      if (k == piv && k != j) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) { const double t = A[i][j]; A[i][j] = A[i][k]; A[i][k] = t; }
+        const int t = perm[j]; perm[j] = perm[k]; perm[k] = t;
+      }
+    }
+    double sig = 0.0, alpha = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      if (i > j && i < q) sig += A[i][j] * A[i][j];
+      if (i == j) alpha = A[i][j];
+    }
+    if (sig == 0.0) continue;
+    const double nrm = sqrt(alpha * alpha + sig);
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    const double tau = (beta - alpha) / beta;
+    const double sc = 1.0 / (alpha - beta);
+    double v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = (i == j) ? 1.0 : ((i > j && i < q) ? A[i][j] * sc : 0.0);
+    // A <- H A on columns >= j
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      if (k < j || k >= q) continue;
+      double w = 0.0;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) w += v[i] * A[i][k];
+      w *= tau;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) A[i][k] -= w * v[i];
+    }
+    // X <- X H
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      double w = 0.0;
+#pragma unroll
+      for (int l = 0; l < Q; ++l) w += X[i][l] * v[l];
+      w *= tau;
+#pragma unroll
+      for (int l = 0; l < Q; ++l) X[i][l] -= w * v[l];
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+      if (i > j) A[i][j] = 0.0;
+  }
+}
+
 // Householder QR (optionally with column pivoting) of an n x n matrix held by
 // ONE warp in registers, lane j = column j (a[i] = entry i, zero padded to
 // NJ).  On exit a[] holds column `lane` of R; the reflector of step j is

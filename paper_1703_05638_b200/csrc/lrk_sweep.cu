@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
   __syncthreads();
 
   const bool timing = a.dbg != nullptr && cta == 0 && tid == 0;
-  long long tacc[14] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = timing ? clock64() : 0;
 #define LRK_TSTAMP(k)               \
   if (timing) {                     \
@@ -340,50 +340,86 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     double* stackY = stack + ms * pc;
     {
       // all loads of the stacked R's are issued before any store
-      constexpr int BATCH = 8;
-      for (int base = 0; base < ms * pc; base += BATCH * NT) {
+      constexpr int BATCH = 16;
+      const int pp = pc * pc, tot = ms * pc;
+      for (int base = 0; base < tot; base += BATCH * NT) {
         double v[BATCH];
 #pragma unroll
         for (int u = 0; u < BATCH; ++u) {
           const int idx = base + u * NT + tid;
-          v[u] = 0.0;
-          if (idx < ms * pc) {
-            const int c = idx / ms, rr = idx % ms;
-            v[u] = __ldcg(part3 + (int64_t)(rr / pc) * a.pstride + (rr % pc) * pc + c);
-          }
+          v[u] = (idx < tot) ? __ldcg(part3 + (int64_t)(idx / pp) * a.pstride + idx % pp) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < BATCH; ++u) {
           const int idx = base + u * NT + tid;
-          if (idx < ms * pc) stack[(idx % ms) + (idx / ms) * ms] = v[u];
+          if (idx < tot) {
+            const int owner = idx / pp, e = idx % pp;  // e = lr * pc + c
+            stack[(owner * pc + e / pc) + (e % pc) * ms] = v[u];
+          }
         }
       }
     }
     for (int i = tid; i < pc * pc; i += NT) sI[i] = (i / pc == i % pc) ? 1.0 : 0.0;
     __syncthreads();
+    LRK_TSTAMP(13);
     block_qr_t<Q>(stack, ms, ms, pc, sTauT, sRp, sRed, sTmp);
+    LRK_TSTAMP(14);
     block_apply_q_t<Q>(stack, ms, ms, pc, sTauT, sI, stackY, ms, sRed, sTmp);
+    LRK_TSTAMP(15);
     if (tid == 0) {
       // rows of the stacked Q that belong to this CTA; rank-revealing fix-up
       // Rp P = X Rt (column pivoting); drop rows at the block's rounding floor
-      for (int i = 0; i < pc; ++i)
-        for (int c = 0; c < pc; ++c) sQs[i * pc + c] = stackY[(cta * pc + i) + c * ms];
-      for (int i = 0; i < pc * pc; ++i) sRb[i] = sRp[i];
-      small_pivoted_qr(sRb, pc, sX, iPiv, sCn);
       double ysq = 0.0;
       for (int s = 0; s < pc; ++s) ysq += sYn[s];
       const double delta = 16.0 * DEPS * sqrt(ysq);
-      for (int j = 0; j < pc; ++j)
-        if (fabs(sRb[j * pc + j]) <= delta)
-          for (int k = 0; k < pc; ++k) { sRb[j * pc + k] = 0.0; sX[k * pc + j] = 0.0; }
-      for (int j = 0; j < pc; ++j)
-        for (int kk = 0; kk < pc; ++kk) sRp[j * pc + iPiv[kk]] = sRb[j * pc + kk];
-      for (int i = 0; i < pc; ++i)
-        for (int j = 0; j < pc; ++j) {
-          double acc = 0.0;
-          for (int k = 0; k < pc; ++k) acc += sQs[i * pc + k] * sX[k * pc + j];
-          sG[i * pc + j] = acc;
-        }
+      if constexpr (Q <= 8) {
+        double A[Q][Q], X[Q][Q], Qr[Q][Q];
+        int pv[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            A[i][k] = (i < pc && k < pc) ? sRp[i * pc + k] : 0.0;
+            Qr[i][k] = (i < pc && k < pc) ? stackY[(cta * pc + i) + k * ms] : 0.0;
+          }
+        pivoted_qr_reg<Q>(A, pc, X, pv);
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+          if (fabs(A[j][j]) <= delta) {
+#pragma unroll
+            for (int k = 0; k < Q; ++k) { A[j][k] = 0.0; X[k][j] = 0.0; }
+          }
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+#pragma unroll
+          for (int kk = 0; kk < Q; ++kk)
+            if (j < pc && kk < pc) sRp[j * pc + pv[kk]] = A[j][kk];
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+          for (int j = 0; j < Q; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) acc += Qr[i][k] * X[k][j];
+            if (i < pc && j < pc) sG[i * pc + j] = acc;
+          }
+      } else {
+        for (int i = 0; i < pc; ++i)
+          for (int c = 0; c < pc; ++c) sQs[i * pc + c] = stackY[(cta * pc + i) + c * ms];
+        for (int i = 0; i < pc * pc; ++i) sRb[i] = sRp[i];
+        small_pivoted_qr(sRb, pc, sX, iPiv, sCn);
+        for (int j = 0; j < pc; ++j)
+          if (fabs(sRb[j * pc + j]) <= delta)
+            for (int k = 0; k < pc; ++k) { sRb[j * pc + k] = 0.0; sX[k * pc + j] = 0.0; }
+        for (int j = 0; j < pc; ++j)
+          for (int kk = 0; kk < pc; ++kk) sRp[j * pc + iPiv[kk]] = sRb[j * pc + kk];
+        for (int i = 0; i < pc; ++i)
+          for (int j = 0; j < pc; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < pc; ++k) acc += sQs[i * pc + k] * sX[k * pc + j];
+            sG[i * pc + j] = acc;
+          }
+      }
     }
     __syncthreads();
     LRK_TSTAMP(5);
@@ -494,7 +530,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     LRK_TSTAMP(8);
   }
   if (timing)
-    for (int k = 0; k < 14; ++k) a.dbg[k] = tacc[k];
+    for (int k = 0; k < 16; ++k) a.dbg[k] = tacc[k];
 #undef LRK_TSTAMP
   // the pane: resident U rows go back to global slot 0
   if (res)
