@@ -238,7 +238,7 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   a.bar = bar; a.ncta = ncta;
   sweep_plan(a, nx, ncta, ucap, p, (size_t)c->smem_optin);
   a.ftz = std::getenv("LRK_FTZ") ? std::atof(std::getenv("LRK_FTZ")) : 0.0;
-  WS(long long, dbg, tag + "dbg", 16);
+  WS(long long, dbg, tag + "dbg", 20);
   a.dbg = std::getenv("LRK_DEBUG") ? dbg : nullptr;
   o.dbg = dbg;
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
@@ -420,15 +420,15 @@ int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOu
     CK(cudaMemcpy(gi, g.info, sizeof(gi), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "[lrk] apply: ranks fwd %d obs %d bwd %d; jacobi sweeps fwd %d bwd %d over %d+%d flushes\n",
                  fi[0], zr[0], gi[0], fi[3], gi[3], f.nflush, g.nflush);
-    long long fd[16], gd[16];
+    long long fd[20], gd[20];
     CK(cudaMemcpy(fd, f.dbg, sizeof(fd), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(gd, g.dbg, sizeof(gd), cudaMemcpyDeviceToHost));
-    const char* names[16] = {"gen+proj1", "barrier1", "reduce2+sub2", "hh_local", "barrier3",
+    const char* names[20] = {"gen+proj1", "barrier1", "reduce2+sub2", "hh_local", "barrier3",
                              "stack_tail", "apply_q", "core+jacobi", "update", "reduce1",
                              "sub1+tn2", "barrier2", "rankcut", "stack_copy", "stack_qr",
-                             "stack_q"};
+                             "stack_q", "stack_copy_warm", "x17", "x18", "x19"};
     std::fprintf(stderr, "[lrk] cycles/flush (fwd | bwd):");
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < 20; ++k)
       std::fprintf(stderr, " %s %lld|%lld", names[k], fd[k] / std::max(1, f.nflush),
                    gd[k] / std::max(1, g.nflush));
     std::fprintf(stderr, "\n");

@@ -291,6 +291,58 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
   return nsweep;
 }
 
+// ----------------------------------------------------------- DMMA helpers
+// FP64 tensor-core MMA (sm_100a has no tcgen05 f64 kind; this is SASS DMMA):
+// D(8x8) += A(8x4, row) * B(4x8, col).  Fragments: a = A[g][t], b = B[t][g],
+// d0,d1 = D[g][2t], D[g][2t+1] with g = lane>>2, t = lane&3.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// In-place row update on the tensor pipe: rows [0, m) of X = [A (na cols) | B
+// (nb cols)] (column-major, lda/ldb) times W (n x rn, col-major ld ldw) are
+// written into A's first rn columns (rn <= 8*NT8).  Each warp owns whole
+// 8-row tiles, so every row is read (into fragments) before the warp writes
+// it.  Called by all threads of the CTA.
+template <int NT8>
+__device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t lda, int na,
+                                                 const double* __restrict__ B, int64_t ldb, int nb,
+                                                 const double* __restrict__ W, int ldw, int rn,
+                                                 int m) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int n = na + nb;
+  const int ntile = (m + 7) >> 3;
+  for (int tile = warp; tile < ntile; tile += NWARP) {
+    const int row = tile * 8 + g;
+    double acc[NT8][2];
+#pragma unroll
+    for (int j = 0; j < NT8; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int k0 = 0; k0 < n; k0 += 4) {
+      const int k = k0 + t;
+      double a = 0.0;
+      if (row < m && k < n) a = (k < na) ? A[row + (int64_t)k * lda] : B[row + (int64_t)(k - na) * ldb];
+#pragma unroll
+      for (int j = 0; j < NT8; ++j) {
+        const int col = j * 8 + g;
+        const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
+        dmma884(acc[j][0], acc[j][1], a, b);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NT8; ++j) {
+      const int c0 = j * 8 + 2 * t;
+      if (row < m) {
+        if (c0 < rn) A[row + (int64_t)c0 * lda] = acc[j][0];
+        if (c0 + 1 < rn) A[row + (int64_t)(c0 + 1) * lda] = acc[j][1];
+      }
+    }
+  }
+}
+
 // Column-pivoted Householder QR of the q x q (q <= Q) matrix A held in
 // registers by one thread (compile-time unrolled, no local memory):
 // A P = X Rt.  On exit A = Rt (upper), X orthogonal, perm[k] = source column
@@ -375,7 +427,8 @@ __device__ __forceinline__ void pivoted_qr_reg(double (&A)[Q][Q], int q, double 
 // colid returns the original column index of the lane (pivot permutation).
 template <int NJ, bool PIVOT>
 __device__ __forceinline__ void warp_qr_cols(double (&a)[NJ], int n, double* __restrict__ Vh,
-                                             int ldv, double* __restrict__ tau, int& colid) {
+                                             int ldv, double* __restrict__ tau, int& colid,
+                                             bool writer = true) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   colid = lane;
@@ -393,12 +446,12 @@ __device__ __forceinline__ void warp_qr_cols(double (&a)[NJ], int n, double* __r
         const int oi = __shfl_xor_sync(full, idx, o);
         if (ot > tn || (ot == tn && oi < idx)) { tn = ot; idx = oi; }
       }
-      if (idx != j) {  // uniform: swap columns j and idx
-        const int src = (lane == j) ? idx : ((lane == idx) ? j : lane);
+      // swap columns j and idx (identity shuffle when idx == j; kept
+      // unconditional so it compiles to plain SHFL)
+      const int src = (lane == j) ? idx : ((lane == idx) ? j : lane);
 #pragma unroll
-        for (int i = 0; i < NJ; ++i) a[i] = __shfl_sync(full, a[i], src);
-        colid = __shfl_sync(full, colid, src);
-      }
+      for (int i = 0; i < NJ; ++i) a[i] = __shfl_sync(full, a[i], src);
+      colid = __shfl_sync(full, colid, src);
     }
     double x[NJ];
 #pragma unroll
@@ -434,16 +487,203 @@ __device__ __forceinline__ void warp_qr_cols(double (&a)[NJ], int n, double* __r
 #pragma unroll
       for (int i = 0; i < NJ; ++i) {
         if (i > j) {
-          Vh[i + j * ldv] = x[i] * scale;
+          if (writer) Vh[i + j * ldv] = x[i] * scale;
           a[i] = 0.0;
         }
         if (i == j) a[i] = beta;
       }
-      tau[j] = t;
+      if (writer) tau[j] = t;
     }
   }
-  if (lane == 0) tau[n - 1] = 0.0;
+  if (lane == 0 && writer) tau[n - 1] = 0.0;
   __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident warp Householder QR of a tall chunk: lane l holds rows
+// l + 32k (k < ROWS) of an (32*ROWS) x q matrix (q <= Q, zero rows padded).
+// Same reflector convention as block_qr_t (beta = -sign(alpha) ||x||); on exit
+// rows i > j of column j hold v_i (unit v_j implicit), rows <= j of columns
+// >= j hold R (lanes < q, k = 0), tau[j] in every lane.
+template <int Q, int ROWS>
+__device__ __forceinline__ void warp_hh_regs(double (&x)[ROWS][Q], int q, double (&tau)[Q]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    tau[j] = 0.0;
+    if (j >= q) continue;  // uniform
+    double s[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) s[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const bool below = (lane + 32 * k) > j;
+#pragma unroll
+      for (int c = j; c < Q; ++c)
+        if (below) s[c] += x[k][j] * x[k][c];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = j; c < Q; ++c) s[c] += __shfl_xor_sync(full, s[c], o);
+    double xr[Q];
+#pragma unroll
+    for (int c = j; c < Q; ++c) xr[c] = __shfl_sync(full, x[0][c], j);
+    const double alpha = xr[j], sig = s[j];
+    double beta = alpha, t = 0.0, scale = 0.0;
+    if (sig != 0.0) {
+      const double nrm = sqrt(alpha * alpha + sig);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    double f[Q];
+#pragma unroll
+    for (int c = j + 1; c < Q; ++c) f[c] = (c < q) ? t * (xr[c] + scale * s[c]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int i = lane + 32 * k;
+      if (i > j) {
+        const double v = x[k][j] * scale;
+        x[k][j] = v;
+#pragma unroll
+        for (int c = j + 1; c < Q; ++c) x[k][c] -= f[c] * v;
+      } else if (i == j) {
+#pragma unroll
+        for (int c = j + 1; c < Q; ++c) x[k][c] = xr[c] - f[c];
+        x[k][j] = beta;
+      }
+    }
+    tau[j] = t;
+  }
+}
+
+// y <- H_0 ... H_{q-1} y for the reflectors left in x by warp_hh_regs.
+template <int Q, int ROWS>
+__device__ __forceinline__ void warp_apply_hh_regs(const double (&x)[ROWS][Q], int q,
+                                                   const double (&tau)[Q], double (&y)[ROWS][Q]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+#pragma unroll
+  for (int j = Q - 1; j >= 0; --j) {
+    if (j >= q || tau[j] == 0.0) continue;  // uniform
+    double w[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) w[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int i = lane + 32 * k;
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        if (i > j) w[c] += x[k][j] * y[k][c];
+        else if (i == j) w[c] += y[k][c];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < Q; ++c) w[c] += __shfl_xor_sync(full, w[c], o);
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int i = lane + 32 * k;
+      const double v = (i > j) ? x[k][j] : ((i == j) ? 1.0 : 0.0);
+#pragma unroll
+      for (int c = 0; c < Q; ++c) y[k][c] -= tau[j] * w[c] * v;
+    }
+  }
+}
+
+// Stacked TSQR of the per-CTA R blocks of a flush (ncta blocks of pc x pc,
+// block o row-major at part[o*pstride]), two levels, all in registers:
+// warp w factors blocks [w*cpw, (w+1)*cpw) (lane = stacked row, loaded
+// straight from L2), publishes its R_w in sRw (NWARP*Q*Q doubles, shared);
+// after the CTA barrier the warp that owns block `me` factors the NWARP
+// stacked R_w's (<= 32 rows) into Rout and forms rows me*pc.. of the stacked
+// Q (= Q_w * (rows of Q_top)) into Qout (both pc x pc row-major, shared).
+// Returns the owner warp.  Requires cpw*Q <= 32*ROWS and NWARP*Q <= 32.
+template <int Q, int ROWS>
+__device__ __forceinline__ int warp_stack_tsqr(const double* __restrict__ part, int64_t pstride,
+                                               int ncta, int pc, int me, double* __restrict__ sRw,
+                                               double* __restrict__ Rout,
+                                               double* __restrict__ Qout) {
+  static_assert(NWARP * Q <= 32, "top level must fit one warp");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cpw = (ncta + NWARP - 1) / NWARP;
+  const int wo = me / cpw;
+  const int b0 = w * cpw;
+  int nb = ncta - b0;
+  nb = nb < 0 ? 0 : (nb > cpw ? cpw : nb);
+  const int rows = nb * pc;
+  double x[ROWS][Q];
+#pragma unroll
+  for (int k = 0; k < ROWS; ++k) {
+    const int i = lane + 32 * k;
+    const int o = i / pc, lr = i - o * pc;
+    const double* src = part + (int64_t)(b0 + o) * pstride + lr * pc;
+#pragma unroll
+    for (int c = 0; c < Q; ++c) x[k][c] = (i < rows && c < pc) ? __ldcg(src + c) : 0.0;
+  }
+  double tau[Q];
+  warp_hh_regs<Q, ROWS>(x, pc, tau);
+  if (lane < Q) {
+#pragma unroll
+    for (int c = 0; c < Q; ++c) sRw[(w * Q + lane) * Q + c] = (c >= lane && lane < pc) ? x[0][c] : 0.0;
+  }
+  __syncthreads();
+  if (w == wo) {
+    // top level: row l = (warp l/Q, row l%Q) of the stacked R_w (pc-strided)
+    double xt[1][Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) xt[0][c] = sRw[lane * Q + c];
+    // compact the rows so that the live ones are contiguous (row index tw*pc+tl)
+    double xc[1][Q];
+    {
+      // destination row d = lane takes source row (d/pc)*Q + d%pc
+      const int sw = lane / pc, sl = lane - sw * pc;
+      const int sidx = (sw < NWARP) ? (sw * Q + sl) : 31;
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        const double v = __shfl_sync(0xffffffffu, xt[0][c], sidx & 31);
+        xc[0][c] = (sw < NWARP) ? v : 0.0;
+      }
+    }
+    double tt[Q];
+    warp_hh_regs<Q, 1>(xc, pc, tt);
+    if (lane < pc) {
+#pragma unroll
+      for (int c = 0; c < Q; ++c)
+        if (c < pc) Rout[lane * pc + c] = (c >= lane) ? xc[0][c] : 0.0;
+    }
+    // rows wo*pc .. wo*pc+pc-1 of Q_top = H..[I; 0]
+    double e[1][Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) e[0][c] = (lane == c && c < pc) ? 1.0 : 0.0;
+    warp_apply_hh_regs<Q, 1>(xc, pc, tt, e);
+    double y[ROWS][Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) {
+      const double tv = __shfl_sync(0xffffffffu, e[0][c], (wo * pc + lane) & 31);
+      y[0][c] = (lane < pc) ? tv : 0.0;
+    }
+#pragma unroll
+    for (int k = 1; k < ROWS; ++k)
+#pragma unroll
+      for (int c = 0; c < Q; ++c) y[k][c] = 0.0;
+    warp_apply_hh_regs<Q, ROWS>(x, pc, tau, y);
+    const int base = (me - b0) * pc;
+#pragma unroll
+    for (int k = 0; k < ROWS; ++k) {
+      const int i = lane + 32 * k - base;
+      if (i >= 0 && i < pc) {
+#pragma unroll
+        for (int c = 0; c < Q; ++c)
+          if (c < pc) Qout[i * pc + c] = y[k][c];
+      }
+    }
+    __syncwarp();
+  }
+  return wo;
 }
 
 // Same algorithm as warp_jacobi_reg, executed by JW warps (threads
@@ -547,14 +787,16 @@ __device__ __forceinline__ int multi_warp_jacobi(const double* __restrict__ Ain,
           rot = true;
         }
       }
-      if (__any_sync(full, rot)) {
+      // unconditional update (c = 1, sl = 0 leaves a column bit-identical):
+      // shuffles outside data-dependent branches compile to plain SHFL
 #pragma unroll
-        for (int k = 0; k < NR; ++k) {
-          a[k] = c * a[k] + sl * ap[k];
-          const double vp = __shfl_sync(full, v[k], p & 31);
-          v[k] = c * v[k] + sl * vp;
-        }
-        if (rot) nrm = lo ? (al - t * g) : (be + t * g);
+      for (int k = 0; k < NR; ++k) {
+        a[k] = c * a[k] + sl * ap[k];
+        const double vp = __shfl_sync(full, v[k], p & 31);
+        v[k] = c * v[k] + sl * vp;
+      }
+      if (rot) {
+        nrm = lo ? (al - t * g) : (be + t * g);
         rotated = true;
       }
     }
@@ -592,11 +834,10 @@ __device__ __forceinline__ int multi_warp_jacobi(const double* __restrict__ Ain,
 //   R1^T = Q2 R2 (unpivoted QR),
 //   X = R2^T,  X W = U_X diag(s)  (multi-warp Jacobi, typically ~2 sweeps
 //   instead of ~6 on the raw core),
-// so M = (Q1 U_X) diag(s) (P Q2 W)^T.  Executed by warps 0..3 (threads
-// [0,128)); the caller synchronises the CTA afterwards.  Outputs as
-// warp_jacobi_reg: Uo[:, k], Vo[:, k] (ld ldo), s_sorted (descending).
-// scr: PRECOND_SCR doubles of shared memory.
-constexpr int PRECOND_SCR = 5 * 32 * 33 + 2 * 32 + 2 * 4 * 32 + 32;
+// so M = (Q1 U_X) diag(s) (P Q2 W)^T.  Executed by ALL threads of the CTA
+// (no divergent call site).  Outputs as warp_jacobi_reg: Uo[:, k], Vo[:, k]
+// (ld ldo), s_sorted (descending).  scr: PRECOND_SCR doubles of shared memory.
+constexpr int PRECOND_SCR = 5 * 32 * 33 + 2 * 32 + 2 * NWARP * 32 + 32;
 template <int NJ>
 __device__ __forceinline__ int precond_svd(const double* __restrict__ core, int ldm, int n,
                                            double* __restrict__ Uo, double* __restrict__ Vo,
@@ -611,34 +852,41 @@ __device__ __forceinline__ int precond_svd(const double* __restrict__ core, int 
   double* t1 = Wj + 32 * L;
   double* t2 = t1 + 32;
   double* gbuf = t2 + 32;
-  int* P = reinterpret_cast<int*>(gbuf + 2 * 4 * 32);
+  int* P = reinterpret_cast<int*>(gbuf + 2 * NWARP * 32);
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < 32) {
+  const bool w0 = tid < 32;
+  {
+    // every warp runs the two register QRs redundantly (no divergent shuffle
+    // paths); warp 0 publishes the reflectors, permutation and R2^T
     double a[NJ];
 #pragma unroll
     for (int i = 0; i < NJ; ++i) a[i] = (lane < n && i < n) ? core[i + lane * ldm] : 0.0;
     int colid;
-    warp_qr_cols<NJ, true>(a, n, V1, L, t1, colid);
-    if (lane < n) P[lane] = colid;
-    // X = R1^T (column i of X = row i of R1)
+    warp_qr_cols<NJ, true>(a, n, V1, L, t1, colid, w0);
+    if (w0 && lane < n) P[lane] = colid;
+    // R1^T through shared memory: column i of R1^T = row i of R1
+    if (w0) {
 #pragma unroll
-    for (int i = 0; i < NJ; ++i)
-      if (lane < n && i < n) X[lane + i * L] = a[i];
-    __syncwarp();
+      for (int i = 0; i < NJ; ++i)
+        if (lane < n && i < n) X[lane + i * L] = a[i];
+    }
+    __syncthreads();
+    double b[NJ];
 #pragma unroll
-    for (int i = 0; i < NJ; ++i) a[i] = (lane < n && i < n) ? X[i + lane * L] : 0.0;
-    __syncwarp();
+    for (int i = 0; i < NJ; ++i) b[i] = (lane < n && i < n) ? X[i + lane * L] : 0.0;
+    __syncthreads();
     int dummy;
-    warp_qr_cols<NJ, false>(a, n, V2, L, t2, dummy);
+    warp_qr_cols<NJ, false>(b, n, V2, L, t2, dummy, w0);
     // X = R2^T
+    if (w0) {
 #pragma unroll
-    for (int i = 0; i < NJ; ++i)
-      if (lane < n && i < n) X[lane + i * L] = a[i];
+      for (int i = 0; i < NJ; ++i)
+        if (lane < n && i < n) X[lane + i * L] = b[i];
+    }
   }
-  int nsw = 0;
-  if (tid < 128) {
-    asm volatile("bar.sync 1, 128;");
-    nsw = multi_warp_jacobi<NJ, 4>(X, L, n, Uj, Wj, L, s_sorted, perm, gbuf);
+  __syncthreads();
+  int nsw = multi_warp_jacobi<NJ, NWARP>(X, L, n, Uj, Wj, L, s_sorted, perm, gbuf);
+  {
     // back-transforms: U = Q1 U_X (threads [0,32)), V = P Q2 W (threads [32,64))
     const bool isU = tid < 32;
     const int k = isU ? tid : tid - 32;
@@ -675,7 +923,7 @@ __device__ __forceinline__ int precond_svd(const double* __restrict__ core, int 
           if (i < n) Vo[P[i] + k * ldo] = u[i];
       }
     }
-    asm volatile("bar.sync 1, 128;");
+    __syncthreads();
   }
   return nsw;
 }

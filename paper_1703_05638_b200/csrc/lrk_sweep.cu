@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
   __syncthreads();
 
   const bool timing = a.dbg != nullptr && cta == 0 && tid == 0;
-  long long tacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tacc[20] = {};
   long long tprev = timing ? clock64() : 0;
 #define LRK_TSTAMP(k)               \
   if (timing) {                     \
@@ -338,7 +338,16 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     if constexpr (RES) stack = sm + a.off_scr;
     else stack = a.stack_smem ? sm + a.off_scr : gscr;
     double* stackY = stack + ms * pc;
-    {
+    // register two-level TSQR when the stacked blocks fit 3 rows per lane
+    const bool fast_stack = (Q <= 4) && ((ncta + NWARP - 1) / NWARP) * pc <= 96;
+    int tail_tid = 0;
+    if (fast_stack) {
+      if constexpr (Q <= 4) {
+        const int wo = warp_stack_tsqr<Q, 3>(part3, a.pstride, ncta, pc, cta, sCore, sRp, sQs);
+        tail_tid = wo * 32;
+      }
+      LRK_TSTAMP(13);
+    } else {
       // all loads of the stacked R's are issued before any store
       constexpr int BATCH = 16;
       const int pp = pc * pc, tot = ms * pc;
@@ -358,15 +367,17 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
           }
         }
       }
+      for (int i = tid; i < pc * pc; i += NT) sI[i] = (i / pc == i % pc) ? 1.0 : 0.0;
+      __syncthreads();
+      LRK_TSTAMP(13);
+      block_qr_t<Q>(stack, ms, ms, pc, sTauT, sRp, sRed, sTmp);
+      LRK_TSTAMP(14);
+      block_apply_q_t<Q>(stack, ms, ms, pc, sTauT, sI, stackY, ms, sRed, sTmp);
+      for (int i = tid; i < pc * pc; i += NT) sQs[i] = stackY[(cta * pc + i / pc) + (i % pc) * ms];
+      __syncthreads();
+      LRK_TSTAMP(15);
     }
-    for (int i = tid; i < pc * pc; i += NT) sI[i] = (i / pc == i % pc) ? 1.0 : 0.0;
-    __syncthreads();
-    LRK_TSTAMP(13);
-    block_qr_t<Q>(stack, ms, ms, pc, sTauT, sRp, sRed, sTmp);
-    LRK_TSTAMP(14);
-    block_apply_q_t<Q>(stack, ms, ms, pc, sTauT, sI, stackY, ms, sRed, sTmp);
-    LRK_TSTAMP(15);
-    if (tid == 0) {
+    if (tid == tail_tid) {
       // rows of the stacked Q that belong to this CTA; rank-revealing fix-up
       // Rp P = X Rt (column pivoting); drop rows at the block's rounding floor
       double ysq = 0.0;
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
             A[i][k] = (i < pc && k < pc) ? sRp[i * pc + k] : 0.0;
-            Qr[i][k] = (i < pc && k < pc) ? stackY[(cta * pc + i) + k * ms] : 0.0;
+            Qr[i][k] = (i < pc && k < pc) ? sQs[i * pc + k] : 0.0;
           }
         pivoted_qr_reg<Q>(A, pc, X, pv);
 #pragma unroll
@@ -404,8 +415,6 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
             if (i < pc && j < pc) sG[i * pc + j] = acc;
           }
       } else {
-        for (int i = 0; i < pc; ++i)
-          for (int c = 0; c < pc; ++c) sQs[i * pc + c] = stackY[(cta * pc + i) + c * ms];
         for (int i = 0; i < pc * pc; ++i) sRb[i] = sRp[i];
         small_pivoted_qr(sRb, pc, sX, iPiv, sCn);
         for (int j = 0; j < pc; ++j)
@@ -494,10 +503,10 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     LRK_TSTAMP(12);
     // ---------------- basis update in place: U' = [U, Q~] Uc[:, :rn]
     if (n <= 32 && rn <= 16) {
-      update_rows<16>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      update_rows_dmma<2>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
       update_time_rows<16>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
     } else if (n <= 32) {
-      update_rows<32>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      update_rows_dmma<4>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
       update_time_rows<32>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
     } else {
       // wide core: out of place through the global alternates, then copy back
@@ -530,7 +539,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     LRK_TSTAMP(8);
   }
   if (timing)
-    for (int k = 0; k < 16; ++k) a.dbg[k] = tacc[k];
+    for (int k = 0; k < 20; ++k) a.dbg[k] = tacc[k];
 #undef LRK_TSTAMP
   // the pane: resident U rows go back to global slot 0
   if (res)
