@@ -57,12 +57,16 @@ typedef struct {
 } lrk_lr;
 
 /* Spatial operator + time grid (discretize.py:107-127, forward.py:40-51).
- * kind: 0 = heat (5-point FD Laplacian), 1 = convdiff (not yet on device).
+ * kind: 0 = heat, 1 = convdiff (not yet on device).
+ * stencil: 0 = FD (5-point in 2-D as the reference, 7-point in 3-D),
+ *          1 = Q1 bilinear FEM stiffness with lumped mass (9-point, 2-D only;
+ *              L = K_Q1 / h^2).
  * The step matrix is S = m_scale * (I + tau * L). */
 enum { LRK_OP_HEAT = 0, LRK_OP_CONVDIFF = 1 };
+enum { LRK_STENCIL_FD = 0, LRK_STENCIL_Q1 = 1 };
 typedef struct {
   int kind;
-  int dim;      /* spatial dimension; 2 */
+  int dim;      /* spatial dimension; 2 or 3 */
   int n_side;   /* interior points per axis; n_x = n_side^dim */
   int n_t;      /* time steps */
   double h;     /* mesh size 1/(n_side+1) */
@@ -70,6 +74,7 @@ typedef struct {
   double m_scale; /* lumped mass h^dim */
   double nu;
   double wind[3];
+  int stencil;  /* LRK_STENCIL_* (0 = the reference's FD operator) */
 } lrk_operator_desc;
 
 /* Observation operator (hessian.py:78-156).
@@ -94,6 +99,14 @@ typedef struct {
   double eps0;          /* TruncationPolicy.eps0                             */
   int r_max;            /* TruncationPolicy.r_max, < 0 means None            */
   int compress_every;   /* sweep flush period (hessian.py:174)               */
+  /* Config extensions; all-zero = reference:
+   * prior_gamma > 0: Gamma_prior^{1/2} = sqrt(gamma_prior) (prior_delta I +
+   *   prior_gamma L)^{-1}, applied on both sides of the misfit Hessian;
+   * obs_every > 1: observe only time steps k (0-based) with (k+1) % obs_every
+   *   == 0 (a row mask on the W2 time factor). */
+  double prior_delta;
+  double prior_gamma;
+  int obs_every;
 } lrk_hessian_desc;
 
 /* ---- context ---------------------------------------------------------- */

@@ -58,6 +58,41 @@ def fd_operator(n_side: int, kind: str = "heat", nu: float = 1.0, wind=(0.0, 0.0
     return sp.csr_matrix(L), h, h * h
 
 
+def config_operator(n_side: int, dim: int = 2, stencil: str = "fd", kind: str = "heat",
+                    nu: float = 1.0, wind=(0.0, 0.0, 0.0)):
+    """Config-extension operators (SURVEY §8(c) "Config features beyond the
+    reference", Appendix D2; unpinned by the reference's own tests, pinned here
+    by closed-form eigenpairs and by golden runs of the unmodified reference
+    with these matrices duck-typed in, tests/golden/make_golden.py):
+      stencil "q1": L = (K1⊗M1 + M1⊗K1)/h², K1 = (1/h)tridiag(-1,2,-1),
+                    M1 = (h/6)tridiag(1,4,1) (Q1 stiffness, lumped mass h²);
+      dim 3 "fd":   7-point nu·(-Δ) + first-order upwind per axis.
+    Returns (L, h, m_scale) with x1 fastest."""
+    if dim == 2 and stencil == "fd":
+        return fd_operator(n_side, kind, nu, tuple(wind)[:2])
+    n = int(n_side)
+    h = 1.0 / (n + 1)
+    one = np.ones(n)
+    eye = sp.identity(n)
+    if stencil == "q1":
+        K1 = sp.diags([-one[1:], 2 * one, -one[1:]], [-1, 0, 1]) / h
+        M1 = sp.diags([one[1:], 4 * one, one[1:]], [-1, 0, 1]) * (h / 6)
+        return sp.csr_matrix((sp.kron(M1, K1) + sp.kron(K1, M1)) / h**2), h, h * h
+    coef = 1.0 if kind == "heat" else nu
+    axes = []
+    for ax in range(3):
+        A = coef * sp.diags([-one[1:], 2 * one, -one[1:]], [-1, 0, 1]) / h**2
+        w = float(wind[ax]) if (kind != "heat" and ax < len(wind)) else 0.0
+        if w > 0:
+            A = A + (w / h) * sp.diags([-one[1:], one], [-1, 0])
+        elif w < 0:
+            A = A + (-w / h) * sp.diags([one, -one[1:]], [0, 1])
+        axes.append(A)
+    L = (sp.kron(eye, sp.kron(eye, axes[0])) + sp.kron(eye, sp.kron(axes[1], eye))
+         + sp.kron(axes[2], sp.kron(eye, eye)))
+    return sp.csr_matrix(L), h, h ** 3
+
+
 class StepSolver:
     """S = M(I + tau L) factorised once by SuperLU, reused for N and T solves (forward.py:40-68)."""
 
@@ -249,8 +284,9 @@ class Problem:
     """Bundle of everything one Hessian apply needs (HessianContext, hessian.py:159-187)."""
 
     def __init__(self, n_side, n_t, mask, beta_noise, gamma_prior, eps0=1e-8, r_max=None,
-                 kind="heat", nu=1.0, wind=(0.0, 0.0), T=1.0, compress_every=4):
-        L, h, m = fd_operator(n_side, kind, nu, wind)
+                 kind="heat", nu=1.0, wind=(0.0, 0.0), T=1.0, compress_every=4, dim=2,
+                 stencil="fd", prior=None, obs_every=1):
+        L, h, m = config_operator(n_side, dim, stencil, kind, nu, wind)
         self.n_side, self.h, self.m = n_side, h, m
         self.tau = T / n_t
         self.solver = StepSolver(L, m, self.tau, n_t)
@@ -259,39 +295,54 @@ class Problem:
         self.gamma = gamma_prior
         self.eps0, self.r_max, self.p = eps0, r_max, compress_every
         self.weight = beta_noise * self.tau * m  # hessian.py:153
+        self.obs_every = int(obs_every)
+        # config prior sqrt: sqrt(gamma) (delta I + gamma_p L)^{-1}
+        self.prior_lu = None
+        if prior is not None:
+            delta, gp = prior
+            self.prior_lu = spla.splu((delta * sp.identity(L.shape[0]) + gp * L).tocsc())
+
+    def prior_sqrt(self, x):
+        """Γ^{1/2} x: sqrt(γ)·x (hessian.py:215) or sqrt(γ)(δI+γ_pL)⁻¹x (config prior)."""
+        x = math.sqrt(self.gamma) * np.asarray(x, float)
+        if self.prior_lu is None:
+            return x
+        return self.prior_lu.solve(x if x.ndim == 2 else x[:, None]).reshape(x.shape)
 
     def observe(self, W1, W2):
-        """Mask + weight + truncate (hessian.py:138-156)."""
+        """Mask + weight + truncate (hessian.py:138-156); time-row mask of
+        time-subsampled sensors before the truncation."""
         if W1.shape[1] == 0:
             return W1, W2
         Z1 = np.where(self.mask[:, None], W1, 0.0) * self.weight
+        if self.obs_every > 1:
+            keep = (np.arange(W2.shape[0]) + 1) % self.obs_every == 0
+            W2 = np.where(keep[:, None], W2, 0.0)
         return truncate(Z1, W2, self.eps0, self.r_max)
 
 
 def hessian_ic(P: Problem, v):
     """H̃ v for the IC parameter (hessian.py:211-226); returns (out, max_rank)."""
-    g = math.sqrt(P.gamma)
     n_t = P.solver.n_t
     e0 = np.zeros((n_t, 1))
     e0[0, 0] = 1.0
-    Y1, Y2, tr1 = sweep(P.solver, (P.m * g * np.asarray(v, float))[:, None], e0, P.eps0, P.r_max,
+    Y1, Y2, tr1 = sweep(P.solver, (P.m * P.prior_sqrt(v))[:, None], e0, P.eps0, P.r_max,
                         False, P.p)
     Z1, Z2 = P.observe(Y1, Y2)
     Q1, Q2, tr2 = sweep(P.solver, Z1, Z2, P.eps0, P.r_max, True, P.p)
-    out = g * P.m * (Q1 @ Q2[0]) if Q1.shape[1] else np.zeros(P.solver.n_x)
-    return out, max(tr1 + [Z1.shape[1]] + tr2)
+    out = P.m * (Q1 @ Q2[0]) if Q1.shape[1] else np.zeros(P.solver.n_x)
+    return P.prior_sqrt(out), max(tr1 + [Z1.shape[1]] + tr2)
 
 
 def hessian_st(P: Problem, V1, V2):
     """H̃ vec(v) for the space-time source (hessian.py:229-245); returns ((W1, W2), max_rank)."""
-    g = math.sqrt(P.gamma)
     inj = P.tau * P.m  # forward.py:118-122
-    r1, r2 = scale((np.asarray(V1, float), np.asarray(V2, float)), g)
-    r1, r2 = scale((r1, r2), inj)
+    r1 = P.prior_sqrt(np.asarray(V1, float))
+    r1, r2 = scale((r1, np.asarray(V2, float)), inj)
     Y1, Y2, tr1 = sweep(P.solver, r1, r2, P.eps0, P.r_max, False, P.p)
     Z1, Z2 = P.observe(Y1, Y2)
     Q1, Q2, tr2 = sweep(P.solver, Z1, Z2, P.eps0, P.r_max, True, P.p)
-    out = truncate(*scale(scale((Q1, Q2), inj), g), P.eps0, P.r_max)
+    out = truncate(*scale((P.prior_sqrt(Q1) if Q1.shape[1] else Q1, Q2), inj), P.eps0, P.r_max)
     return out, max(tr1 + [Z1.shape[1]] + tr2 + [out[0].shape[1]])
 
 
@@ -396,3 +447,41 @@ def ic_eigenvalue_full_obs(m, n, n_side, n_t, beta_noise, gamma, T=1.0):
     tau = T / n_t
     theta = 1.0 / (1.0 + tau * fd_eig(m, n, n_side))
     return gamma * beta_noise * tau * h * h * sum(theta ** (2 * k) for k in range(1, n_t + 1))
+
+
+def config_eig(modes, n_side, stencil="fd"):
+    """Eigenvalue of the config L on a separable DST-I mode."""
+    h = 1.0 / (n_side + 1)
+    ms = np.asarray(modes, float)
+    if stencil == "q1":
+        c = np.cos(ms * math.pi * h)
+        k1, m1 = (2 / h) * (1 - c), (h / 3) * (2 + c)
+        return float((k1[0] * m1[1] + m1[0] * k1[1]) / h**2)
+    s_ = np.sin(ms * math.pi * h / 2)
+    return float(4.0 / h**2 * np.sum(s_ * s_))
+
+
+def config_eigvec(modes, n_side):
+    """Unit separable DST-I eigenvector (x1 fastest) in 2-D or 3-D."""
+    x = np.arange(1, n_side + 1) / (n_side + 1)
+    v = np.ones(1)
+    for m in modes:  # x1 first -> innermost
+        f = np.sin(m * math.pi * x)
+        v = np.kron(f / np.linalg.norm(f), v)
+    return v
+
+
+def config_ic_eigenvalue(modes, n_side, n_t, beta_noise, gamma=1.0, stencil="fd", prior=None,
+                         obs_every=1, T=1.0):
+    """Full-observation IC Hessian eigenvalue on a DST-I mode, generalising
+    test_hessian.py:129-139: μ = γ β τ M Σ_{k observed} θ^{2k} · (δ+γ_p λ)⁻²."""
+    d = len(modes)
+    h = 1.0 / (n_side + 1)
+    tau = T / n_t
+    lam = config_eig(modes, n_side, stencil)
+    theta = 1.0 / (1.0 + tau * lam)
+    ks = [k for k in range(1, n_t + 1) if k % obs_every == 0]
+    mu = gamma * beta_noise * tau * h**d * sum(theta ** (2 * k) for k in ks)
+    if prior is not None:
+        mu /= (prior[0] + prior[1] * lam) ** 2
+    return mu

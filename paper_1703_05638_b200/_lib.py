@@ -48,7 +48,7 @@ class lrk_operator_desc(Structure):
     _fields_ = [
         ("kind", c_int), ("dim", c_int), ("n_side", c_int), ("n_t", c_int),
         ("h", c_double), ("tau", c_double), ("m_scale", c_double), ("nu", c_double),
-        ("wind", c_double * 3),
+        ("wind", c_double * 3), ("stencil", c_int),
     ]
 
 
@@ -64,6 +64,7 @@ class lrk_hessian_desc(Structure):
     _fields_ = [
         ("mode", c_int), ("gamma_prior", c_double), ("obs_weight", c_double),
         ("eps0", c_double), ("r_max", c_int), ("compress_every", c_int),
+        ("prior_delta", c_double), ("prior_gamma", c_double), ("obs_every", c_int),
     ]
 
 

@@ -43,6 +43,7 @@ struct lrk_ctx {
   double* dThetaM = nullptr;  // n_x: theta / m_scale (eigenvalues of S^{-1})
   double* dE0 = nullptr;      // n_t: e_0
   double* dInvLam = nullptr;  // n_x: 1/lambda (steady Poisson solve)
+  double* dLam = nullptr;     // n_x: lambda (config prior (delta + gamma lambda)^{-1})
   // observation
   bool has_obs = false;
   int obs_kind = LRK_OBS_FULL;
@@ -61,6 +62,7 @@ struct lrk_ctx {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (auto& kv : ws) cudaFree(kv.second.p);
     cudaFree(dS); cudaFree(dTheta); cudaFree(dThetaM); cudaFree(dE0); cudaFree(dInvLam);
+    cudaFree(dLam);
     cudaFree(dList); cudaFree(dS1T); cudaFree(dS2); cudaFree(dS1); cudaFree(dS2T);
   }
 };
@@ -138,31 +140,43 @@ int pick_ncta(lrk_ctx* c, int64_t rows) {
 // --------------------------------------------------------------- GEMMs
 int gemm(lrk_ctx* c, int M, int N, int K, const double* A, int64_t lda, int64_t sA,
          const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-         double alpha, int batch, const int* batch_dev, cudaStream_t s) {
+         double alpha, int batch, const int* batch_dev, cudaStream_t s, int batch_mult = 1) {
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.A = A; g.lda = lda; g.sA = sA;
   g.B = B; g.ldb = ldb; g.sB = sB;
   g.C = C; g.ldc = ldc; g.sC = sC;
   g.alpha = alpha; g.beta = 0.0;
-  g.batch = batch; g.batch_dev = batch_dev;
+  g.batch = batch; g.batch_dev = batch_dev; g.batch_mult = batch_mult;
   g.m_dev = nullptr; g.m_mult = 1;
   CK(launch_gemm(g, s));
   ++c->launches;
   return LRK_OK;
 }
 
-// Y[:, j] = alpha * (S (x) S) X[:, j]: 2-D DST-I of each column.
+// Y[:, j] = alpha * (S (x) S [(x) S]) X[:, j]: 2-D or 3-D DST-I of each column
+// (x1 fastest), one DMMA GEMM pass per axis.
 int dst2(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int ncols,
          const int* ncols_dev, double alpha, cudaStream_t s) {
   if (ncols <= 0) return LRK_OK;
   const int n = c->n;
   const int64_t nx = c->n_x;
   WS(double, T, "dst_T", nx * (int64_t)ncols);
-  // T_j = X_j S      (X_j: n x n row-major view of column j)
-  TRY(gemm(c, n, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
-  // Y_j = alpha S T_j
-  TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s));
+  if (c->op.dim == 2) {
+    // T_j = X_j S      (X_j: n x n row-major view of column j)
+    TRY(gemm(c, n, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
+    // Y_j = alpha S T_j
+    TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s));
+    return LRK_OK;
+  }
+  const int64_t pl = (int64_t)n * n;
+  WS(double, T2, "dst_T2", nx * (int64_t)ncols);
+  // x1: T_j = X_j S, X_j viewed as (n^2) x n row-major
+  TRY(gemm(c, (int)pl, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
+  // x2: per (column, x3-plane) slice: T2 = S T_slice  (batch ncols * n, stride n^2)
+  TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, pl, T2, n, pl, 1.0, ncols * n, ncols_dev, s, n));
+  // x3: Y_j = alpha S T2_j, T2_j viewed as n x (n^2) row-major
+  TRY(gemm(c, n, (int)pl, n, c->dS, n, 0, T2, pl, nx, Y, pl, ldy, alpha, ncols, ncols_dev, s));
   return LRK_OK;
 }
 
@@ -317,8 +331,8 @@ int check_op(lrk_ctx* c) {
 
 // Observation + weight + truncation of the forward pane (apply_obs_weight,
 // hessian.py:138-156).  Output: spectral Zhat (n_x x cap), Z2 (n_t x cap), zinfo.
-int obs_weight(lrk_ctx* c, const SweepOut& y, double w, double eps0, int r_max, double** Zhat,
-               double** Z2, int** zinfo, int* zcap, cudaStream_t s) {
+int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, int r_max,
+               double** Zhat, double** Z2, int** zinfo, int* zcap, cudaStream_t s) {
   const int64_t nx = c->n_x;
   const int nt = c->op.n_t;
   const int cap = y.ucap;
@@ -327,12 +341,18 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, double eps0, int r_max, 
   scale_cols_kernel<<<dim3(grid1(nt, 256, 64), cap), 256, 0, s>>>(y.V, y.ldv, nt, y.sigma,
                                                                    y.info, cap, w, W2s, nt);
   CKL();
+  if (every > 1) {  // time-subsampled sensors
+    mask_time_rows_kernel<<<dim3(grid1(nt, 256, 64), cap), 256, 0, s>>>(W2s, nt, nt, cap, every);
+    CKL();
+  }
+  // a time mask breaks the orthonormality of the time factor
+  const int w2flag = every > 1 ? 0 : LRK_TRUNC_W2_ORTHOSCALED;
   WS(double, Zh, "ob_Zhat", nx * (int64_t)cap);
   WS(double, Zt, "ob_Z2", (int64_t)nt * cap);
   TruncOut to;
   if (c->obs_kind == LRK_OBS_FULL) {
     TRY(run_truncate(c, "ob_", nx, nt, y.U, y.ldu, W2s, nt, cap, y.info,
-                     LRK_TRUNC_W1_ORTHO | LRK_TRUNC_W2_ORTHOSCALED, eps0, r_max, Zh, nx, Zt, nt,
+                     LRK_TRUNC_W1_ORTHO | w2flag, eps0, r_max, Zh, nx, Zt, nt,
                      cap, nullptr, nullptr, 1, to, s));
   } else {
     const int no = c->n_obs;
@@ -347,7 +367,7 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, double eps0, int r_max, 
                                                                          y.info, cap, Uo, no);
       CKL();
     }
-    TRY(run_truncate(c, "ob_", no, nt, Uo, no, W2s, nt, cap, y.info, LRK_TRUNC_W2_ORTHOSCALED,
+    TRY(run_truncate(c, "ob_", no, nt, Uo, no, W2s, nt, cap, y.info, w2flag,
                      eps0, r_max, Zo, no, Zt, nt, cap, nullptr, nullptr, 1, to, s));
     if (c->obs_kind == LRK_OBS_SUBGRID) {
       TRY(subgrid_scatter(c, Zo, no, Zh, nx, cap, to.info, s));
@@ -374,6 +394,20 @@ int hd_check(lrk_ctx* c, const lrk_hessian_desc* hd) {
     return fail(c, LRK_ERR_SHAPE, "eps0 must lie in (0, 1)");
   if (!c->has_obs) return fail(c, LRK_ERR_CONFIG, "no observation layout installed");
   if (!(hd->gamma_prior > 0.0)) return fail(c, LRK_ERR_CONFIG, "gamma_prior must be positive");
+  if (hd->prior_gamma < 0.0 || (hd->prior_gamma > 0.0 && !(hd->prior_delta > 0.0)))
+    return fail(c, LRK_ERR_CONFIG, "operator prior needs prior_delta > 0 and prior_gamma >= 0");
+  if (hd->obs_every < 0) return fail(c, LRK_ERR_CONFIG, "obs_every must be >= 0");
+  return LRK_OK;
+}
+
+// In-place spectral prior factor (prior_delta + prior_gamma lambda)^{-1} on the
+// rows of X (no-op for the reference's scalar prior).
+int apply_prior(lrk_ctx* c, const lrk_hessian_desc* hd, double* X, int64_t ldx, int ncols,
+                const int* ncols_dev, cudaStream_t s) {
+  if (!(hd->prior_gamma > 0.0) || ncols <= 0) return LRK_OK;
+  prior_scale_kernel<<<dim3(grid1(c->n_x, 256, 1024), ncols), 256, 0, s>>>(
+      X, ldx, c->dLam, c->n_x, ncols, ncols_dev, 1.0, hd->prior_delta, hd->prior_gamma, X, ldx);
+  CKL();
   return LRK_OK;
 }
 
@@ -511,35 +545,55 @@ int lrk_last_traces(lrk_ctx* c, int* fwd, int* bwd, int cap, int* n_fwd, int* n_
 int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
   if (!c || !op) return LRK_ERR_CONFIG;
   CK(cudaSetDevice(c->device));
-  if (op->dim != 2) return fail(c, LRK_ERR_UNSUPPORTED, "only dim=2 operators are implemented");
+  if (op->dim != 2 && op->dim != 3)
+    return fail(c, LRK_ERR_UNSUPPORTED, "dim must be 2 or 3");
+  if (op->stencil != LRK_STENCIL_FD && op->stencil != LRK_STENCIL_Q1)
+    return fail(c, LRK_ERR_CONFIG, "unknown stencil");
+  if (op->stencil == LRK_STENCIL_Q1 && (op->dim != 2 || op->kind != LRK_OP_HEAT))
+    return fail(c, LRK_ERR_UNSUPPORTED, "the Q1-lumped stencil is implemented for 2-D heat");
   if (op->n_side < 2 || op->n_t < 1 || !(op->tau > 0) || !(op->h > 0) || !(op->m_scale > 0))
     return fail(c, LRK_ERR_CONFIG, "invalid operator descriptor");
   const int n = op->n_side;
-  const int64_t nx = (int64_t)n * n;
-  std::vector<double> S((size_t)n * n), th(nx), thm(nx), il(nx), l1(n), e0(op->n_t, 0.0);
+  const int64_t nx = op->dim == 3 ? (int64_t)n * n * n : (int64_t)n * n;
+  std::vector<double> S((size_t)n * n), th(nx), thm(nx), il(nx), lm(nx), l1(n), m1(n),
+      e0(op->n_t, 0.0);
   const double f = std::sqrt(2.0 / (n + 1));
   for (int j = 0; j < n; ++j)
     for (int k = 0; k < n; ++k)
       S[(size_t)j * n + k] = f * std::sin(M_PI * (double)(j + 1) * (double)(k + 1) / (n + 1));
   const double h = op->h;
+  // per-axis symbols of the DST-I eigenvectors
   for (int m = 0; m < n; ++m) {
     const double sv = std::sin((m + 1) * M_PI * h / 2.0);
-    l1[m] = (4.0 / (h * h)) * sv * sv;  // discretize.py:137-144 (per axis)
-  }
-  for (int i2 = 0; i2 < n; ++i2)
-    for (int i1 = 0; i1 < n; ++i1) {
-      const double lam = l1[i1] + l1[i2];
-      const double t = 1.0 / (1.0 + op->tau * lam);
-      th[(size_t)i2 * n + i1] = t;
-      thm[(size_t)i2 * n + i1] = t / op->m_scale;
-      il[(size_t)i2 * n + i1] = 1.0 / lam;
+    if (op->stencil == LRK_STENCIL_FD) {
+      l1[m] = (4.0 / (h * h)) * sv * sv;  // discretize.py:137-144 (per axis)
+    } else {
+      // Q1: K1 = (1/h)[-1 2 -1] -> (2/h)(1 - cos), M1 = (h/6)[1 4 1] -> (h/3)(2 + cos);
+      // L = (K1 (x) M1 + M1 (x) K1) / h^2
+      const double cs = std::cos((m + 1) * M_PI * h);
+      l1[m] = (2.0 / h) * (1.0 - cs);
+      m1[m] = (h / 3.0) * (2.0 + cs);
     }
+  }
+  for (int64_t i = 0; i < nx; ++i) {
+    const int i1 = (int)(i % n), i2 = (int)((i / n) % n), i3 = (int)(i / ((int64_t)n * n));
+    double lam;
+    if (op->stencil == LRK_STENCIL_Q1) lam = (l1[i1] * m1[i2] + m1[i1] * l1[i2]) / (h * h);
+    else lam = l1[i1] + l1[i2] + (op->dim == 3 ? l1[i3] : 0.0);
+    const double t = 1.0 / (1.0 + op->tau * lam);
+    th[i] = t;
+    thm[i] = t / op->m_scale;
+    il[i] = 1.0 / lam;
+    lm[i] = lam;
+  }
   e0[0] = 1.0;
   cudaFree(c->dS); cudaFree(c->dTheta); cudaFree(c->dThetaM); cudaFree(c->dE0);
-  cudaFree(c->dInvLam);
-  c->dS = c->dTheta = c->dThetaM = c->dE0 = c->dInvLam = nullptr;
+  cudaFree(c->dInvLam); cudaFree(c->dLam);
+  c->dS = c->dTheta = c->dThetaM = c->dE0 = c->dInvLam = c->dLam = nullptr;
   CK(cudaMalloc(&c->dInvLam, nx * sizeof(double)));
   CK(cudaMemcpy(c->dInvLam, il.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&c->dLam, nx * sizeof(double)));
+  CK(cudaMemcpy(c->dLam, lm.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&c->dS, S.size() * sizeof(double)));
   CK(cudaMalloc(&c->dTheta, nx * sizeof(double)));
   CK(cudaMalloc(&c->dThetaM, nx * sizeof(double)));
@@ -567,6 +621,8 @@ int lrk_set_observation(lrk_ctx* c, const lrk_obs_desc* obs) {
   if (obs->kind == LRK_OBS_FULL) {
     c->n_obs = (int)c->n_x;
   } else if (obs->kind == LRK_OBS_SUBGRID) {
+    if (c->op.dim != 2)
+      return fail(c, LRK_ERR_UNSUPPORTED, "separable subgrids are 2-D; pass a dof list in 3-D");
     const int s1 = obs->n1, s2 = obs->n2;
     if (s1 < 1 || s2 < 1) return fail(c, LRK_ERR_CONFIG, "empty sensor subgrid");
     std::vector<double> S1T((size_t)n * s1), S2((size_t)s2 * n), S1((size_t)s1 * n),
@@ -719,18 +775,32 @@ int lrk_operator_apply(lrk_ctx* c, const lrk_lr* Y, int adjoint, lrk_lr* out, vo
   const lrk_operator_desc& op = c->op;
   const double h = op.h, ih2 = 1.0 / (h * h);
   StencilArgs a{};
-  double cc, cw, ce, cs_, cn_;
-  if (op.kind == LRK_OP_HEAT) {
-    cc = 4.0 * ih2; cw = ce = cs_ = cn_ = -ih2;
+  auto cf = [&](int d1, int d2, int d3) -> double& { return a.coef[(d3 + 1) * 9 + (d2 + 1) * 3 + (d1 + 1)]; };
+  const double sc = op.kind == LRK_OP_HEAT ? 1.0 : op.nu;
+  if (op.stencil == LRK_STENCIL_Q1) {
+    // K_Q1 / h^2 with lumped mass: centre 8/3, all eight neighbours -1/3
+    for (int d2 = -1; d2 <= 1; ++d2)
+      for (int d1 = -1; d1 <= 1; ++d1) cf(d1, d2, 0) = -ih2 / 3.0;
+    cf(0, 0, 0) = 8.0 * ih2 / 3.0;
   } else {
-    cc = op.nu * 4.0 * ih2; cw = ce = cs_ = cn_ = -op.nu * ih2;
-    const double w1 = op.wind[0], w2 = op.wind[1];
-    if (w1 > 0) { cc += w1 / h; cw -= w1 / h; } else if (w1 < 0) { cc -= w1 / h; ce += w1 / h; }
-    if (w2 > 0) { cc += w2 / h; cs_ -= w2 / h; } else if (w2 < 0) { cc -= w2 / h; cn_ += w2 / h; }
+    cf(0, 0, 0) = 2.0 * op.dim * sc * ih2;
+    cf(-1, 0, 0) = cf(1, 0, 0) = cf(0, -1, 0) = cf(0, 1, 0) = -sc * ih2;
+    if (op.dim == 3) cf(0, 0, -1) = cf(0, 0, 1) = -sc * ih2;
+    if (op.kind != LRK_OP_HEAT) {
+      // first-order upwind per axis by the sign of the wind (discretize.py:96-104)
+      for (int ax = 0; ax < op.dim; ++ax) {
+        const double w = op.wind[ax];
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        lo[ax] = -1; hi[ax] = 1;
+        if (w > 0) { cf(0, 0, 0) += w / h; cf(lo[0], lo[1], lo[2]) -= w / h; }
+        else if (w < 0) { cf(0, 0, 0) -= w / h; cf(hi[0], hi[1], hi[2]) += w / h; }
+      }
+    }
   }
-  if (adjoint) { std::swap(cw, ce); std::swap(cs_, cn_); }
-  a.X = Y->W1; a.ldx = Y->ld1; a.Y = out->W1; a.ldy = out->ld1; a.n = c->n; a.ncols = r;
-  a.cc = cc; a.cw = cw; a.ce = ce; a.cs = cs_; a.cn = cn_; a.m_scale = op.m_scale; a.tau = op.tau;
+  if (adjoint)
+    for (int k = 0; k < 13; ++k) std::swap(a.coef[k], a.coef[26 - k]);
+  a.X = Y->W1; a.ldx = Y->ld1; a.Y = out->W1; a.ldy = out->ld1; a.n = c->n; a.dim = op.dim;
+  a.ncols = r; a.m_scale = op.m_scale; a.tau = op.tau;
   stencil_kernel<<<dim3(grid1(c->n_x, 256, 1 << 30), r), 256, 0, s>>>(a);
   CKL();
   // W2 copy into the first r columns; shift + (-M W1) into the second r
@@ -803,19 +873,22 @@ int lrk_hessian_apply_ic(lrk_ctx* c, const lrk_hessian_desc* hd, int nbatch, con
     double* out = OUT + (int64_t)b * ldo;
     // inject: rhs = (M sqrt(g) v) e_0^T, spectral  (forward.py:108-109)
     TRY(dst2(c, v, nx, Bv, nx, 1, nullptr, sg * M, s));
+    TRY(apply_prior(c, hd, Bv, nx, 1, nullptr, s));
     SweepOut fw, bw;
     TRY(run_sweep(c, "f_", Bv, nx, 1, nullptr, c->dE0, nt, 0, hd->compress_every, hd->eps0,
                   hd->r_max, fw, s));
     double *Zh, *Z2;
     int* zinfo;
     int zcap;
-    TRY(obs_weight(c, fw, hd->obs_weight, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo, &zcap, s));
+    TRY(obs_weight(c, fw, hd->obs_weight, hd->obs_every, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo,
+                   &zcap, s));
     TRY(run_sweep(c, "b_", Zh, nx, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
                   bw, s));
     // extract: sqrt(g) M Q.column(0)  (forward.py:111-112)
     column_eval_kernel<<<grid1(nx, 256, 1024), 256, 0, s>>>(bw.U, bw.ldu, nx, bw.sigma, bw.V,
                                                               bw.ldv, 0, bw.info, q);
     CKL();
+    TRY(apply_prior(c, hd, q, nx, 1, nullptr, s));
     TRY(dst2(c, q, nx, out, nx, 1, nullptr, sg * M, s));
     int mr = 0;
     TRY(host_max_rank(c, fw, zinfo, bw, nullptr, &mr, hd->compress_every, 1, 1, s));
@@ -839,26 +912,36 @@ int lrk_hessian_apply_st(lrk_ctx* c, const lrk_hessian_desc* hd, const lrk_lr* v
   WS(double, Bh, "st_B", nx * (int64_t)v->r);
   // rhs = tau M sqrt(g) v  (forward.py:121-122, hessian.py:236)
   TRY(dst2(c, v->W1, v->ld1, Bh, nx, v->r, nullptr, tau * M * sg, s));
+  TRY(apply_prior(c, hd, Bh, nx, v->r, nullptr, s));
   SweepOut fw, bw;
   TRY(run_sweep(c, "f_", Bh, nx, v->r, nullptr, v->W2, v->ld2, 0, hd->compress_every, hd->eps0,
                 hd->r_max, fw, s));
   double *Zh, *Z2;
   int* zinfo;
   int zcap;
-  TRY(obs_weight(c, fw, hd->obs_weight, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo, &zcap, s));
+  TRY(obs_weight(c, fw, hd->obs_weight, hd->obs_every, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo,
+                 &zcap, s));
   TRY(run_sweep(c, "b_", Zh, nx, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
                 bw, s));
   // out = truncate(sqrt(g) tau M Q)  (hessian.py:242)
   const int cap = bw.ucap;
   WS(double, Up, "st_Uphys", nx * (int64_t)cap);
   WS(double, W2o, "st_W2o", (int64_t)nt * cap);
-  TRY(dst2(c, bw.U, bw.ldu, Up, nx, cap, bw.info, 1.0, s));
+  const double* Uspec = bw.U;
+  if (hd->prior_gamma > 0.0) {
+    WS(double, Up2, "st_Uprior", nx * (int64_t)cap);
+    prior_scale_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(
+        bw.U, bw.ldu, c->dLam, nx, cap, bw.info, 1.0, hd->prior_delta, hd->prior_gamma, Up2, nx);
+    CKL();
+    Uspec = Up2;
+  }
+  TRY(dst2(c, Uspec, Uspec == bw.U ? bw.ldu : nx, Up, nx, cap, bw.info, 1.0, s));
   scale_cols_kernel<<<dim3(grid1(nt, 256, 64), cap), 256, 0, s>>>(bw.V, bw.ldv, nt, bw.sigma,
                                                                    bw.info, cap, sg * tau * M, W2o, nt);
   CKL();
   TruncOut to;
   TRY(run_truncate(c, "so_", nx, nt, Up, nx, W2o, nt, cap, bw.info,
-                   LRK_TRUNC_W1_ORTHO | LRK_TRUNC_W2_ORTHOSCALED, hd->eps0, hd->r_max, out->W1,
+                   (hd->prior_gamma > 0.0 ? 0 : LRK_TRUNC_W1_ORTHO) | LRK_TRUNC_W2_ORTHOSCALED, hd->eps0, hd->r_max, out->W1,
                    out->ld1, out->W2, out->ld2, out->cap, nullptr, nullptr, 0, to, s));
   int info[8];
   CK(cudaMemcpyAsync(info, to.info, sizeof(info), cudaMemcpyDeviceToHost, s));

@@ -28,7 +28,10 @@ __global__ void __launch_bounds__(GT) gemm_kernel(GemmArgs g) {
   int M = g.M;
   if (g.m_dev) { const int md = (*g.m_dev) * g.m_mult; if (md < M) M = md; }
   int batch = g.batch;
-  if (g.batch_dev) { const int bd = *g.batch_dev; if (bd < batch) batch = bd; }
+  if (g.batch_dev) {
+    const int bd = (*g.batch_dev) * (g.batch_mult > 0 ? g.batch_mult : 1);
+    if (bd < batch) batch = bd;
+  }
   const int b = blockIdx.z;
   if (b >= batch) return;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;

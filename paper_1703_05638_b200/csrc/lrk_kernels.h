@@ -102,7 +102,8 @@ struct GemmArgs {
   double* C; int64_t ldc; int64_t sC;
   double alpha, beta;
   int batch;
-  const int* batch_dev;    // optional: batch = min(batch, *batch_dev)
+  const int* batch_dev;    // optional: batch = min(batch, *batch_dev * batch_mult)
+  int batch_mult;
   const int* m_dev;        // optional: M = min(M, *m_dev * m_mult)
   int m_mult;
 };

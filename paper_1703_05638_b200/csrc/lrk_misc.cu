@@ -8,23 +8,35 @@ namespace lrk {
 
 // ---------------------------------------------------------------- stencil
 // K.apply / apply_adjoint spatial part (forward.py:79-95):
-//   out[:, c] = m_scale * (X[:, c] + tau * L X[:, c])   (L^T when adjoint)
-// for the 5-point FD operators of discretize.py:90-127, generated on the fly
-// (no CSR): (L x)_i = cc x_i + cw x_{i-1} + ce x_{i+1} + cs x_{i-n} + cn x_{i+n}
-// with zero Dirichlet data.  One thread per output entry, coalesced along x1.
+// (S x) = m_scale (x + tau L x) for the constant-coefficient box stencils of
+// discretize.py:90-127 (5-point FD) and their config extensions (Q1-lumped
+// 9-point, 3-D 7-point), generated on the fly (no CSR), zero Dirichlet data.
+// One thread per output entry, coalesced along x1; neighbours come through L1.
 __global__ void stencil_kernel(StencilArgs a) {
   const int c = blockIdx.y;
-  const int64_t n_x = (int64_t)a.n * a.n;
+  const int n = a.n;
+  const int64_t plane = (int64_t)n * n;
+  const int64_t n_x = a.dim == 3 ? plane * n : plane;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_x || c >= a.ncols) return;
   const double* x = a.X + (int64_t)c * a.ldx;
-  const int i1 = (int)(i % a.n), i2 = (int)(i / a.n);
+  const int i1 = (int)(i % n), i2 = (int)((i / n) % n), i3 = (int)(i / plane);
   const double xc = x[i];
-  double lx = a.cc * xc;
-  if (i1 > 0) lx += a.cw * x[i - 1];
-  if (i1 < a.n - 1) lx += a.ce * x[i + 1];
-  if (i2 > 0) lx += a.cs * x[i - a.n];
-  if (i2 < a.n - 1) lx += a.cn * x[i + a.n];
+  double lx = 0.0;
+  const int d3lo = a.dim == 3 ? -1 : 0, d3hi = a.dim == 3 ? 1 : 0;
+  for (int d3 = d3lo; d3 <= d3hi; ++d3) {
+    if (i3 + d3 < 0 || i3 + d3 >= (a.dim == 3 ? n : 1)) continue;
+#pragma unroll
+    for (int d2 = -1; d2 <= 1; ++d2) {
+      if (i2 + d2 < 0 || i2 + d2 >= n) continue;
+#pragma unroll
+      for (int d1 = -1; d1 <= 1; ++d1) {
+        const double cf = a.coef[(d3 + 1) * 9 + (d2 + 1) * 3 + (d1 + 1)];
+        if (cf == 0.0 || i1 + d1 < 0 || i1 + d1 >= n) continue;
+        lx += cf * x[i + d1 + (int64_t)d2 * n + (int64_t)d3 * plane];
+      }
+    }
+  }
   a.Y[i + (int64_t)c * a.ldy] = a.m_scale * (xc + a.tau * lx);
 }
 
@@ -45,6 +57,28 @@ __global__ void shift_kernel(const double* W2, int64_t ld2, int n_t, int ncols, 
 }
 
 // ---------------------------------------------------------- utilities
+// Y[:, c] = alpha * X[:, c] / (delta + gamma * lam): the spectral image of the
+// config prior (delta I + gamma L)^{-1}.
+__global__ void prior_scale_kernel(const double* X, int64_t ldx, const double* lam, int64_t n,
+                                   int ncols, const int* ncols_dev, double alpha, double delta,
+                                   double gamma, double* Y, int64_t ldy) {
+  const int c = blockIdx.y;
+  const int nc = ncols_dev ? min(ncols, *ncols_dev) : ncols;
+  if (c >= nc) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    Y[i + (int64_t)c * ldy] = alpha * X[i + (int64_t)c * ldx] / (delta + gamma * lam[i]);
+}
+
+// Zero the rows k of a time factor with (k+1) % every != 0 (time-subsampled
+// sensors).
+__global__ void mask_time_rows_kernel(double* W2, int64_t ld2, int n_t, int ncols, int every) {
+  const int c = blockIdx.y;
+  if (c >= ncols) return;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_t; k += gridDim.x * blockDim.x)
+    if ((k + 1) % every != 0) W2[k + (int64_t)c * ld2] = 0.0;
+}
+
 __global__ void scale_rows_kernel(const double* X, int64_t ldx, const double* s, int64_t n,
                                   int ncols, const int* ncols_dev, double alpha, double* Y,
                                   int64_t ldy) {

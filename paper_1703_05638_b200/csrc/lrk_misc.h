@@ -9,8 +9,11 @@ struct StencilArgs {
   const double* X; int64_t ldx;
   double* Y; int64_t ldy;
   int n;          // n_side
+  int dim;        // 2 or 3
   int ncols;
-  double cc, cw, ce, cs, cn;  // (L x)_i coefficients (already transposed for adjoint)
+  // (L x)_i = sum over the 3^dim box of coef[(d3+1)*9 + (d2+1)*3 + (d1+1)] x_{i+d}
+  // (already mirrored for the adjoint); zero entries are skipped uniformly
+  double coef[27];
   double m_scale, tau;
 };
 
@@ -18,6 +21,10 @@ __global__ void stencil_kernel(StencilArgs a);
 __global__ void shift_kernel(const double* W2, int64_t ld2, int n_t, int ncols, int adjoint,
                              double* out, int64_t ldo, const double* W1, int64_t ld1,
                              int64_t n_x, double neg_m, double* out1, int64_t ldo1);
+__global__ void prior_scale_kernel(const double* X, int64_t ldx, const double* lam, int64_t n,
+                                   int ncols, const int* ncols_dev, double alpha, double delta,
+                                   double gamma, double* Y, int64_t ldy);
+__global__ void mask_time_rows_kernel(double* W2, int64_t ld2, int n_t, int ncols, int every);
 __global__ void scale_rows_kernel(const double* X, int64_t ldx, const double* s, int64_t n,
                                   int ncols, const int* ncols_dev, double alpha, double* Y,
                                   int64_t ldy);

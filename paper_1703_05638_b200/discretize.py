@@ -42,6 +42,9 @@ class Grid:
 
     def coords(self):
         axis = self.h * (1 + np.arange(self.n_side))
+        if self.d == 3:
+            n = self.n_side
+            return (np.tile(axis, n * n), np.tile(np.repeat(axis, n), n), np.repeat(axis, n * n))
         return np.tile(axis, self.n_side), np.repeat(axis, self.n_side)
 
 
@@ -60,17 +63,20 @@ class SpatialOperator:
     grid: Grid
     L: sp.csr_matrix
     nu: float = 1.0
-    wind: tuple[float, float] = (0.0, 0.0)
+    wind: tuple = (0.0, 0.0)
+    stencil: str = "fd"   # "fd" (reference 5-point / 3-D 7-point) or "q1" (Q1-lumped 9-point)
 
     @property
     def m_scale(self) -> float:
         return self.grid.m_scale
 
 
-def build_grid(n_side: int) -> Grid:
+def build_grid(n_side: int, d: int = 2) -> Grid:
     if n_side < 2:
         raise InvalidConfigError(f"n_side must be >= 2, got {n_side}")
-    return Grid(n_side=int(n_side), h=1.0 / (n_side + 1))
+    if d not in (2, 3):
+        raise InvalidConfigError(f"dimension must be 2 or 3, got {d}")
+    return Grid(n_side=int(n_side), h=1.0 / (n_side + 1), d=int(d))
 
 
 def build_time_grid(n_t: int, T: float = 1.0) -> TimeGrid:
@@ -115,16 +121,79 @@ def _assemble(grid: Grid, coeffs) -> sp.csr_matrix:
     return sp.diags(diags, offsets, shape=(n * n, n * n), format="csr")
 
 
-def assemble_heat(grid: Grid) -> SpatialOperator:
+def _lap1(n: int, h: float):
+    one = np.ones(n)
+    return sp.diags([-one[1:], 2 * one, -one[1:]], [-1, 0, 1]) / h**2
+
+
+def _upwind1(n: int, h: float, w: float):
+    """First-order upwind w·d/dx by the sign of w (discretize.py:96-104)."""
+    one = np.ones(n)
+    if w > 0:
+        return (w / h) * sp.diags([-one[1:], one], [-1, 0])
+    if w < 0:
+        return (-w / h) * sp.diags([one, -one[1:]], [0, 1])
+    return sp.csr_matrix((n, n))
+
+
+def _assemble_3d(grid: Grid, nu: float = 1.0, wind=(0.0, 0.0, 0.0)) -> sp.csr_matrix:
+    """3-D 7-point FD nu·(-Δ) + per-axis upwind, x1 fastest (config C4/C5 extension)."""
+    n, h = grid.n_side, grid.h
+    eye = sp.identity(n)
+    ops = [nu * _lap1(n, h) + _upwind1(n, h, float(w)) for w in (tuple(wind) + (0.0,) * 3)[:3]]
+    return sp.csr_matrix(sp.kron(eye, sp.kron(eye, ops[0])) + sp.kron(eye, sp.kron(ops[1], eye))
+                         + sp.kron(ops[2], sp.kron(eye, eye)))
+
+
+def _assemble_q1(grid: Grid) -> sp.csr_matrix:
+    """Q1 bilinear stiffness with lumped mass, L = K_Q1 / h²:
+    K_Q1 = K1 ⊗ M1 + M1 ⊗ K1, K1 = (1/h)[-1 2 -1], M1 = (h/6)[1 4 1]; the
+    9-point stencil has centre 8/3 and all eight neighbours -1/3 (times 1/h²)."""
+    n, h = grid.n_side, grid.h
+    one = np.ones(n)
+    K1 = sp.diags([-one[1:], 2 * one, -one[1:]], [-1, 0, 1]) / h
+    M1 = sp.diags([one[1:], 4 * one, one[1:]], [-1, 0, 1]) * (h / 6)
+    return sp.csr_matrix((sp.kron(K1, M1) + sp.kron(M1, K1)) / h**2)
+
+
+def assemble_heat(grid: Grid, stencil: str = "fd") -> SpatialOperator:
+    if stencil not in ("fd", "q1"):
+        raise InvalidConfigError(f"unknown stencil {stencil!r}")
+    if stencil == "q1":
+        if grid.d != 2:
+            raise InvalidConfigError("the Q1-lumped stencil is 2-D")
+        return SpatialOperator(kind="heat", grid=grid, L=_assemble_q1(grid), stencil="q1")
+    if grid.d == 3:
+        return SpatialOperator(kind="heat", grid=grid, L=_assemble_3d(grid))
     return SpatialOperator(kind="heat", grid=grid, L=_assemble(grid, stencil_coefficients("heat", grid.h)))
 
 
 def assemble_convdiff(grid: Grid, nu: float, wind) -> SpatialOperator:
     if nu <= 0:
         raise InvalidConfigError(f"viscosity nu must be positive, got {nu}")
+    if grid.d == 3:
+        w3 = tuple(float(x) for x in (tuple(wind) + (0.0,) * 3)[:3])
+        return SpatialOperator(kind="convdiff", grid=grid, L=_assemble_3d(grid, float(nu), w3),
+                               nu=float(nu), wind=w3)
     w = (float(wind[0]), float(wind[1]))
     L = _assemble(grid, stencil_coefficients("convdiff", grid.h, nu, w))
     return SpatialOperator(kind="convdiff", grid=grid, L=L, nu=float(nu), wind=w)
+
+
+def operator_eig(grid: Grid, modes, stencil: str = "fd") -> float:
+    """Eigenvalue of L on the separable DST-I mode `modes` (1-based, one per
+    axis): FD sum of (4/h²)sin²(mπh/2); Q1-lumped [k1(m)m1(n) + m1(m)k1(n)]/h²
+    with k1 = (2/h)(1 - cos mπh), m1 = (h/3)(2 + cos mπh)."""
+    h = grid.h
+    ms = np.asarray(modes, dtype=float)
+    if ms.size != grid.d or np.any(ms < 1) or np.any(ms > grid.n_side):
+        raise InvalidConfigError(f"need {grid.d} mode indices in [1, {grid.n_side}]")
+    if stencil == "q1":
+        c = np.cos(ms * np.pi * h)
+        k1, m1 = (2 / h) * (1 - c), (h / 3) * (2 + c)
+        return float((k1[0] * m1[1] + m1[0] * k1[1]) / h**2)
+    s = np.sin(ms * np.pi * h / 2)
+    return float(4.0 / h**2 * np.sum(s * s))
 
 
 def analytic_poisson_eig(m: int, n: int, a: float = 1.0, b: float = 1.0) -> float:
@@ -152,6 +221,12 @@ def analytic_separable_eigvec(m: int, n: int, grid: Grid):
     return f1 / np.linalg.norm(f1), f2 / np.linalg.norm(f2)
 
 
-def eigvec_dense(m: int, n: int, grid: Grid) -> np.ndarray:
+def eigvec_dense(m: int, n: int, grid: Grid, k: int | None = None) -> np.ndarray:
     f1, f2 = analytic_separable_eigvec(m, n, grid)
+    if grid.d == 3:
+        if k is None or not (1 <= k <= grid.n_side):
+            raise InvalidConfigError("3-D eigenvectors need a third mode index")
+        x = grid.h * (1 + np.arange(grid.n_side))
+        f3 = np.sin(k * np.pi * x)
+        return np.kron(f3 / np.linalg.norm(f3), np.kron(f2, f1))
     return np.kron(f2, f1)

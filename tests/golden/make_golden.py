@@ -141,6 +141,83 @@ def main():
     out["arn_iters"] = np.array([res.iterations])
     out["arn_var"] = summ.variance_field
 
+    # --- config extensions: the UNMODIFIED reference pipeline
+    # (st_solve_sweep / apply_obs_weight / lr_truncate / InitInjection) with the
+    # config matrices duck-typed into SpaceTimeOperator, the (δI+γL)⁻¹ prior
+    # wrapped around it and the time-row mask inserted before the truncation,
+    # following hessian.py:211-226 line by line.
+    import math
+
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    from types import SimpleNamespace
+
+    from lrpostcov.forward import InitInjection
+
+    def q1_matrix(n, h):
+        one = np.ones(n)
+        K1 = sp.diags([-one[1:], 2 * one, -one[1:]], [-1, 0, 1]) / h
+        M1 = sp.diags([one[1:], 4 * one, one[1:]], [-1, 0, 1]) * (h / 6)
+        return sp.csr_matrix((sp.kron(M1, K1) + sp.kron(K1, M1)) / h**2)
+
+    def fd3_matrix(n, h):
+        one = np.ones(n)
+        A = sp.diags([-one[1:], 2 * one, -one[1:]], [-1, 0, 1]) / h**2
+        I = sp.identity(n)
+        return sp.csr_matrix(sp.kron(I, sp.kron(I, A)) + sp.kron(I, sp.kron(A, I))
+                             + sp.kron(A, sp.kron(I, I)))
+
+    for name, (n_side, dim, stencil, n_t, sens, every, delta, gp, sigma, rmax, seed) in {
+        "cfg_q1": (15, 2, "q1", 16, 5, 1, 1.0, 0.05, 0.01, None, 11),
+        "cfg_q1b": (24, 2, "q1", 12, 8, 1, 1.0, 0.1, 0.01, 12, 12),
+        "cfg_3d": (7, 3, "fd", 12, 3, 4, 1.0, 0.02, 0.005, None, 13),
+    }.items():
+        h = 1.0 / (n_side + 1)
+        m = h ** dim
+        L = q1_matrix(n_side, h) if stencil == "q1" else fd3_matrix(n_side, h)
+        n_x = n_side ** dim
+        grid = SimpleNamespace(n_x=n_x, m_scale=m, n_side=n_side, h=h, d=dim)
+        spatial = SimpleNamespace(grid=grid, L=L, m_scale=m, kind="heat")
+        K = lp.SpaceTimeOperator(spatial, lp.build_time_grid(n_t))
+        stride = n_side // sens
+        idx = stride // 2 + stride * np.arange(sens)
+        mask = np.zeros(n_x, bool)
+        if dim == 3:
+            mask[(idx[:, None, None] * n_side**2 + idx[None, :, None] * n_side
+                  + idx[None, None, :]).ravel()] = True
+        else:
+            mask[(idx[:, None] * n_side + idx[None, :]).ravel()] = True
+        layout = hs.SensorLayout(patches=(), mask=mask)
+        tau = 1.0 / n_t
+        beta_noise = 1.0 / (sigma**2 * tau * m)  # w = 1/sigma^2
+        cov = hs.CovarianceSpec(beta_noise=beta_noise, beta_prior=1.0, gamma_prior=1.0)
+        pol = lp.TruncationPolicy(1e-8, rmax)
+        P = spla.splu((delta * sp.identity(n_x) + gp * L).tocsc())
+        inj = InitInjection(K)
+
+        def apply(v):
+            local = []
+            x = math.sqrt(cov.gamma_prior) * P.solve(v)
+            Y = lp.st_solve_sweep(K, inj.rhs(x), pol, compress_every=4, trace=local)
+            Z = hs.apply_obs_weight(Y, layout, cov, K.time, K.m_scale, pol=None)
+            if every > 1 and Z.r:
+                keep = (np.arange(n_t) + 1) % every == 0
+                Z = lp.LowRankMat(Z.W1, np.where(keep[:, None], Z.W2, 0.0))
+            Z = lp.lr_truncate(Z, pol)
+            local.append(Z.r)
+            Q = lp.st_solve_adjoint_sweep(K, Z, pol, compress_every=4, trace=local)
+            return math.sqrt(cov.gamma_prior) * P.solve(inj.extract(Q)), max(local)
+
+        V = np.random.default_rng(seed).standard_normal((n_x, 2))
+        V /= np.linalg.norm(V, axis=0)
+        res = [apply(V[:, j]) for j in range(2)]
+        out[f"{name}_meta"] = np.array([n_side, dim, 1 if stencil == "q1" else 0, n_t, every,
+                                        delta, gp, beta_noise, -1 if rmax is None else rmax])
+        out[f"{name}_mask"] = mask
+        out[f"{name}_V"] = V
+        out[f"{name}_O"] = np.column_stack([r[0] for r in res])
+        out[f"{name}_ranks"] = np.array([r[1] for r in res])
+
     path = os.path.join(HERE, "reference_golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path} ({os.path.getsize(path) / 1e3:.0f} kB, {len(out)} arrays)")

@@ -311,3 +311,96 @@ def test_diagonal_operator_arnoldi_numpy_callable():
     res = lp.lr_arnoldi(lambda x: d * x, np.ones(5) / np.sqrt(5), POL,
                         lp.StopRule(m_a=5, eps_eig=1e-12, check_every=100))
     np.testing.assert_allclose(np.sort(res.ritz_values.real)[::-1], d, rtol=1e-10)
+
+
+# ------------------------------------------------- config extensions
+def _cfg_ctx(golden, name):
+    n_side, dim, q1, n_t, every, delta, gp, bn, rmax = golden[f"{name}_meta"]
+    grid = lp.build_grid(int(n_side), int(dim))
+    op = lp.assemble_heat(grid, "q1" if q1 else "fd")
+    K = lp.SpaceTimeOperator(op, lp.build_time_grid(int(n_t)))
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=float(delta), prior_gamma=float(gp))
+    layout = lp.SensorLayout(patches=(), mask=golden[f"{name}_mask"].astype(bool),
+                             time_every=int(every))
+    pol = lp.TruncationPolicy(1e-8, _rmax(rmax))
+    return lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=pol)
+
+
+@pytest.mark.parametrize("name", ["cfg_q1", "cfg_q1b", "cfg_3d"])
+def test_config_hessian_ic_vs_reference(golden, name):
+    """Q1-lumped / 3-D 7-point operators, (δI+γL)⁻¹ prior and time-subsampled
+    sensors against the reference pipeline run on the same matrices."""
+    ctx = _cfg_ctx(golden, name)
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    for j in range(V.shape[1]):
+        out = ctx.apply(V[:, j])
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-10 * np.linalg.norm(Oref[:, j])
+    assert ctx.rank_trace == golden[f"{name}_ranks"].tolist()
+
+
+def test_config_stencil_apply_is_the_dense_operator():
+    """Matrix-free Q1 9-point and 3-D 7-point SpMM (+ upwind) vs the assembled S."""
+    rng = np.random.default_rng(21)
+    for op in (lp.assemble_heat(lp.build_grid(7), "q1"), lp.assemble_heat(lp.build_grid(5, 3)),
+               lp.assemble_convdiff(lp.build_grid(5, 3), 0.02, (0.5, -1.0, 0.25))):
+        K = lp.SpaceTimeOperator(op, lp.build_time_grid(4))
+        Y = lp.LowRankMat(rng.standard_normal((op.grid.n_x, 2)), rng.standard_normal((4, 2)))
+        Yd = _dense(Y)
+        A = K.step_matrix.toarray()
+        ref = A @ Yd
+        ref[:, 1:] -= op.grid.m_scale * Yd[:, :-1]
+        assert np.abs(_dense(K.apply(Y)) - ref).max() < 1e-12 * np.abs(ref).max()
+        ref_t = A.T @ Yd
+        ref_t[:, :-1] -= op.grid.m_scale * Yd[:, 1:]
+        assert np.abs(_dense(K.apply_adjoint(Y)) - ref_t).max() < 1e-12 * np.abs(ref_t).max()
+
+
+def test_config_step_solve_vs_superlu():
+    rng = np.random.default_rng(22)
+    for op in (lp.assemble_heat(lp.build_grid(9), "q1"), lp.assemble_heat(lp.build_grid(6, 3))):
+        K = lp.SpaceTimeOperator(op, lp.build_time_grid(8))
+        B = rng.standard_normal((op.grid.n_x, 3))
+        ref = O.StepSolver(op.L, op.grid.m_scale, 1 / 8, 8).solve(B)
+        out = K.solve_step(B)
+        assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("dim,stencil,n_side,n_t,modes,every", [
+    (2, "q1", 256, 512, (1, 1), 1),   # the C2 operator and prior at full size
+    (2, "q1", 256, 512, (5, 3), 1),
+    (3, "fd", 64, 128, (1, 2, 1), 4),  # C4-type operator, obs every 4th step
+])
+def test_config_full_obs_eigenpairs_at_scale(dim, stencil, n_side, n_t, modes, every):
+    """μ = β τ M Σ_{k observed} θ^{2k} (δ+γλ)⁻² on DST-I modes."""
+    grid = lp.build_grid(n_side, dim)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, stencil), lp.build_time_grid(n_t))
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    prior = (1.0, 0.05)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=prior[0], prior_gamma=prior[1])
+    layout = lp.SensorLayout((), np.ones(grid.n_x, bool), time_every=every)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=POL)
+    v = O.config_eigvec(modes, n_side)
+    out = ctx.apply(v)
+    mu = O.config_ic_eigenvalue(modes, n_side, n_t, bn, 1.0, stencil, prior, every)
+    assert np.linalg.norm(out - mu * v) <= 1e-8 * mu
+
+
+def test_config_c2_subgrid_vs_oracle_mid_size():
+    """The C2 configuration (Q1-lumped, (I+0.05L)⁻¹ prior, w = 1/σ², 32x32-type
+    point subgrid) at reduced size against the oracle."""
+    n_side, n_t = 48, 96
+    grid = lp.build_grid(n_side)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, "q1"), lp.build_time_grid(n_t))
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    layout = lp.make_sensor_subgrid(grid, 6)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                            pol=lp.TruncationPolicy(1e-8, 32))
+    P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, 32, stencil="q1", prior=(1.0, 0.05))
+    rng = np.random.default_rng(23)
+    for _ in range(2):
+        v = rng.standard_normal(grid.n_x)
+        ref, r = O.hessian_ic(P, v)
+        out = ctx.apply(v)
+        assert np.linalg.norm(out - ref) <= 1e-10 * np.linalg.norm(ref)
+        assert ctx.rank_trace[-1] == r

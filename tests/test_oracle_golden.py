@@ -56,6 +56,46 @@ def test_hessian_ic_matches_reference(golden, name):
     assert ranks == golden[f"{name}_ranks"].tolist()
 
 
+CFG = ["cfg_q1", "cfg_q1b", "cfg_3d"]
+
+
+def cfg_problem(golden, name):
+    n_side, dim, q1, n_t, every, delta, gp, bn, rmax = golden[f"{name}_meta"]
+    return O.Problem(int(n_side), int(n_t), golden[f"{name}_mask"], bn, 1.0, 1e-8, _rmax(rmax),
+                     dim=int(dim), stencil="q1" if q1 else "fd", prior=(delta, gp),
+                     obs_every=int(every))
+
+
+@pytest.mark.parametrize("name", CFG)
+def test_config_hessian_ic_matches_reference(golden, name):
+    """Config extensions (Q1-lumped, 3-D 7-point, (δI+γL)⁻¹ prior, time-subsampled
+    sensors) against the unmodified reference pipeline run with the same
+    matrices duck-typed in (tests/golden/make_golden.py)."""
+    P = cfg_problem(golden, name)
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    ranks = []
+    for j in range(V.shape[1]):
+        out, r = O.hessian_ic(P, V[:, j])
+        ranks.append(r)
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-12 * np.linalg.norm(Oref[:, j])
+    assert ranks == golden[f"{name}_ranks"].tolist()
+
+
+@pytest.mark.parametrize("dim,stencil,modes,every", [
+    (2, "q1", (1, 1), 1), (2, "q1", (3, 5), 1), (2, "q1", (7, 2), 4),
+    (3, "fd", (1, 1, 1), 1), (3, "fd", (2, 1, 3), 4),
+])
+def test_config_full_observation_closed_form(dim, stencil, modes, every):
+    """μ = β τ M Σ_{k observed} θ^{2k} (δ+γλ)⁻² on DST-I modes."""
+    n_side, n_t, bn, prior = (12 if dim == 2 else 6), 16, 1e4, (1.0, 0.05)
+    P = O.Problem(n_side, n_t, np.ones(n_side ** dim, bool), bn, 1.0, 1e-10, dim=dim,
+                  stencil=stencil, prior=prior, obs_every=every)
+    v = O.config_eigvec(modes, n_side)
+    out, _ = O.hessian_ic(P, v)
+    mu = O.config_ic_eigenvalue(modes, n_side, n_t, bn, 1.0, stencil, prior, every)
+    assert np.linalg.norm(out - mu * v) <= 1e-9 * mu
+
+
 def test_hessian_source_matches_reference(golden):
     n_side, n_t, bn, bp, g = golden["hst_meta"]
     P = O.Problem(int(n_side), int(n_t), np.ones(int(n_side) ** 2, bool), bn, g)
