@@ -5,10 +5,10 @@ Workload (BASELINE.json configs[1], the metric's config): 2-D heat equation on
 [0,1]^2, 256x256 interior grid (n_x = 65,536), n_t = 512, T = 1, implicit
 Euler, fp64; initial-condition parameter; 32x32 uniform point-sensor subgrid
 observed at every step; noise sigma = 0.01 (pointwise weight 1/sigma^2,
-SURVEY Appendix D1); prior gamma = 0.05; truncation eps0 = 1e-8, rank cap 32;
-seed 1.  Operator: the reference's own 5-point FD Laplacian with lumped mass
-(discretize.py:107-112) standing in for the config's Q1 FEM (SURVEY §0 gap
-table); prior scalar gamma*I as in the reference (hessian.py:40-75).
+SURVEY Appendix D1); prior (delta I + gamma L)^-2 with delta = 1, gamma = 0.05
+(square root applied on both sides); truncation eps0 =
+1e-8, rank cap 32; seed 1.  Operator: Q1 bilinear FEM stiffness with lumped
+mass (9-point stencil), exactly the config's discretisation.
 
 One step = one prior-preconditioned misfit Hessian apply (forward sweep, obs,
 adjoint sweep; hessian.py:211-226) on a seeded N(0,1) unit probe already
@@ -38,20 +38,22 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_SIDE, N_T, SENSORS, SIGMA, GAMMA, EPS0, R_MAX, SEED, P_FLUSH = 256, 512, 32, 0.01, 0.05, 1e-8, 32, 1, 4
+N_SIDE, N_T, SENSORS, SIGMA, EPS0, R_MAX, SEED, P_FLUSH = 256, 512, 32, 0.01, 1e-8, 32, 1, 4
+PRIOR_DELTA, PRIOR_GAMMA = 1.0, 0.05
+STENCIL = "q1"
 CPU_SAMPLE_STEPS = 32   # time steps per sweep in one CPU sample (of 512)
 L2_FLUSH_BYTES = 512 << 20
 
-WORKLOAD = ("C2: 2D heat 256x256 (n_x=65536), n_t=512, FD 5-point + lumped mass (reference "
-            "operator), IC parameter, 32x32 point sensors every step, sigma=0.01 (w=1/sigma^2), "
-            "gamma=0.05, eps0=1e-8, r_max=32, compress_every=4, seed 1")
+WORKLOAD = ("C2: 2D heat 256x256 (n_x=65536), n_t=512, Q1 FEM (lumped mass, 9-point), IC "
+            "parameter, 32x32 point sensors every step, sigma=0.01 (w=1/sigma^2), prior "
+            "(I+0.05L)^-2, eps0=1e-8, r_max=32, compress_every=4, seed 1")
 
 
 def problem_scalars():
     h = 1.0 / (N_SIDE + 1)
     tau = 1.0 / N_T
     beta_noise = 1.0 / (SIGMA ** 2 * tau * h * h)  # w = beta_noise*tau*h^2 = 1/sigma^2
-    beta_prior = 1.0 / (GAMMA * h * h)
+    beta_prior = 1.0 / (h * h)  # unused by the apply; gamma_prior = 1 scales nothing
     return h, tau, beta_noise, beta_prior
 
 
@@ -80,8 +82,8 @@ def _cpu_sample(args):
     from oracle import lrk_oracle as O
 
     h, tau, bn, bp = problem_scalars()
-    P = O.Problem(N_SIDE, CPU_SAMPLE_STEPS, sensor_mask(), bn, GAMMA, EPS0, R_MAX,
-                  T=CPU_SAMPLE_STEPS * tau)
+    P = O.Problem(N_SIDE, CPU_SAMPLE_STEPS, sensor_mask(), bn, 1.0, EPS0, R_MAX,
+                  T=CPU_SAMPLE_STEPS * tau, stencil=STENCIL, prior=(PRIOR_DELTA, PRIOR_GAMMA))
     v = probes(N_SIDE * N_SIDE, 1, seed)[:, 0]
     t0 = time.perf_counter()
     for _ in range(reps):
@@ -194,8 +196,9 @@ def gpu_arm(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     h, tau, bn, bp = problem_scalars()
     grid = lp.build_grid(N_SIDE)
-    K = lp.SpaceTimeOperator(lp.assemble_heat(grid), lp.build_time_grid(N_T))
-    cov = lp.CovarianceSpec(beta_noise=bn, beta_prior=bp, gamma_prior=GAMMA)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, STENCIL), lp.build_time_grid(N_T))
+    cov = lp.CovarianceSpec(beta_noise=bn, beta_prior=bp, gamma_prior=1.0,
+                            prior_delta=PRIOR_DELTA, prior_gamma=PRIOR_GAMMA)
     ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.SensorLayout((), sensor_mask()),
                             cov=cov, pol=lp.TruncationPolicy(EPS0, R_MAX), compress_every=P_FLUSH)
     nprobe = args.steps + args.warmup
