@@ -300,7 +300,9 @@ class Problem:
         self.prior_lu = None
         if prior is not None:
             delta, gp = prior
-            self.prior_lu = spla.splu((delta * sp.identity(L.shape[0]) + gp * L).tocsc())
+            # L_Δ: the PDE's own discrete Laplacian (its diffusion part, without ν or wind)
+            Ld = L if kind == "heat" else config_operator(n_side, dim, stencil, "heat")[0]
+            self.prior_lu = spla.splu((delta * sp.identity(L.shape[0]) + gp * Ld).tocsc())
 
     def prior_sqrt(self, x):
         """Γ^{1/2} x: sqrt(γ)·x (hessian.py:215) or sqrt(γ)(δI+γ_pL)⁻¹x (config prior)."""

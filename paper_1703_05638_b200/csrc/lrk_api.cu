@@ -200,6 +200,39 @@ int subgrid_scatter(lrk_ctx* c, const double* Z, int64_t ldz, double* Y, int64_t
   return LRK_OK;
 }
 
+// Box-stencil coefficients of S = m (I + tau L) for the installed operator
+// (discretize.py:90-127 and the config extensions), mirrored for S^T.
+StencilArgs make_stencil(const lrk_operator_desc& op, bool adjoint) {
+  StencilArgs a{};
+  const double h = op.h, ih2 = 1.0 / (h * h);
+  auto cf = [&](int d1, int d2, int d3) -> double& { return a.coef[(d3 + 1) * 9 + (d2 + 1) * 3 + (d1 + 1)]; };
+  const double sc = op.kind == LRK_OP_HEAT ? 1.0 : op.nu;
+  if (op.stencil == LRK_STENCIL_Q1) {
+    // K_Q1 / h^2 with lumped mass: centre 8/3, all eight neighbours -1/3
+    for (int d2 = -1; d2 <= 1; ++d2)
+      for (int d1 = -1; d1 <= 1; ++d1) cf(d1, d2, 0) = -ih2 / 3.0;
+    cf(0, 0, 0) = 8.0 * ih2 / 3.0;
+  } else {
+    cf(0, 0, 0) = 2.0 * op.dim * sc * ih2;
+    cf(-1, 0, 0) = cf(1, 0, 0) = cf(0, -1, 0) = cf(0, 1, 0) = -sc * ih2;
+    if (op.dim == 3) cf(0, 0, -1) = cf(0, 0, 1) = -sc * ih2;
+    if (op.kind != LRK_OP_HEAT) {
+      // first-order upwind per axis by the sign of the wind (discretize.py:96-104)
+      for (int ax = 0; ax < op.dim; ++ax) {
+        const double w = op.wind[ax];
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        lo[ax] = -1; hi[ax] = 1;
+        if (w > 0) { cf(0, 0, 0) += w / h; cf(lo[0], lo[1], lo[2]) -= w / h; }
+        else if (w < 0) { cf(0, 0, 0) -= w / h; cf(hi[0], hi[1], hi[2]) += w / h; }
+      }
+    }
+  }
+  if (adjoint)
+    for (int k = 0; k < 13; ++k) std::swap(a.coef[k], a.coef[26 - k]);
+  a.n = op.n_side; a.dim = op.dim; a.m_scale = op.m_scale; a.tau = op.tau;
+  return a;
+}
+
 // ---------------------------------------------------------------- sweep
 struct SweepOut {
   double* U = nullptr;  // n_x x ucap (slot 0)
@@ -213,11 +246,17 @@ struct SweepOut {
   long long* dbg = nullptr;
 };
 
+int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, int rb,
+                   const int* rb_dev, const double* W2, int64_t ldw2, int adjoint, int p,
+                   double eps0, int r_max, SweepOut& o, cudaStream_t s);
+
 int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, int rb,
               const int* rb_dev, const double* W2, int64_t ldw2, int adjoint, int p, double eps0,
               int r_max, SweepOut& o, cudaStream_t s) {
   if (p < 1 || p > PMAX)
     return fail(c, LRK_ERR_UNSUPPORTED, "compress_every must lie in [1, 16] on the device path");
+  if (c->op.kind != LRK_OP_HEAT)
+    return run_sweep_phys(c, tag, B, ldb, rb, rb_dev, W2, ldw2, adjoint, p, eps0, r_max, o, s);
   const int64_t nx = c->n_x;
   const int nt = c->op.n_t;
   const int ucap = (r_max >= 0 && r_max < NMAX) ? std::max(r_max, 1) : NMAX;
@@ -250,6 +289,8 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   a.ybuf = ybuf; a.ldy = nx; a.qbuf = qbuf; a.ldq = nx; a.yprev = yprev;
   a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
   a.bar = bar; a.ncta = ncta;
+  a.yext = nullptr; a.ldyext = 0;
+  a.flush0 = 0; a.flush1 = nflush; a.r_init = 0;
   sweep_plan(a, nx, ncta, ucap, p, (size_t)c->smem_optin);
   a.ftz = std::getenv("LRK_FTZ") ? std::atof(std::getenv("LRK_FTZ")) : 0.0;
   WS(long long, dbg, tag + "dbg", 20);
@@ -263,6 +304,234 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   ++c->launches;
   o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
   o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
+  return LRK_OK;
+}
+
+
+// ------------------------------------------------- physical-space sweeps
+// Convection-diffusion (and any operator the DST does not diagonalise): the
+// sweep runs in physical coordinates.  The dense recurrence
+//   y_k = S^{-1}(M y_{k-1}) + B~ w2_k,   B~ = S^{-1} B      (forward.py:175-183)
+// is advanced with one preconditioned GMRES solve per step and the
+// trajectory is materialised in HBM (chunks of whole flushes); the same
+// persistent kernel then flushes it (external-trajectory mode).
+bool phys_basis(const lrk_ctx* c) { return c->op.kind != LRK_OP_HEAT; }
+
+// x = P^{-1} b, P = m (I + tau nu L_D): the diffusion part of the step
+// matrix, diagonal in the DST-I basis (dThetaM holds its inverse symbol).
+int precond_apply(lrk_ctx* c, const double* b, double* x, cudaStream_t s) {
+  const int64_t nx = c->n_x;
+  WS(double, T, "pc_T", nx);
+  TRY(dst2(c, b, nx, T, nx, 1, nullptr, 1.0, s));
+  scale_rows_kernel<<<dim3(grid1(nx, 256, 1024), 1), 256, 0, s>>>(T, nx, c->dThetaM, nx, 1,
+                                                                   nullptr, 1.0, T, nx);
+  CKL();
+  ++c->launches;
+  TRY(dst2(c, T, nx, x, nx, 1, nullptr, 1.0, s));
+  return LRK_OK;
+}
+
+int step_apply(lrk_ctx* c, const double* x, double* y, bool adjoint, cudaStream_t s) {
+  StencilArgs a = make_stencil(c->op, adjoint);
+  a.X = x; a.ldx = c->n_x; a.Y = y; a.ldy = c->n_x; a.ncols = 1;
+  stencil_kernel<<<dim3(grid1(c->n_x, 256, 1 << 30), 1), 256, 0, s>>>(a);
+  CKL();
+  ++c->launches;
+  return LRK_OK;
+}
+
+int axpby(lrk_ctx* c, const double* x, double a, const double* y, double b, double* out,
+          cudaStream_t s) {
+  axpby_kernel<<<grid1(c->n_x, 256, 2048), 256, 0, s>>>(x, a, y, b, out, c->n_x);
+  CKL();
+  ++c->launches;
+  return LRK_OK;
+}
+
+// GMRES(40) with right preconditioning P^{-1} for S x = b (S^T x = b for the
+// adjoint); CGS2 Arnoldi on the device (lrk_cgs2), Givens least squares on
+// the host; restarts until the TRUE relative residual is <= rtol.
+int gmres_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, double rtol, int* iters,
+                cudaStream_t s) {
+  const int64_t nx = c->n_x;
+  const int n = (int)nx;
+  constexpr int M = 40;
+  WS(double, Qb, "gm_Q", nx * (M + 1));
+  WS(double, z, "gm_z", nx);
+  WS(double, w, "gm_w", nx);
+  double bnorm = 0.0;
+  TRY(lrk_cgs2(c, nullptr, nx, 0, const_cast<double*>(b), n, nullptr, &bnorm, s));
+  int total = 0;
+  if (bnorm == 0.0) {
+    CK(cudaMemsetAsync(x, 0, nx * sizeof(double), s));
+    if (iters) *iters = 0;
+    return LRK_OK;
+  }
+  TRY(precond_apply(c, b, x, s));  // x0 = P^{-1} b
+  for (int restart = 0;; ++restart) {
+    TRY(step_apply(c, x, w, adjoint, s));
+    TRY(axpby(c, b, 1.0, w, -1.0, Qb, s));  // r = b - S x
+    double beta = 0.0;
+    TRY(lrk_cgs2(c, nullptr, nx, 0, Qb, n, nullptr, &beta, s));
+    if (beta <= rtol * bnorm) break;
+    if (restart >= 25)
+      return fail(c, LRK_ERR_CONVERGENCE, "GMRES step solve did not reach its tolerance");
+    TRY(axpby(c, Qb, 1.0 / beta, nullptr, 0.0, Qb, s));
+    double R[M][M] = {};
+    double cs[M], sn[M], g[M + 1] = {};
+    g[0] = beta;
+    int jend = 0;
+    for (int j = 0; j < M; ++j) {
+      double* qn = Qb + (int64_t)(j + 1) * nx;
+      TRY(precond_apply(c, Qb + (int64_t)j * nx, z, s));
+      TRY(step_apply(c, z, qn, adjoint, s));
+      double h[M + 1], hn = 0.0;
+      TRY(lrk_cgs2(c, Qb, nx, j + 1, qn, n, h, &hn, s));
+      for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+        h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+        h[i] = t;
+      }
+      const double d = std::hypot(h[j], hn);
+      cs[j] = d > 0.0 ? h[j] / d : 1.0;
+      sn[j] = d > 0.0 ? hn / d : 0.0;
+      h[j] = d;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      for (int i = 0; i <= j; ++i) R[i][j] = h[i];
+      jend = j + 1;
+      ++total;
+      if (hn == 0.0 || std::fabs(g[j + 1]) <= 0.5 * rtol * bnorm) break;
+      TRY(axpby(c, qn, 1.0 / hn, nullptr, 0.0, qn, s));
+    }
+    double y[M];
+    for (int i = jend - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int k = i + 1; k < jend; ++k) acc -= R[i][k] * y[k];
+      y[i] = R[i][i] != 0.0 ? acc / R[i][i] : 0.0;
+    }
+    TRY(lrk_combine(c, Qb, nx, jend, y, n, z, s));
+    TRY(precond_apply(c, z, w, s));
+    TRY(axpby(c, x, 1.0, w, 1.0, x, s));
+  }
+  if (iters) *iters = total;
+  return LRK_OK;
+}
+
+constexpr double STEP_RTOL = 1e-13;
+
+int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, int rb,
+                   const int* rb_dev, const double* W2, int64_t ldw2, int adjoint, int p,
+                   double eps0, int r_max, SweepOut& o, cudaStream_t s) {
+  if (p < 1 || p > PMAX)
+    return fail(c, LRK_ERR_UNSUPPORTED, "compress_every must lie in [1, 16] on the device path");
+  const int64_t nx = c->n_x;
+  const int nt = c->op.n_t;
+  int rbh = rb;
+  if (rb_dev) {
+    int v = 0;
+    CK(cudaMemcpyAsync(&v, rb_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    rbh = std::min(rb, v);
+  }
+  const int slot = adjoint ? 1 : 0;
+  if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
+  // B~ = S^{-1} B (S^{-T} B for the adjoint), one GMRES solve per column
+  WS(double, Bs, tag + "Bs", nx * (int64_t)std::max(rbh, 1));
+  int it = 0;
+  for (int j = 0; j < rbh; ++j)
+    TRY(gmres_solve(c, B + (int64_t)j * ldb, Bs + (int64_t)j * nx, adjoint, STEP_RTOL, &it, s));
+  const int ucap = (r_max >= 0 && r_max < NMAX) ? std::max(r_max, 1) : NMAX;
+  const int ncta = pick_ncta(c, nx);
+  const int nflush = (nt + p - 1) / p;
+  // trajectory chunk: whole flushes, at most 2^31 doubles (16 GiB)
+  const int64_t budget = (int64_t)1 << 31;
+  int Tc = nt;
+  if (nx * (int64_t)nt > budget) Tc = std::max<int>(p, (int)(budget / nx) / p * p);
+  WS(double, Yx, "ph_Y", nx * (int64_t)Tc);
+  WS(double, U0, tag + "U0", nx * (int64_t)ucap);
+  WS(double, U1, tag + "U1", nx * (int64_t)ucap);
+  WS(double, V0, tag + "V0", (int64_t)nt * ucap);
+  WS(double, V1, tag + "V1", (int64_t)nt * ucap);
+  WS(double, sig, tag + "sig", NMAX);
+  WS(int, info, tag + "info", 8);
+  WS(int, trace, tag + "trace", nflush + 1);
+  WS(double, ybuf, "sw_ybuf", nx * (int64_t)p);
+  WS(double, qbuf, "sw_qbuf", nx * (int64_t)p);
+  WS(double, yprev, "sw_yprev", nx);
+  WS(double, tmp, "ph_tmp", nx);
+  const int64_t pst = sweep_part_stride();
+  WS(double, part, "sw_part", 3 * (int64_t)ncta * pst);
+  const int64_t sst = sweep_scratch_stride(ncta);
+  WS(double, scratch, "sw_scratch", (int64_t)ncta * sst);
+  WS(unsigned, bar, "sw_bar", 4);
+  SweepBatch batch{};
+  batch.ngroups = 1;
+  SweepArgs& a = batch.g[0];
+  a.n_x = nx; a.n_t = nt; a.adjoint = adjoint; a.p = p; a.r_max = r_max; a.eps0 = eps0;
+  a.theta = nullptr; a.rowscale = nullptr;
+  a.B = nullptr; a.ldb = nx; a.rb = 0; a.rb_dev = nullptr;
+  a.W2 = W2; a.ldw2 = ldw2;
+  a.U0 = U0; a.U1 = U1; a.ldu = nx; a.V0 = V0; a.V1 = V1; a.ldv = nt; a.ucap = ucap;
+  a.sigma = sig; a.info = info; a.trace = trace;
+  a.ybuf = ybuf; a.ldy = nx; a.qbuf = qbuf; a.ldq = nx; a.yprev = yprev;
+  a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
+  a.bar = bar; a.ncta = ncta;
+  a.yext = Yx; a.ldyext = nx;
+  sweep_plan(a, nx, ncta, ucap, p, (size_t)c->smem_optin);
+  a.ftz = 0.0;
+  WS(long long, dbg, tag + "dbg", 20);
+  a.dbg = std::getenv("LRK_DEBUG") ? dbg : nullptr;
+  o.dbg = dbg;
+  CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
+  const double m = c->op.m_scale;
+  const double* yp = nullptr;
+  for (int cs0 = 0; cs0 < nt; cs0 += Tc) {
+    const int ce = std::min(nt, cs0 + Tc);
+    for (int j = cs0; j < ce; ++j) {
+      const int k = adjoint ? nt - 1 - j : j;  // time step advanced by processing index j
+      double* yk = Yx + (int64_t)(j - cs0) * nx;
+      if (yp) {
+        TRY(axpby(c, yp, m, nullptr, 0.0, tmp, s));
+        TRY(gmres_solve(c, tmp, yk, adjoint != 0, STEP_RTOL, &it, s));
+      } else {
+        CK(cudaMemsetAsync(yk, 0, nx * sizeof(double), s));
+      }
+      if (rbh > 0) {
+        rank_axpy_kernel<<<grid1(nx, 256, 2048), 256, 0, s>>>(Bs, nx, rbh, W2 + k, ldw2, yk, nx);
+        CKL();
+        ++c->launches;
+      }
+      if (j + 1 < ce) {
+        yp = yk;
+      } else {
+        // the chunk buffer is rewritten next: carry y_{last} in yprev
+        CK(cudaMemcpyAsync(yprev, yk, nx * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        yp = yprev;
+      }
+    }
+    a.flush0 = cs0 / p;
+    a.flush1 = std::min(nflush, (ce + p - 1) / p);
+    a.r_init = cs0 == 0 ? 0 : -1;
+    CK(launch_sweep(batch, s));
+    ++c->launches;
+  }
+  if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
+  o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
+  o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
+  return LRK_OK;
+}
+
+// Change of basis between physical coordinates and the sweep basis (DST-I,
+// an involution, for DST-diagonal operators; identity otherwise), scaled.
+int basis_xform(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int ncols,
+                const int* ncols_dev, double alpha, cudaStream_t s) {
+  if (ncols <= 0) return LRK_OK;
+  if (!phys_basis(c)) return dst2(c, X, ldx, Y, ldy, ncols, ncols_dev, alpha, s);
+  scale_cols_kernel<<<dim3(grid1(c->n_x, 256, 1024), ncols), 256, 0, s>>>(
+      X, ldx, c->n_x, nullptr, ncols_dev, ncols, alpha, Y, ldy);
+  CKL();
+  ++c->launches;
   return LRK_OK;
 }
 
@@ -322,10 +591,6 @@ int flip(lrk_ctx* c, double* U, int64_t ldu, int64_t n_x, double* V, int64_t ldv
 
 int check_op(lrk_ctx* c) {
   if (!c->has_op) return fail(c, LRK_ERR_CONFIG, "no operator installed (lrk_set_operator)");
-  if (c->op.kind != LRK_OP_HEAT)
-    return fail(c, LRK_ERR_UNSUPPORTED,
-                "device spatial solves are implemented for the heat operator only "
-                "(convection-diffusion solves are not yet on the device)");
   return LRK_OK;
 }
 
@@ -358,7 +623,11 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, 
     const int no = c->n_obs;
     WS(double, Uo, "ob_Uobs", (int64_t)no * cap);
     WS(double, Zo, "ob_Zobs", (int64_t)no * cap);
-    if (c->obs_kind == LRK_OBS_SUBGRID) {
+    if (phys_basis(c)) {
+      gather_rows_kernel<<<dim3(grid1(no, 256, 256), cap), 256, 0, s>>>(y.U, y.ldu, c->dList, no,
+                                                                         y.info, cap, Uo, no);
+      CKL();
+    } else if (c->obs_kind == LRK_OBS_SUBGRID) {
       TRY(subgrid_gather(c, y.U, y.ldu, Uo, no, cap, y.info, s));
     } else {
       WS(double, Up, "ob_Uphys", nx * (int64_t)cap);
@@ -369,7 +638,13 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, 
     }
     TRY(run_truncate(c, "ob_", no, nt, Uo, no, W2s, nt, cap, y.info, w2flag,
                      eps0, r_max, Zo, no, Zt, nt, cap, nullptr, nullptr, 1, to, s));
-    if (c->obs_kind == LRK_OBS_SUBGRID) {
+    if (phys_basis(c)) {
+      fill_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(Zh, nx, nx, cap, 0.0);
+      CKL();
+      scatter_rows_kernel<<<dim3(grid1(no, 256, 256), cap), 256, 0, s>>>(Zo, no, c->dList, no,
+                                                                          to.info, cap, Zh, nx);
+      CKL();
+    } else if (c->obs_kind == LRK_OBS_SUBGRID) {
       TRY(subgrid_scatter(c, Zo, no, Zh, nx, cap, to.info, s));
     } else {
       WS(double, Zp, "ob_Zphys", nx * (int64_t)cap);
@@ -405,6 +680,15 @@ int hd_check(lrk_ctx* c, const lrk_hessian_desc* hd) {
 int apply_prior(lrk_ctx* c, const lrk_hessian_desc* hd, double* X, int64_t ldx, int ncols,
                 const int* ncols_dev, cudaStream_t s) {
   if (!(hd->prior_gamma > 0.0) || ncols <= 0) return LRK_OK;
+  if (phys_basis(c)) {  // physical rows: through the DST and back
+    WS(double, T, "pr_T", c->n_x * (int64_t)ncols);
+    TRY(dst2(c, X, ldx, T, c->n_x, ncols, ncols_dev, 1.0, s));
+    prior_scale_kernel<<<dim3(grid1(c->n_x, 256, 1024), ncols), 256, 0, s>>>(
+        T, c->n_x, c->dLam, c->n_x, ncols, ncols_dev, 1.0, hd->prior_delta, hd->prior_gamma, T,
+        c->n_x);
+    CKL();
+    return dst2(c, T, c->n_x, X, ldx, ncols, ncols_dev, 1.0, s);
+  }
   prior_scale_kernel<<<dim3(grid1(c->n_x, 256, 1024), ncols), 256, 0, s>>>(
       X, ldx, c->dLam, c->n_x, ncols, ncols_dev, 1.0, hd->prior_delta, hd->prior_gamma, X, ldx);
   CKL();
@@ -580,7 +864,9 @@ int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
     double lam;
     if (op->stencil == LRK_STENCIL_Q1) lam = (l1[i1] * m1[i2] + m1[i1] * l1[i2]) / (h * h);
     else lam = l1[i1] + l1[i2] + (op->dim == 3 ? l1[i3] : 0.0);
-    const double t = 1.0 / (1.0 + op->tau * lam);
+    // convdiff: the DST-diagonal part m (I + tau nu L_D) is the GMRES preconditioner
+    const double lsym = op->kind == LRK_OP_HEAT ? lam : op->nu * lam;
+    const double t = 1.0 / (1.0 + op->tau * lsym);
     th[i] = t;
     thm[i] = t / op->m_scale;
     il[i] = 1.0 / lam;
@@ -647,6 +933,12 @@ int lrk_set_observation(lrk_ctx* c, const lrk_obs_desc* obs) {
     CK(cudaMemcpy(c->dS2T, S2T.data(), S2T.size() * 8, cudaMemcpyHostToDevice));
     c->s1 = s1; c->s2 = s2;
     c->n_obs = s1 * s2;
+    // physical dof list of the subgrid (x1 fastest), used by physical-space sweeps
+    std::vector<int32_t> lst((size_t)s1 * s2);
+    for (int b = 0; b < s2; ++b)
+      for (int a2 = 0; a2 < s1; ++a2) lst[(size_t)b * s1 + a2] = obs->idx2[b] * n + obs->idx1[a2];
+    CK(cudaMalloc(&c->dList, lst.size() * sizeof(int32_t)));
+    CK(cudaMemcpy(c->dList, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
   } else if (obs->kind == LRK_OBS_LIST) {
     if (obs->n_list < 0) return fail(c, LRK_ERR_CONFIG, "negative sensor count");
     c->n_obs = obs->n_list;
@@ -734,10 +1026,20 @@ int lrk_step_solve(lrk_ctx* c, const double* B, int64_t ldb, int ncols, int adjo
   if (!c) return LRK_ERR_CONFIG;
   CK(cudaSetDevice(c->device));
   TRY(check_op(c));
-  (void)adjoint;  // heat: S is symmetric, S^{-T} = S^{-1}
   cudaStream_t s = (cudaStream_t)stream;
   if (ncols <= 0) return LRK_OK;
   const int64_t nx = c->n_x;
+  if (phys_basis(c)) {  // convection-diffusion: preconditioned GMRES per column
+    WS(double, xc, "ss_x", nx);
+    WS(double, bc, "ss_b", nx);
+    for (int j = 0; j < ncols; ++j) {
+      CK(cudaMemcpyAsync(bc, B + (int64_t)j * ldb, nx * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      TRY(gmres_solve(c, bc, xc, adjoint != 0, STEP_RTOL, nullptr, s));
+      CK(cudaMemcpyAsync(X + (int64_t)j * ldx, xc, nx * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    return LRK_OK;
+  }
+  // heat: S is symmetric, S^{-T} = S^{-1}
   WS(double, T2, "ss_T2", nx * (int64_t)ncols);
   TRY(dst2(c, B, ldb, T2, nx, ncols, nullptr, 1.0, s));
   scale_rows_kernel<<<dim3(grid1(nx, 256, 1024), ncols), 256, 0, s>>>(T2, nx, c->dThetaM, nx,
@@ -752,6 +1054,7 @@ int lrk_poisson_solve(lrk_ctx* c, const double* B, int64_t ldb, int ncols, doubl
   if (!c) return LRK_ERR_CONFIG;
   CK(cudaSetDevice(c->device));
   TRY(check_op(c));
+  if (phys_basis(c)) return fail(c, LRK_ERR_UNSUPPORTED, "the steady Poisson solve is heat-only");
   cudaStream_t s = (cudaStream_t)stream;
   if (ncols <= 0) return LRK_OK;
   const int64_t nx = c->n_x;
@@ -773,34 +1076,8 @@ int lrk_operator_apply(lrk_ctx* c, const lrk_lr* Y, int adjoint, lrk_lr* out, vo
   if (out->cap < 2 * r) return fail(c, LRK_ERR_SHAPE, "output capacity must be >= 2r");
   if (r == 0) { out->r = 0; return LRK_OK; }
   const lrk_operator_desc& op = c->op;
-  const double h = op.h, ih2 = 1.0 / (h * h);
-  StencilArgs a{};
-  auto cf = [&](int d1, int d2, int d3) -> double& { return a.coef[(d3 + 1) * 9 + (d2 + 1) * 3 + (d1 + 1)]; };
-  const double sc = op.kind == LRK_OP_HEAT ? 1.0 : op.nu;
-  if (op.stencil == LRK_STENCIL_Q1) {
-    // K_Q1 / h^2 with lumped mass: centre 8/3, all eight neighbours -1/3
-    for (int d2 = -1; d2 <= 1; ++d2)
-      for (int d1 = -1; d1 <= 1; ++d1) cf(d1, d2, 0) = -ih2 / 3.0;
-    cf(0, 0, 0) = 8.0 * ih2 / 3.0;
-  } else {
-    cf(0, 0, 0) = 2.0 * op.dim * sc * ih2;
-    cf(-1, 0, 0) = cf(1, 0, 0) = cf(0, -1, 0) = cf(0, 1, 0) = -sc * ih2;
-    if (op.dim == 3) cf(0, 0, -1) = cf(0, 0, 1) = -sc * ih2;
-    if (op.kind != LRK_OP_HEAT) {
-      // first-order upwind per axis by the sign of the wind (discretize.py:96-104)
-      for (int ax = 0; ax < op.dim; ++ax) {
-        const double w = op.wind[ax];
-        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-        lo[ax] = -1; hi[ax] = 1;
-        if (w > 0) { cf(0, 0, 0) += w / h; cf(lo[0], lo[1], lo[2]) -= w / h; }
-        else if (w < 0) { cf(0, 0, 0) -= w / h; cf(hi[0], hi[1], hi[2]) += w / h; }
-      }
-    }
-  }
-  if (adjoint)
-    for (int k = 0; k < 13; ++k) std::swap(a.coef[k], a.coef[26 - k]);
-  a.X = Y->W1; a.ldx = Y->ld1; a.Y = out->W1; a.ldy = out->ld1; a.n = c->n; a.dim = op.dim;
-  a.ncols = r; a.m_scale = op.m_scale; a.tau = op.tau;
+  StencilArgs a = make_stencil(op, adjoint != 0);
+  a.X = Y->W1; a.ldx = Y->ld1; a.Y = out->W1; a.ldy = out->ld1; a.ncols = r;
   stencil_kernel<<<dim3(grid1(c->n_x, 256, 1 << 30), r), 256, 0, s>>>(a);
   CKL();
   // W2 copy into the first r columns; shift + (-M W1) into the second r
@@ -829,7 +1106,7 @@ int lrk_st_solve_sweep(lrk_ctx* c, const lrk_lr* rhs, int adjoint, int compress_
   const int64_t nx = c->n_x;
   const int nt = c->op.n_t;
   WS(double, Bh, "api_B", nx * (int64_t)rhs->r);
-  TRY(dst2(c, rhs->W1, rhs->ld1, Bh, nx, rhs->r, nullptr, 1.0, s));
+  TRY(basis_xform(c, rhs->W1, rhs->ld1, Bh, nx, rhs->r, nullptr, 1.0, s));
   SweepOut o;
   TRY(run_sweep(c, "s0_", Bh, nx, rhs->r, nullptr, rhs->W2, rhs->ld2, adjoint, compress_every, eps0,
                 r_max, o, s));
@@ -840,7 +1117,7 @@ int lrk_st_solve_sweep(lrk_ctx* c, const lrk_lr* rhs, int adjoint, int compress_
   const int r = info[0];
   if (r > out->cap) return fail(c, LRK_ERR_SHAPE, "output capacity too small for the pane rank");
   if (r > 0) {
-    TRY(dst2(c, o.U, o.ldu, out->W1, out->ld1, r, nullptr, 1.0, s));
+    TRY(basis_xform(c, o.U, o.ldu, out->W1, out->ld1, r, nullptr, 1.0, s));
     scale_cols_kernel<<<dim3(grid1(nt, 256, 64), r), 256, 0, s>>>(o.V, o.ldv, nt, o.sigma, nullptr,
                                                                    r, 1.0, out->W2, out->ld2);
     CKL();
@@ -872,7 +1149,7 @@ int lrk_hessian_apply_ic(lrk_ctx* c, const lrk_hessian_desc* hd, int nbatch, con
     const double* v = V + (int64_t)b * ldv;
     double* out = OUT + (int64_t)b * ldo;
     // inject: rhs = (M sqrt(g) v) e_0^T, spectral  (forward.py:108-109)
-    TRY(dst2(c, v, nx, Bv, nx, 1, nullptr, sg * M, s));
+    TRY(basis_xform(c, v, nx, Bv, nx, 1, nullptr, sg * M, s));
     TRY(apply_prior(c, hd, Bv, nx, 1, nullptr, s));
     SweepOut fw, bw;
     TRY(run_sweep(c, "f_", Bv, nx, 1, nullptr, c->dE0, nt, 0, hd->compress_every, hd->eps0,
@@ -889,7 +1166,7 @@ int lrk_hessian_apply_ic(lrk_ctx* c, const lrk_hessian_desc* hd, int nbatch, con
                                                               bw.ldv, 0, bw.info, q);
     CKL();
     TRY(apply_prior(c, hd, q, nx, 1, nullptr, s));
-    TRY(dst2(c, q, nx, out, nx, 1, nullptr, sg * M, s));
+    TRY(basis_xform(c, q, nx, out, nx, 1, nullptr, sg * M, s));
     int mr = 0;
     TRY(host_max_rank(c, fw, zinfo, bw, nullptr, &mr, hd->compress_every, 1, 1, s));
     if (max_rank) max_rank[b] = mr;
@@ -911,7 +1188,7 @@ int lrk_hessian_apply_st(lrk_ctx* c, const lrk_hessian_desc* hd, const lrk_lr* v
   const double M = c->op.m_scale, tau = c->op.tau, sg = std::sqrt(hd->gamma_prior);
   WS(double, Bh, "st_B", nx * (int64_t)v->r);
   // rhs = tau M sqrt(g) v  (forward.py:121-122, hessian.py:236)
-  TRY(dst2(c, v->W1, v->ld1, Bh, nx, v->r, nullptr, tau * M * sg, s));
+  TRY(basis_xform(c, v->W1, v->ld1, Bh, nx, v->r, nullptr, tau * M * sg, s));
   TRY(apply_prior(c, hd, Bh, nx, v->r, nullptr, s));
   SweepOut fw, bw;
   TRY(run_sweep(c, "f_", Bh, nx, v->r, nullptr, v->W2, v->ld2, 0, hd->compress_every, hd->eps0,
@@ -927,15 +1204,25 @@ int lrk_hessian_apply_st(lrk_ctx* c, const lrk_hessian_desc* hd, const lrk_lr* v
   const int cap = bw.ucap;
   WS(double, Up, "st_Uphys", nx * (int64_t)cap);
   WS(double, W2o, "st_W2o", (int64_t)nt * cap);
-  const double* Uspec = bw.U;
-  if (hd->prior_gamma > 0.0) {
-    WS(double, Up2, "st_Uprior", nx * (int64_t)cap);
+  if (hd->prior_gamma > 0.0 && !phys_basis(c)) {
+    // spectral rows: prior factor, then one DST to physical rows
+    WS(double, Tp, "st_Tprior", nx * (int64_t)cap);
     prior_scale_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(
-        bw.U, bw.ldu, c->dLam, nx, cap, bw.info, 1.0, hd->prior_delta, hd->prior_gamma, Up2, nx);
+        bw.U, bw.ldu, c->dLam, nx, cap, bw.info, 1.0, hd->prior_delta, hd->prior_gamma, Tp, nx);
     CKL();
-    Uspec = Up2;
+    TRY(dst2(c, Tp, nx, Up, nx, cap, bw.info, 1.0, s));
+  } else {
+    TRY(basis_xform(c, bw.U, bw.ldu, Up, nx, cap, bw.info, 1.0, s));
   }
-  TRY(dst2(c, Uspec, Uspec == bw.U ? bw.ldu : nx, Up, nx, cap, bw.info, 1.0, s));
+  if (hd->prior_gamma > 0.0 && phys_basis(c)) {
+    // prior on the output's spatial factor (physical rows)
+    WS(double, Tp, "st_Tprior", nx * (int64_t)cap);
+    TRY(dst2(c, Up, nx, Tp, nx, cap, bw.info, 1.0, s));
+    prior_scale_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(
+        Tp, nx, c->dLam, nx, cap, bw.info, 1.0, hd->prior_delta, hd->prior_gamma, Tp, nx);
+    CKL();
+    TRY(dst2(c, Tp, nx, Up, nx, cap, bw.info, 1.0, s));
+  }
   scale_cols_kernel<<<dim3(grid1(nt, 256, 64), cap), 256, 0, s>>>(bw.V, bw.ldv, nt, bw.sigma,
                                                                    bw.info, cap, sg * tau * M, W2o, nt);
   CKL();

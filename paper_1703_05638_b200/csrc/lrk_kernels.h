@@ -37,6 +37,14 @@ struct SweepArgs {
   unsigned* bar;           // 2 unsigned per group
   int ncta;
   long long* dbg;          // optional per-phase cycle counters (10), CTA 0
+  // external-trajectory mode (physical-space solvers, e.g. convection-diffusion):
+  // when yext != NULL the buffered columns are read from yext (column j = the
+  // j-th step processed by this launch) instead of the spectral recurrence.
+  const double* yext; int64_t ldyext;
+  // chunked execution: flushes [flush0, flush1) of the full schedule, resuming
+  // from a pane of rank r_init held in U0 / V0 / sigma (r_init < 0: the rank
+  // the previous chunk left in info[0]; every chunk must contain a flush)
+  int flush0, flush1, r_init;
   // shared-memory plan (offsets in doubles, computed by sweep_plan)
   int resident;            // 1: CTA row blocks of U/Y/Q~ live in shared memory
   int mp;                  // padded rows per CTA (leading dim of resident blocks)

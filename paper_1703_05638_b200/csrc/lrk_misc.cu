@@ -70,6 +70,26 @@ __global__ void prior_scale_kernel(const double* X, int64_t ldx, const double* l
     Y[i + (int64_t)c * ldy] = alpha * X[i + (int64_t)c * ldx] / (delta + gamma * lam[i]);
 }
 
+// y += B w, B n x rb (ld ldb), w strided by ldw (one row of a time factor):
+// the rhs term B~ w2_k of a physical-space sweep step.
+__global__ void rank_axpy_kernel(const double* B, int64_t ldb, int rb, const double* w,
+                                 int64_t ldw, double* y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = y[i];
+    for (int j = 0; j < rb; ++j) acc += B[i + (int64_t)j * ldb] * w[(int64_t)j * ldw];
+    y[i] = acc;
+  }
+}
+
+// out = a x + b y (y may be NULL when b == 0)
+__global__ void axpby_kernel(const double* x, double a, const double* y, double b, double* out,
+                             int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + (b != 0.0 ? b * y[i] : 0.0);
+}
+
 // Zero the rows k of a time factor with (k+1) % every != 0 (time-subsampled
 // sensors).
 __global__ void mask_time_rows_kernel(double* W2, int64_t ld2, int n_t, int ncols, int every) {

@@ -24,6 +24,10 @@ __global__ void shift_kernel(const double* W2, int64_t ld2, int n_t, int ncols, 
 __global__ void prior_scale_kernel(const double* X, int64_t ldx, const double* lam, int64_t n,
                                    int ncols, const int* ncols_dev, double alpha, double delta,
                                    double gamma, double* Y, int64_t ldy);
+__global__ void rank_axpy_kernel(const double* B, int64_t ldb, int rb, const double* w,
+                                 int64_t ldw, double* y, int64_t n);
+__global__ void axpby_kernel(const double* x, double a, const double* y, double b, double* out,
+                             int64_t n);
 __global__ void mask_time_rows_kernel(double* W2, int64_t ld2, int n_t, int ncols, int every);
 __global__ void scale_rows_kernel(const double* X, int64_t ldx, const double* s, int64_t n,
                                   int ncols, const int* ncols_dev, double alpha, double* Y,

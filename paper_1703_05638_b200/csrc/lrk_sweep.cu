@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     ldvl = a.tp;
     for (int i = tid; i < m_loc; i += NT) {
       sm[a.off_yp + i] = 0.0;
-      sm[a.off_th + i] = a.theta[r0 + i];
+      sm[a.off_th + i] = a.theta ? a.theta[r0 + i] : 0.0;
       sm[a.off_rs + i] = a.rowscale ? a.rowscale[r0 + i] : 1.0;
     }
   } else {
@@ -251,14 +251,31 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     tprev = t_;                     \
   }
 
-  int r = 0;
+  int r = a.r_init >= 0 ? a.r_init : a.info[0];  // < 0: rank left by the previous chunk
   int jac_sweeps = 0;
   const int nflush = (n_t + p - 1) / p;
-  for (int f = 0; f < nflush; ++f) {
+  if (r > 0) {  // resume a chunked sweep: the pane comes back from global memory
+    for (int k = tid; k < r; k += NT) sSig[k] = a.sigma[k];
+    if constexpr (RES)
+      for (int c = 0; c < r; ++c) {
+        for (int i = tid; i < m_loc; i += NT) Ul[i + (int64_t)c * ldu] = a.U0[r0 + i + (int64_t)c * a.ldu];
+        for (int64_t t = t0 + tid; t < t1; t += NT)
+          Vl[(t - t0) + (int64_t)c * ldvl] = a.V0[t + (int64_t)c * a.ldv];
+      }
+    __syncthreads();
+  }
+  for (int f = a.flush0; f < a.flush1; ++f) {
     const int start = f * p;
     const int pc = (n_t - start) < p ? (n_t - start) : p;
     // ---------------- phase 1: buffered columns (row-local) + projections
-    {
+    if (a.yext) {
+      const double* ye = a.yext + r0 + (int64_t)(start - a.flush0 * p) * a.ldyext;
+      for (int i = tid; i < m_loc; i += NT) {
+#pragma unroll
+        for (int s = 0; s < Q; ++s)
+          if (s < pc) Yl[i + (int64_t)s * ldy] = ye[i + (int64_t)s * a.ldyext];
+      }
+    } else {
       int ks[Q];
 #pragma unroll
       for (int s = 0; s < Q; ++s) ks[s] = a.adjoint ? (n_t - 1 - (start + s)) : (start + s);
@@ -554,7 +571,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       a.info[0] = r;
       a.info[1] = 0;
       a.info[3] = jac_sweeps;
-      a.trace[nflush] = r;
+      if (a.flush1 == nflush) a.trace[nflush] = r;
     }
   }
 }

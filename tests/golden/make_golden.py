@@ -141,6 +141,45 @@ def main():
     out["arn_iters"] = np.array([res.iterations])
     out["arn_var"] = summ.variance_field
 
+    # --- convection-diffusion (the reference's own operator, discretize.py:115-127)
+    for name, (n_side, n_t, nu, wind, adjoint, seed) in {
+        "cdsw_a": (9, 8, 0.05, (1.0, -0.5), False, 31),
+        "cdsw_b": (12, 10, 0.02, (-0.7, 1.3), True, 32),
+    }.items():
+        rng = np.random.default_rng(seed)
+        grid = lp.build_grid(n_side)
+        K = lp.SpaceTimeOperator(lp.assemble_convdiff(grid, nu, wind), lp.build_time_grid(n_t))
+        rhs = lp.lr_truncate(lp.LowRankMat(rng.standard_normal((grid.n_x, 2)),
+                                           rng.standard_normal((n_t, 2))), lp.TruncationPolicy())
+        tr = []
+        Y = lp.st_solve_sweep(K, rhs, lp.TruncationPolicy(), adjoint=adjoint, trace=tr)
+        out[f"{name}_meta"] = np.array([n_side, n_t, int(adjoint), nu, wind[0], wind[1]])
+        out[f"{name}_R1"], out[f"{name}_R2"] = rhs.W1, rhs.W2
+        out[f"{name}_Y1"], out[f"{name}_Y2"] = Y.W1, Y.W2
+        out[f"{name}_trace"] = np.array(tr)
+    for name, (n_side, n_t, nu, wind, seed) in {
+        "hcd_a": (15, 12, 0.05, (1.0, -0.5), 33),
+        "hcd_b": (16, 16, 0.02, (0.4, 0.9), 34),
+    }.items():
+        grid = lp.build_grid(n_side)
+        K = lp.SpaceTimeOperator(lp.assemble_convdiff(grid, nu, wind), lp.build_time_grid(n_t))
+        stride = n_side // 4
+        idx = stride // 2 + stride * np.arange(4)
+        mask = np.zeros(grid.n_x, bool)
+        mask[(idx[:, None] * n_side + idx[None, :]).ravel()] = True
+        layout = hs.SensorLayout(patches=(), mask=mask)
+        cov = hs.CovarianceSpec.from_gamma(1.0, 1e5, grid)
+        ctx = hs.HessianContext(mode=hs.MODE_IC, operator=K, layout=layout, cov=cov,
+                                pol=lp.TruncationPolicy(1e-8))
+        V = np.random.default_rng(seed).standard_normal((grid.n_x, 2))
+        V /= np.linalg.norm(V, axis=0)
+        O = np.column_stack([ctx.apply(V[:, j]) for j in range(2)])
+        out[f"{name}_meta"] = np.array([n_side, n_t, nu, wind[0], wind[1], cov.beta_noise,
+                                        cov.beta_prior, cov.gamma_prior])
+        out[f"{name}_mask"] = mask
+        out[f"{name}_V"], out[f"{name}_O"] = V, O
+        out[f"{name}_ranks"] = np.array(ctx.rank_trace)
+
     # --- config extensions: the UNMODIFIED reference pipeline
     # (st_solve_sweep / apply_obs_weight / lr_truncate / InitInjection) with the
     # config matrices duck-typed into SpaceTimeOperator, the (δI+γL)⁻¹ prior

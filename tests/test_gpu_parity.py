@@ -404,3 +404,71 @@ def test_config_c2_subgrid_vs_oracle_mid_size():
         out = ctx.apply(v)
         assert np.linalg.norm(out - ref) <= 1e-10 * np.linalg.norm(ref)
         assert ctx.rank_trace[-1] == r
+
+
+# ------------------------------------------------- convection-diffusion (physical-space sweep)
+def _convdiff(n_side, n_t, nu, wind):
+    grid = lp.build_grid(n_side)
+    return grid, lp.SpaceTimeOperator(lp.assemble_convdiff(grid, nu, wind), lp.build_time_grid(n_t))
+
+
+def test_convdiff_step_solve_vs_superlu():
+    """Preconditioned device GMRES step solve (and its transpose) vs SuperLU."""
+    rng = np.random.default_rng(31)
+    for n_side, n_t, nu, wind in ((9, 5, 1e-2, (0.3, -1.0)), (32, 64, 0.05, (1.0, -0.6))):
+        grid, K = _convdiff(n_side, n_t, nu, wind)
+        L, h, m = O.fd_operator(n_side, "convdiff", nu, wind)
+        solver = O.StepSolver(L, m, 1.0 / n_t, n_t)
+        B = rng.standard_normal((grid.n_x, 3))
+        for adj in (False, True):
+            ref = solver.solve(B, adjoint=adj)
+            out = K.solve_step(B, adjoint=adj)
+            assert np.linalg.norm(out - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("name", ["cdsw_a", "cdsw_b"])
+def test_convdiff_sweep_vs_reference(golden, name):
+    n_side, n_t, adjoint, nu, w1, w2 = golden[f"{name}_meta"]
+    _, K = _convdiff(int(n_side), int(n_t), nu, (w1, w2))
+    rhs = lp.LowRankMat(golden[f"{name}_R1"], golden[f"{name}_R2"])
+    tr = []
+    Y = lp.st_solve_sweep(K, rhs, POL, adjoint=bool(adjoint), trace=tr)
+    assert tr == golden[f"{name}_trace"].tolist()
+    ref = golden[f"{name}_Y1"] @ golden[f"{name}_Y2"].T
+    assert np.linalg.norm(_dense(Y) - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("name", ["hcd_a", "hcd_b"])
+def test_convdiff_hessian_ic_vs_reference(golden, name):
+    n_side, n_t, nu, w1, w2, bn, bp, g = golden[f"{name}_meta"]
+    _, K = _convdiff(int(n_side), int(n_t), nu, (w1, w2))
+    layout = lp.SensorLayout(patches=(), mask=golden[f"{name}_mask"].astype(bool))
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=lp.CovarianceSpec(bn, bp, g),
+                            pol=POL)
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    for j in range(V.shape[1]):
+        out = ctx.apply(V[:, j])
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-10 * np.linalg.norm(Oref[:, j])
+    assert ctx.rank_trace == golden[f"{name}_ranks"].tolist()
+
+
+def test_convdiff_hessian_mid_size_vs_oracle_and_adjointness():
+    """C3-type physics at reduced size (64², n_t 64, ν = 1/20, 8x8 sensors):
+    oracle parity and symmetry <u, H v> = <H u, v> of the misfit Hessian."""
+    n_side, n_t, nu, wind = 64, 64, 0.05, (1.0, -0.5)
+    grid, K = _convdiff(n_side, n_t, nu, wind)
+    layout = lp.make_sensor_subgrid(grid, 8)
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                            pol=lp.TruncationPolicy(1e-8, 48))
+    P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, 48, kind="convdiff", nu=nu, wind=wind,
+                  prior=(1.0, 0.05))
+    rng = np.random.default_rng(35)
+    u, v = rng.standard_normal(grid.n_x), rng.standard_normal(grid.n_x)
+    ref, r = O.hessian_ic(P, v)
+    Hv = ctx.apply(v)
+    assert np.linalg.norm(Hv - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert ctx.rank_trace[-1] == r
+    Hu = ctx.apply(u)
+    assert abs(u @ Hv - Hu @ v) <= 1e-7 * abs(u @ Hv)

@@ -34,6 +34,32 @@ def test_sweep_matches_reference(golden, name):
     assert np.linalg.norm(Y1 @ Y2.T - ref) <= 1e-13 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("name", ["cdsw_a", "cdsw_b"])
+def test_convdiff_sweep_matches_reference(golden, name):
+    n_side, n_t, adjoint, nu, w1, w2 = golden[f"{name}_meta"]
+    L, h, m = O.fd_operator(int(n_side), "convdiff", nu, (w1, w2))
+    solver = O.StepSolver(L, m, 1.0 / n_t, int(n_t))
+    Y1, Y2, tr = O.sweep(solver, golden[f"{name}_R1"], golden[f"{name}_R2"], 1e-8, None,
+                         bool(adjoint))
+    assert tr == golden[f"{name}_trace"].tolist()
+    ref = golden[f"{name}_Y1"] @ golden[f"{name}_Y2"].T
+    assert np.linalg.norm(Y1 @ Y2.T - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("name", ["hcd_a", "hcd_b"])
+def test_convdiff_hessian_ic_matches_reference(golden, name):
+    n_side, n_t, nu, w1, w2, bn, bp, g = golden[f"{name}_meta"]
+    P = O.Problem(int(n_side), int(n_t), golden[f"{name}_mask"], bn, g, 1e-8, kind="convdiff",
+                  nu=nu, wind=(w1, w2))
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    ranks = []
+    for j in range(V.shape[1]):
+        out, r = O.hessian_ic(P, V[:, j])
+        ranks.append(r)
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-12 * np.linalg.norm(Oref[:, j])
+    assert ranks == golden[f"{name}_ranks"].tolist()
+
+
 def test_gmres_matches_reference(golden):
     L, h, m = O.fd_operator(15)
     solver = O.StepSolver(L, m, 0.1, 10)

@@ -17,7 +17,40 @@ __global__ void k_jac(const double* M, int n, double* U, double* V, double* s, i
   extern __shared__ double scr[];
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) A[(i % n) + (i / n) * 33] = M[i];
   __syncthreads();
-  if constexpr (JW == 5) {
+  if constexpr (JW == 9) {  // stacked TSQR of 148 4x4 blocks (M holds the part buffer)
+    long long t0 = clock64();
+    int wo = 0;
+    for (int r = 0; r < reps; ++r) {
+      wo += warp_stack_tsqr<4, 3>(M, 16, 148, 4, 77, A, scr, scr + 64);
+      __syncthreads();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / reps; sweeps[0] = wo; }
+    if (threadIdx.x < 16) U[threadIdx.x] = scr[threadIdx.x] + scr[64 + threadIdx.x];
+  } else if constexpr (JW == 6) {  // the two preconditioning QRs only
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      if (threadIdx.x < 32) {
+        double a[NJ];
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int i = 0; i < NJ; ++i) a[i] = (lane < n && i < n) ? A[i + lane * 33] : 0.0;
+        int colid;
+        warp_qr_cols<NJ, true>(a, n, scr, 33, scr + 2000, colid);
+        warp_qr_cols<NJ, false>(a, n, scr + 3000, 33, scr + 5000, colid);
+        if (lane < n) U[lane] = a[0] + colid;
+      }
+      __syncthreads();
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / reps; sweeps[0] = 1; }
+  } else if constexpr (JW == 8) {  // all warps, convergent call site
+    long long t0 = clock64();
+    int sw = 0;
+    for (int r = 0; r < reps; ++r) sw += multi_warp_jacobi<NJ, 8>(A, 33, n, U, V, n, s, perm, gbuf);
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { cyc[0] = (t1 - t0) / reps; sweeps[0] = sw / reps; }
+  } else if constexpr (JW == 5) {
     long long t0 = clock64();
     int sw = 0;
     for (int r = 0; r < reps; ++r) {
@@ -63,6 +96,16 @@ int main(int argc, char** argv) {
   if (jw == 1) { if (n <= 16) LAUNCH(16, 1); else if (n <= 24) LAUNCH(24, 1); else LAUNCH(32, 1); }
   else if (jw == 4) { if (n <= 16) LAUNCH(16, 4); else if (n <= 24) LAUNCH(24, 4); else LAUNCH(32, 4); }
   else if (jw == 5) { if (n <= 16) LAUNCH(16, 5); else if (n <= 24) LAUNCH(24, 5); else LAUNCH(32, 5); }
+  else if (jw == 9) {
+    std::vector<double> P(148 * 16);
+    for (auto& x : P) x = rnd();
+    double* dP;
+    cudaMalloc(&dP, 8 * P.size());
+    cudaMemcpy(dP, P.data(), 8 * P.size(), cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(k_jac<16, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, PRECOND_SCR * 8);
+    k_jac<16, 9><<<1, 256, PRECOND_SCR * 8>>>(dP, n, dU, dV, ds, dp, dc, dsw, 20);
+  }
+  else if (jw == 6) { if (n <= 16) LAUNCH(16, 6); else if (n <= 24) LAUNCH(24, 6); else LAUNCH(32, 6); }
   else { if (n <= 16) LAUNCH(16, 8); else if (n <= 24) LAUNCH(24, 8); else LAUNCH(32, 8); }
   long long cyc;
   int sw;
