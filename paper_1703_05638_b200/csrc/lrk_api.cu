@@ -44,6 +44,8 @@ struct lrk_ctx {
   double* dE0 = nullptr;      // n_t: e_0
   double* dInvLam = nullptr;  // n_x: 1/lambda (steady Poisson solve)
   double* dLam = nullptr;     // n_x: lambda (config prior (delta + gamma lambda)^{-1})
+  int rich_it = 0;            // physical step solves: Richardson sweeps (0 unknown, -1 GMRES)
+  double rich_q = 1.0;        // measured contraction of I - P^{-1} S
   // observation
   bool has_obs = false;
   int obs_kind = LRK_OBS_FULL;
@@ -140,13 +142,15 @@ int pick_ncta(lrk_ctx* c, int64_t rows) {
 // --------------------------------------------------------------- GEMMs
 int gemm(lrk_ctx* c, int M, int N, int K, const double* A, int64_t lda, int64_t sA,
          const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-         double alpha, int batch, const int* batch_dev, cudaStream_t s, int batch_mult = 1) {
+         double alpha, int batch, const int* batch_dev, cudaStream_t s, int batch_mult = 1,
+         const double* emul = nullptr, int64_t lde = 0, double beta = 0.0) {
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.A = A; g.lda = lda; g.sA = sA;
   g.B = B; g.ldb = ldb; g.sB = sB;
   g.C = C; g.ldc = ldc; g.sC = sC;
-  g.alpha = alpha; g.beta = 0.0;
+  g.alpha = alpha; g.beta = beta;
+  g.emul = emul; g.lde = lde;
   g.batch = batch; g.batch_dev = batch_dev; g.batch_mult = batch_mult;
   g.m_dev = nullptr; g.m_mult = 1;
   CK(launch_gemm(g, s));
@@ -156,8 +160,11 @@ int gemm(lrk_ctx* c, int M, int N, int K, const double* A, int64_t lda, int64_t 
 
 // Y[:, j] = alpha * (S (x) S [(x) S]) X[:, j]: 2-D or 3-D DST-I of each column
 // (x1 fastest), one DMMA GEMM pass per axis.
+// Optional epilogue on the last pass: Y = alpha * DST(X) .* emul + beta * Y
+// (emul: an n_x array in the x1-fastest layout, shared by all columns).
 int dst2(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int ncols,
-         const int* ncols_dev, double alpha, cudaStream_t s) {
+         const int* ncols_dev, double alpha, cudaStream_t s, const double* emul = nullptr,
+         double beta = 0.0) {
   if (ncols <= 0) return LRK_OK;
   const int n = c->n;
   const int64_t nx = c->n_x;
@@ -166,7 +173,8 @@ int dst2(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int n
     // T_j = X_j S      (X_j: n x n row-major view of column j)
     TRY(gemm(c, n, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
     // Y_j = alpha S T_j
-    TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s));
+    TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s, 1, emul,
+             n, beta));
     return LRK_OK;
   }
   const int64_t pl = (int64_t)n * n;
@@ -176,7 +184,8 @@ int dst2(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int n
   // x2: per (column, x3-plane) slice: T2 = S T_slice  (batch ncols * n, stride n^2)
   TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, pl, T2, n, pl, 1.0, ncols * n, ncols_dev, s, n));
   // x3: Y_j = alpha S T2_j, T2_j viewed as n x (n^2) row-major
-  TRY(gemm(c, n, (int)pl, n, c->dS, n, 0, T2, pl, nx, Y, pl, ldy, alpha, ncols, ncols_dev, s));
+  TRY(gemm(c, n, (int)pl, n, c->dS, n, 0, T2, pl, nx, Y, pl, ldy, alpha, ncols, ncols_dev, s, 1,
+           emul, pl, beta));
   return LRK_OK;
 }
 
@@ -319,15 +328,13 @@ bool phys_basis(const lrk_ctx* c) { return c->op.kind != LRK_OP_HEAT; }
 
 // x = P^{-1} b, P = m (I + tau nu L_D): the diffusion part of the step
 // matrix, diagonal in the DST-I basis (dThetaM holds its inverse symbol).
-int precond_apply(lrk_ctx* c, const double* b, double* x, cudaStream_t s) {
+// (beta = 1: x += P^{-1} b; the spectral scaling and the accumulation ride in
+// the DST GEMM epilogues.)
+int precond_apply(lrk_ctx* c, const double* b, double* x, cudaStream_t s, double beta = 0.0) {
   const int64_t nx = c->n_x;
   WS(double, T, "pc_T", nx);
-  TRY(dst2(c, b, nx, T, nx, 1, nullptr, 1.0, s));
-  scale_rows_kernel<<<dim3(grid1(nx, 256, 1024), 1), 256, 0, s>>>(T, nx, c->dThetaM, nx, 1,
-                                                                   nullptr, 1.0, T, nx);
-  CKL();
-  ++c->launches;
-  TRY(dst2(c, T, nx, x, nx, 1, nullptr, 1.0, s));
+  TRY(dst2(c, b, nx, T, nx, 1, nullptr, 1.0, s, c->dThetaM, 0.0));
+  TRY(dst2(c, T, nx, x, nx, 1, nullptr, 1.0, s, nullptr, beta));
   return LRK_OK;
 }
 
@@ -420,6 +427,83 @@ int gmres_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, double rto
 
 constexpr double STEP_RTOL = 1e-13;
 
+// Sync-free preconditioned Richardson for S x = b:  x <- x + P^{-1}(b - S x),
+// a fixed number of sweeps c->rich_it chosen from the contraction factor
+// measured once per operator (rich_setup); the true residual is checked on
+// the device and any miss raises *flag (the caller redoes the work with GMRES).
+int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, cudaStream_t s) {
+  const int64_t nx = c->n_x;
+  WS(double, r, "rs_r", nx);
+  WS(double, part, "rs_part", 2 * 296);
+  WS(unsigned, cnt, "rs_cnt", 1);
+  TRY(precond_apply(c, b, x, s));
+  StencilArgs a = make_stencil(c->op, adjoint);
+  a.X = x; a.ldx = nx; a.Y = r; a.ldy = nx; a.ncols = 1; a.Bres = b; a.ldbres = nx;
+  for (int it = 0; it < c->rich_it; ++it) {
+    stencil_kernel<<<dim3(grid1(nx, 256, 1 << 30), 1), 256, 0, s>>>(a);
+    CKL();
+    ++c->launches;
+    TRY(precond_apply(c, r, x, s, 1.0));
+  }
+  if (flag) {
+    stencil_kernel<<<dim3(grid1(nx, 256, 1 << 30), 1), 256, 0, s>>>(a);
+    CKL();
+    resid_flag_kernel<<<296, 256, 0, s>>>(r, b, nx, STEP_RTOL * STEP_RTOL, part, cnt, flag);
+    CKL();
+    c->launches += 2;
+  }
+  return LRK_OK;
+}
+
+// Measure q = ||I - P^{-1} S|| on a fixed pseudo-random vector and choose the
+// Richardson sweep count (rich_it = -1: contraction too weak, use GMRES).
+int rich_setup(lrk_ctx* c, cudaStream_t s) {
+  if (c->rich_it != 0) return LRK_OK;
+  const int64_t nx = c->n_x;
+  WS(double, b, "rq_b", nx);
+  WS(double, x, "rq_x", nx);
+  WS(double, r, "rq_r", nx);
+  WS(unsigned, cnt, "rs_cnt", 1);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s));
+  std::vector<double> hb(nx);
+  uint64_t st = 0x9e3779b97f4a7c15ull;
+  for (int64_t i = 0; i < nx; ++i) {
+    st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+    hb[i] = (double)(st >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+  CK(cudaMemcpyAsync(b, hb.data(), nx * sizeof(double), cudaMemcpyHostToDevice, s));
+  TRY(precond_apply(c, b, x, s));
+  StencilArgs a = make_stencil(c->op, false);
+  a.X = x; a.ldx = nx; a.Y = r; a.ldy = nx; a.ncols = 1; a.Bres = b; a.ldbres = nx;
+  std::vector<double> res;
+  for (int it = 0; it < 10; ++it) {
+    stencil_kernel<<<dim3(grid1(nx, 256, 1 << 30), 1), 256, 0, s>>>(a);
+    CKL();
+    double nr = 0.0;
+    TRY(lrk_cgs2(c, nullptr, nx, 0, r, (int)nx, nullptr, &nr, s));
+    res.push_back(nr);
+    TRY(precond_apply(c, r, x, s, 1.0));
+  }
+  double q = 1.0;
+  if (res[2] > 0.0 && res[9] > 0.0) q = std::pow(res[9] / res[2], 1.0 / 7.0);
+  else if (res[2] == 0.0 || res[9] == 0.0) q = 0.0;
+  if (!(q < 0.6)) {
+    c->rich_it = -1;
+  } else {
+    // residual after x0 = P^{-1} b is ~ q ||b||; reach 1e-3 * STEP_RTOL with margin
+    const double need = std::log(0.1 * STEP_RTOL) / std::log(std::max(q, 1e-6));
+    c->rich_it = std::max(2, std::min(60, (int)std::ceil(need) + 1));
+  }
+  c->rich_q = q;
+  if (std::getenv("LRK_DEBUG")) {
+    std::fprintf(stderr, "[lrk] step-solve contraction q = %.3e -> %s %d; residuals:", q,
+                 c->rich_it > 0 ? "Richardson sweeps" : "GMRES", c->rich_it);
+    for (double v : res) std::fprintf(stderr, " %.2e", v);
+    std::fprintf(stderr, "\n");
+  }
+  return LRK_OK;
+}
+
 int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, int rb,
                    const int* rb_dev, const double* W2, int64_t ldw2, int adjoint, int p,
                    double eps0, int r_max, SweepOut& o, cudaStream_t s) {
@@ -435,12 +519,35 @@ int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t 
     rbh = std::min(rb, v);
   }
   const int slot = adjoint ? 1 : 0;
-  if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
-  // B~ = S^{-1} B (S^{-T} B for the adjoint), one GMRES solve per column
-  WS(double, Bs, tag + "Bs", nx * (int64_t)std::max(rbh, 1));
+  TRY(rich_setup(c, s));
+  const bool rich = c->rich_it > 0;
+  WS(int, flag, "ph_flag", 1);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
   int it = 0;
-  for (int j = 0; j < rbh; ++j)
-    TRY(gmres_solve(c, B + (int64_t)j * ldb, Bs + (int64_t)j * nx, adjoint, STEP_RTOL, &it, s));
+  auto solve = [&](const double* b, double* x, bool force_gmres) -> int {
+    if (rich && !force_gmres) return rich_solve(c, b, x, adjoint != 0, flag, s);
+    return gmres_solve(c, b, x, adjoint != 0, STEP_RTOL, &it, s);
+  };
+  auto flag_raised = [&](bool& raised) -> int {
+    raised = false;
+    if (!rich) return LRK_OK;
+    int hf = 0;
+    CK(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hf) CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    raised = hf != 0;
+    return LRK_OK;
+  };
+  if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
+  // B~ = S^{-1} B (S^{-T} B for the adjoint), one solve per column
+  WS(double, Bs, tag + "Bs", nx * (int64_t)std::max(rbh, 1));
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int j = 0; j < rbh; ++j)
+      TRY(solve(B + (int64_t)j * ldb, Bs + (int64_t)j * nx, pass == 1));
+    bool raised = false;
+    TRY(flag_raised(raised));
+    if (!raised) break;
+  }
   const int ucap = (r_max >= 0 && r_max < NMAX) ? std::max(r_max, 1) : NMAX;
   const int ncta = pick_ncta(c, nx);
   const int nflush = (nt + p - 1) / p;
@@ -488,28 +595,32 @@ int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t 
   const double* yp = nullptr;
   for (int cs0 = 0; cs0 < nt; cs0 += Tc) {
     const int ce = std::min(nt, cs0 + Tc);
-    for (int j = cs0; j < ce; ++j) {
-      const int k = adjoint ? nt - 1 - j : j;  // time step advanced by processing index j
-      double* yk = Yx + (int64_t)(j - cs0) * nx;
-      if (yp) {
-        TRY(axpby(c, yp, m, nullptr, 0.0, tmp, s));
-        TRY(gmres_solve(c, tmp, yk, adjoint != 0, STEP_RTOL, &it, s));
-      } else {
-        CK(cudaMemsetAsync(yk, 0, nx * sizeof(double), s));
-      }
-      if (rbh > 0) {
-        rank_axpy_kernel<<<grid1(nx, 256, 2048), 256, 0, s>>>(Bs, nx, rbh, W2 + k, ldw2, yk, nx);
-        CKL();
-        ++c->launches;
-      }
-      if (j + 1 < ce) {
+    const double* yp0 = yp;  // y before this chunk (yprev or null), for a GMRES redo
+    for (int pass = 0; pass < 2; ++pass) {
+      yp = yp0;
+      for (int j = cs0; j < ce; ++j) {
+        const int k = adjoint ? nt - 1 - j : j;  // time step advanced by processing index j
+        double* yk = Yx + (int64_t)(j - cs0) * nx;
+        if (yp) {
+          TRY(axpby(c, yp, m, nullptr, 0.0, tmp, s));
+          TRY(solve(tmp, yk, pass == 1));
+        } else {
+          CK(cudaMemsetAsync(yk, 0, nx * sizeof(double), s));
+        }
+        if (rbh > 0) {
+          rank_axpy_kernel<<<grid1(nx, 256, 2048), 256, 0, s>>>(Bs, nx, rbh, W2 + k, ldw2, yk, nx);
+          CKL();
+          ++c->launches;
+        }
         yp = yk;
-      } else {
-        // the chunk buffer is rewritten next: carry y_{last} in yprev
-        CK(cudaMemcpyAsync(yprev, yk, nx * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        yp = yprev;
       }
+      bool raised = false;
+      TRY(flag_raised(raised));
+      if (!raised) break;
     }
+    // the chunk buffer is rewritten next: carry y_{last} in yprev
+    CK(cudaMemcpyAsync(yprev, yp, nx * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    yp = yprev;
     a.flush0 = cs0 / p;
     a.flush1 = std::min(nflush, (ce + p - 1) / p);
     a.r_init = cs0 == 0 ? 0 : -1;
@@ -891,6 +1002,7 @@ int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
   c->op = *op;
   c->n = n;
   c->n_x = nx;
+  c->rich_it = 0;
   c->has_op = true;
   c->has_obs = false;
   return LRK_OK;

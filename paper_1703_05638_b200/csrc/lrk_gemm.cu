@@ -11,8 +11,7 @@
 namespace lrk {
 
 namespace {
-constexpr int TM = 64, TN = 64, TK = 16, GT = 128;
-constexpr int SP = TM + 4;  // padded k-major stride (conflict-free fragments)
+constexpr int TK = 16, GT = 128;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile(
@@ -22,9 +21,16 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 }  // namespace
 
+// TM x TN CTA tile (64x64 or 32x32), 4 warps each owning a (TM/2)x(TN/2)
+// sub-tile of FI x FJ m8n8 fragments.
+template <int TM, int TN>
 __global__ void __launch_bounds__(GT) gemm_kernel(GemmArgs g) {
+  constexpr int SP = TM + 4;  // padded k-major stride (conflict-free fragments)
+  constexpr int SPN = TN + 4;
+  constexpr int FI = TM / 16, FJ = TN / 16;
+  constexpr int LA = TM * TK / GT, LB = TK * TN / GT;  // staged elements per thread
   __shared__ double As[2][TK][SP];
-  __shared__ double Bs[2][TK][SP];
+  __shared__ double Bs[2][TK][SPN];
   int M = g.M;
   if (g.m_dev) { const int md = (*g.m_dev) * g.m_mult; if (md < M) M = md; }
   int batch = g.batch;
@@ -41,35 +47,43 @@ __global__ void __launch_bounds__(GT) gemm_kernel(GemmArgs g) {
   const double* B = g.B + (int64_t)b * g.sB;
   double* C = g.C + (int64_t)b * g.sC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * (TM / 2), wn = (warp & 1) * (TN / 2);
   const int gi = lane >> 2, ti = lane & 3;
 
-  double acc[4][4][2];
+  double acc[FI][FJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < FJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // global -> register staging: A tile 64x16 (8 per thread), B tile 16x64
-  double ra[8], rb[8];
+  // global -> register staging: A tile TMx16, B tile 16xTN
+  double ra[LA], rb[LB];
   auto load_tile = [&](int k0) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * GT;        // 0..1023
-      const int am = e >> 4, ak = e & 15;  // A: row am, col ak
+    for (int q = 0; q < LA; ++q) {
+      const int e = tid + q * GT;
+      const int am = e / TK, ak = e % TK;  // A: row am, col ak
       const int gm = m0 + am, gk = k0 + ak;
       ra[q] = (gm < M && gk < K) ? A[(int64_t)gm * g.lda + gk] : 0.0;
-      const int bk = e >> 6, bn = e & 63;  // B: row bk, col bn
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int e = tid + q * GT;
+      const int bk = e / TN, bn = e % TN;  // B: row bk, col bn
       const int gk2 = k0 + bk, gn = n0 + bn;
       rb[q] = (gk2 < K && gn < N) ? B[(int64_t)gk2 * g.ldb + gn] : 0.0;
     }
   };
   auto store_tile = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < LA; ++q) {
       const int e = tid + q * GT;
-      As[buf][e & 15][e >> 4] = ra[q];
-      Bs[buf][e >> 6][e & 63] = rb[q];
+      As[buf][e % TK][e / TK] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int e = tid + q * GT;
+      Bs[buf][e / TN][e % TN] = rb[q];
     }
   };
   const int nk = (K + TK - 1) / TK;
@@ -81,32 +95,33 @@ __global__ void __launch_bounds__(GT) gemm_kernel(GemmArgs g) {
     if (kt + 1 < nk) load_tile((kt + 1) * TK);
 #pragma unroll
     for (int kk = 0; kk < TK; kk += 4) {
-      double af[4], bf[4];
+      double af[FI], bf[FJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[buf][kk + ti][wm + i * 8 + gi];
+      for (int i = 0; i < FI; ++i) af[i] = As[buf][kk + ti][wm + i * 8 + gi];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kk + ti][wn + j * 8 + gi];
+      for (int j = 0; j < FJ; ++j) bf[j] = Bs[buf][kk + ti][wn + j * 8 + gi];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < FJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     if (kt + 1 < nk) store_tile(buf ^ 1);
     __syncthreads();
   }
   // epilogue
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < FI; ++i) {
     const int row = m0 + wm + i * 8 + gi;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < FJ; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = n0 + wn + j * 8 + 2 * ti + h;
         if (col < N) {
           double* c = C + (int64_t)row * g.ldc + col;
-          const double v = g.alpha * acc[i][j][h];
+          double v = g.alpha * acc[i][j][h];
+          if (g.emul) v *= g.emul[(int64_t)row * g.lde + col];
           *c = (g.beta == 0.0) ? v : v + g.beta * (*c);
         }
       }
@@ -116,8 +131,14 @@ __global__ void __launch_bounds__(GT) gemm_kernel(GemmArgs g) {
 
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
-  dim3 grid((g.N + TN - 1) / TN, (g.M + TM - 1) / TM, g.batch);
-  gemm_kernel<<<grid, GT, 0, s>>>(g);
+  const int64_t tiles64 = (int64_t)((g.N + 63) / 64) * ((g.M + 63) / 64) * g.batch;
+  if (tiles64 >= 2 * 148) {
+    dim3 grid((g.N + 63) / 64, (g.M + 63) / 64, g.batch);
+    gemm_kernel<64, 64><<<grid, GT, 0, s>>>(g);
+  } else {  // under-filled grid (e.g. one 512^2 DST column): 4x more CTAs
+    dim3 grid((g.N + 31) / 32, (g.M + 31) / 32, g.batch);
+    gemm_kernel<32, 32><<<grid, GT, 0, s>>>(g);
+  }
   return cudaGetLastError();
 }
 

@@ -114,6 +114,8 @@ struct GemmArgs {
   int batch_mult;
   const int* m_dev;        // optional: M = min(M, *m_dev * m_mult)
   int m_mult;
+  const double* emul;      // optional epilogue: C = alpha * (A B) .* E + beta * C, E[row*lde + col]
+  int64_t lde;
 };
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s);
 

@@ -37,7 +37,8 @@ __global__ void stencil_kernel(StencilArgs a) {
       }
     }
   }
-  a.Y[i + (int64_t)c * a.ldy] = a.m_scale * (xc + a.tau * lx);
+  const double sx = a.m_scale * (xc + a.tau * lx);
+  a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
 }
 
 // out2[:, c] = shift(W2[:, c]) (forward: down one row; adjoint: up one row)
@@ -79,6 +80,42 @@ __global__ void rank_axpy_kernel(const double* B, int64_t ldb, int rb, const dou
     double acc = y[i];
     for (int j = 0; j < rb; ++j) acc += B[i + (int64_t)j * ldb] * w[(int64_t)j * ldw];
     y[i] = acc;
+  }
+}
+
+// flag |= (||r||^2 > tol2 ||b||^2): device-side convergence check of an
+// iterative step solve (grid-wide; the last block to finish reduces the
+// per-block partials in a fixed order and re-arms the counter).
+__global__ void resid_flag_kernel(const double* r, const double* b, int64_t n, double tol2,
+                                  double* part, unsigned* counter, int* flag) {
+  __shared__ double srr[NWARP], sbb[NWARP];
+  __shared__ bool last;
+  double rr = 0.0, bb = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    rr += r[i] * r[i];
+    bb += b[i] * b[i];
+  }
+  rr = warp_sum(rr);
+  bb = warp_sum(bb);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { srr[w] = rr; sbb[w] = bb; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { a += srr[k]; c += sbb[k]; }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = c;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double a = 0.0, c = 0.0;
+    for (unsigned k = 0; k < gridDim.x; ++k) { a += __ldcg(part + 2 * k); c += __ldcg(part + 2 * k + 1); }
+    if (a > tol2 * c) *flag = 1;
+    *counter = 0;
   }
 }
 

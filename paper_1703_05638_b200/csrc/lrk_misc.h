@@ -15,6 +15,8 @@ struct StencilArgs {
   // (already mirrored for the adjoint); zero entries are skipped uniformly
   double coef[27];
   double m_scale, tau;
+  const double* Bres;     // optional: Y = Bres - S X (residual form)
+  int64_t ldbres;
 };
 
 __global__ void stencil_kernel(StencilArgs a);
@@ -26,6 +28,8 @@ __global__ void prior_scale_kernel(const double* X, int64_t ldx, const double* l
                                    double gamma, double* Y, int64_t ldy);
 __global__ void rank_axpy_kernel(const double* B, int64_t ldb, int rb, const double* w,
                                  int64_t ldw, double* y, int64_t n);
+__global__ void resid_flag_kernel(const double* r, const double* b, int64_t n, double tol2,
+                                  double* part, unsigned* counter, int* flag);
 __global__ void axpby_kernel(const double* x, double a, const double* y, double b, double* out,
                              int64_t n);
 __global__ void mask_time_rows_kernel(double* W2, int64_t ld2, int n_t, int ncols, int every);
