@@ -64,6 +64,7 @@ typedef struct {
  * The step matrix is S = m_scale * (I + tau * L). */
 enum { LRK_OP_HEAT = 0, LRK_OP_CONVDIFF = 1 };
 enum { LRK_STENCIL_FD = 0, LRK_STENCIL_Q1 = 1 };
+enum { LRK_WIND_CONST = 0, LRK_WIND_ROTATING = 1 };
 typedef struct {
   int kind;
   int dim;      /* spatial dimension; 2 or 3 */
@@ -75,6 +76,11 @@ typedef struct {
   double nu;
   double wind[3];
   int stencil;  /* LRK_STENCIL_* (0 = the reference's FD operator) */
+  /* convdiff wind: 0 = constant wind[] (the reference); 1 = wind[] + the
+   * rotating field (2 x2 (1 - x1^2), -2 x1 (1 - x2^2), 0) of configs C3/C5,
+   * upwinded per node by the sign of the local wind (discretize.py:96-104
+   * applied node by node). */
+  int wind_field;
 } lrk_operator_desc;
 
 /* Observation operator (hessian.py:78-156).

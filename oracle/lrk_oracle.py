@@ -34,6 +34,37 @@ FLOOR = 1e-15  # lowrank.py:20-22
 
 
 # ---------------------------------------------------------------- operators
+def rotating_upwind(n_side: int, dim: int, w0=(0.0, 0.0, 0.0)):
+    """Config C3/C5 convection (extension; unpinned by the reference's tests):
+    w(x) = w0 + (2 x2 (1 - x1²), -2 x1 (1 - x2²), 0) upwinded node by node with
+    the rule of discretize.py:96-104 (sign of the local wind picks the
+    one-sided difference).  Returns the n_x × n_x sparse W (x1 fastest)."""
+    n = int(n_side)
+    h = 1.0 / (n + 1)
+    N = n ** dim
+    g = h * (np.arange(n) + 1)
+    i = np.arange(N)
+    ii = [i % n, (i // n) % n, i // (n * n)]
+    x1, x2 = g[ii[0]], g[ii[1]]
+    w = [w0[0] + 2 * x2 * (1 - x1**2), w0[1] - 2 * x1 * (1 - x2**2)]
+    if dim == 3:
+        w.append(np.full(N, float(w0[2])))
+    W = sp.lil_matrix((N, N))
+    strides = [1, n, n * n]
+    for a in range(dim):
+        for q in range(N):
+            wa = w[a][q]
+            if wa > 0:
+                W[q, q] += wa / h
+                if ii[a][q] > 0:
+                    W[q, q - strides[a]] -= wa / h
+            elif wa < 0:
+                W[q, q] -= wa / h
+                if ii[a][q] < n - 1:
+                    W[q, q + strides[a]] += wa / h
+    return sp.csr_matrix(W)
+
+
 def fd_operator(n_side: int, kind: str = "heat", nu: float = 1.0, wind=(0.0, 0.0)):
     """5-point FD -Δ, or nu·(5-point) + first-order upwind (discretize.py:90-127).
 
@@ -59,7 +90,7 @@ def fd_operator(n_side: int, kind: str = "heat", nu: float = 1.0, wind=(0.0, 0.0
 
 
 def config_operator(n_side: int, dim: int = 2, stencil: str = "fd", kind: str = "heat",
-                    nu: float = 1.0, wind=(0.0, 0.0, 0.0)):
+                    nu: float = 1.0, wind=(0.0, 0.0, 0.0), wind_field: str = "const"):
     """Config-extension operators (SURVEY §8(c) "Config features beyond the
     reference", Appendix D2; unpinned by the reference's own tests, pinned here
     by closed-form eigenpairs and by golden runs of the unmodified reference
@@ -68,6 +99,10 @@ def config_operator(n_side: int, dim: int = 2, stencil: str = "fd", kind: str = 
                     M1 = (h/6)tridiag(1,4,1) (Q1 stiffness, lumped mass h²);
       dim 3 "fd":   7-point nu·(-Δ) + first-order upwind per axis.
     Returns (L, h, m_scale) with x1 fastest."""
+    if kind != "heat" and wind_field == "rotating":
+        Ld, h, m = config_operator(n_side, dim, "fd", "heat")
+        w3 = tuple(float(v) for v in (tuple(wind) + (0.0,) * 3)[:3])
+        return sp.csr_matrix(nu * Ld + rotating_upwind(n_side, dim, w3)), h, m
     if dim == 2 and stencil == "fd":
         return fd_operator(n_side, kind, nu, tuple(wind)[:2])
     n = int(n_side)
@@ -285,8 +320,8 @@ class Problem:
 
     def __init__(self, n_side, n_t, mask, beta_noise, gamma_prior, eps0=1e-8, r_max=None,
                  kind="heat", nu=1.0, wind=(0.0, 0.0), T=1.0, compress_every=4, dim=2,
-                 stencil="fd", prior=None, obs_every=1):
-        L, h, m = config_operator(n_side, dim, stencil, kind, nu, wind)
+                 stencil="fd", prior=None, obs_every=1, wind_field="const"):
+        L, h, m = config_operator(n_side, dim, stencil, kind, nu, wind, wind_field)
         self.n_side, self.h, self.m = n_side, h, m
         self.tau = T / n_t
         self.solver = StepSolver(L, m, self.tau, n_t)

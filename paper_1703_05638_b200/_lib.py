@@ -48,7 +48,7 @@ class lrk_operator_desc(Structure):
     _fields_ = [
         ("kind", c_int), ("dim", c_int), ("n_side", c_int), ("n_t", c_int),
         ("h", c_double), ("tau", c_double), ("m_scale", c_double), ("nu", c_double),
-        ("wind", c_double * 3), ("stencil", c_int),
+        ("wind", c_double * 3), ("stencil", c_int), ("wind_field", c_int),
     ]
 
 

@@ -225,7 +225,7 @@ StencilArgs make_stencil(const lrk_operator_desc& op, bool adjoint) {
     cf(0, 0, 0) = 2.0 * op.dim * sc * ih2;
     cf(-1, 0, 0) = cf(1, 0, 0) = cf(0, -1, 0) = cf(0, 1, 0) = -sc * ih2;
     if (op.dim == 3) cf(0, 0, -1) = cf(0, 0, 1) = -sc * ih2;
-    if (op.kind != LRK_OP_HEAT) {
+    if (op.kind != LRK_OP_HEAT && op.wind_field == LRK_WIND_CONST) {
       // first-order upwind per axis by the sign of the wind (discretize.py:96-104)
       for (int ax = 0; ax < op.dim; ++ax) {
         const double w = op.wind[ax];
@@ -239,6 +239,10 @@ StencilArgs make_stencil(const lrk_operator_desc& op, bool adjoint) {
   if (adjoint)
     for (int k = 0; k < 13; ++k) std::swap(a.coef[k], a.coef[26 - k]);
   a.n = op.n_side; a.dim = op.dim; a.m_scale = op.m_scale; a.tau = op.tau;
+  a.wind_field = op.kind != LRK_OP_HEAT ? op.wind_field : 0;
+  a.adjoint = adjoint ? 1 : 0;
+  a.w0[0] = op.wind[0]; a.w0[1] = op.wind[1]; a.w0[2] = op.wind[2];
+  a.h = h;
   return a;
 }
 
@@ -944,6 +948,8 @@ int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
     return fail(c, LRK_ERR_UNSUPPORTED, "dim must be 2 or 3");
   if (op->stencil != LRK_STENCIL_FD && op->stencil != LRK_STENCIL_Q1)
     return fail(c, LRK_ERR_CONFIG, "unknown stencil");
+  if (op->wind_field != LRK_WIND_CONST && op->wind_field != LRK_WIND_ROTATING)
+    return fail(c, LRK_ERR_CONFIG, "unknown wind field");
   if (op->stencil == LRK_STENCIL_Q1 && (op->dim != 2 || op->kind != LRK_OP_HEAT))
     return fail(c, LRK_ERR_UNSUPPORTED, "the Q1-lumped stencil is implemented for 2-D heat");
   if (op->n_side < 2 || op->n_t < 1 || !(op->tau > 0) || !(op->h > 0) || !(op->m_scale > 0))

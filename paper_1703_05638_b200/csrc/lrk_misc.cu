@@ -12,6 +12,45 @@ namespace lrk {
 // discretize.py:90-127 (5-point FD) and their config extensions (Q1-lumped
 // 9-point, 3-D 7-point), generated on the fly (no CSR), zero Dirichlet data.
 // One thread per output entry, coalesced along x1; neighbours come through L1.
+// Local wind at interior node (i1, i2, i3): w0 + (2 x2 (1 - x1^2), -2 x1 (1 - x2^2), 0).
+__device__ __forceinline__ double wind_at(const StencilArgs& a, int ax, int i1, int i2) {
+  const double x1 = a.h * (i1 + 1), x2 = a.h * (i2 + 1);
+  if (ax == 0) return a.w0[0] + 2.0 * x2 * (1.0 - x1 * x1);
+  if (ax == 1) return a.w0[1] - 2.0 * x1 * (1.0 - x2 * x2);
+  return a.w0[2];
+}
+
+// Per-node first-order upwind (row i of W, or of W^T for the adjoint):
+// row q: diag += |w_a(q)|/h; entry (q, q - e_a) = -w_a(q)/h if w_a(q) > 0,
+// entry (q, q + e_a) = +w_a(q)/h if w_a(q) < 0.
+__device__ __forceinline__ double var_upwind(const StencilArgs& a, const double* x, int64_t i,
+                                             int i1, int i2, int i3, int64_t plane) {
+  const int n = a.n;
+  const double ih = 1.0 / a.h;
+  double acc = 0.0;
+  const int idx[3] = {i1, i2, i3};
+  const int64_t stride[3] = {1, n, plane};
+  for (int ax = 0; ax < a.dim; ++ax) {
+    const double w = wind_at(a, ax, i1, i2);
+    acc += fabs(w) * ih * x[i];
+    if (!a.adjoint) {
+      if (w > 0.0 && idx[ax] > 0) acc -= w * ih * x[i - stride[ax]];
+      if (w < 0.0 && idx[ax] < n - 1) acc += w * ih * x[i + stride[ax]];
+    } else {
+      // column i of W: rows i + e_a (their lower neighbour is i) and i - e_a
+      if (idx[ax] < n - 1) {
+        const double wp = wind_at(a, ax, i1 + (ax == 0), i2 + (ax == 1));
+        if (wp > 0.0) acc -= wp * ih * x[i + stride[ax]];
+      }
+      if (idx[ax] > 0) {
+        const double wm = wind_at(a, ax, i1 - (ax == 0), i2 - (ax == 1));
+        if (wm < 0.0) acc += wm * ih * x[i - stride[ax]];
+      }
+    }
+  }
+  return acc;
+}
+
 __global__ void stencil_kernel(StencilArgs a) {
   const int c = blockIdx.y;
   const int n = a.n;
@@ -37,6 +76,7 @@ __global__ void stencil_kernel(StencilArgs a) {
       }
     }
   }
+  if (a.wind_field) lx += var_upwind(a, x, i, i1, i2, i3, plane);
   const double sx = a.m_scale * (xc + a.tau * lx);
   a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
 }

@@ -17,6 +17,12 @@ struct StencilArgs {
   double m_scale, tau;
   const double* Bres;     // optional: Y = Bres - S X (residual form)
   int64_t ldbres;
+  // variable wind (wind_field = 1): per-node upwind of w = w0 + rotating field,
+  // added on top of coef (which then holds the diffusion part only)
+  int wind_field;
+  int adjoint;
+  double w0[3];
+  double h;
 };
 
 __global__ void stencil_kernel(StencilArgs a);

@@ -65,6 +65,7 @@ class SpatialOperator:
     nu: float = 1.0
     wind: tuple = (0.0, 0.0)
     stencil: str = "fd"   # "fd" (reference 5-point / 3-D 7-point) or "q1" (Q1-lumped 9-point)
+    wind_field: str = "const"  # "const" (reference) or "rotating" (configs C3/C5)
 
     @property
     def m_scale(self) -> float:
@@ -168,9 +169,50 @@ def assemble_heat(grid: Grid, stencil: str = "fd") -> SpatialOperator:
     return SpatialOperator(kind="heat", grid=grid, L=_assemble(grid, stencil_coefficients("heat", grid.h)))
 
 
-def assemble_convdiff(grid: Grid, nu: float, wind) -> SpatialOperator:
+def rotating_wind(grid: Grid, w0=(0.0, 0.0, 0.0)):
+    """Per-node wind of configs C3/C5: w0 + (2 x2 (1 - x1²), -2 x1 (1 - x2²), 0)."""
+    c = grid.coords()
+    x1, x2 = c[0], c[1]
+    w0 = tuple(float(v) for v in (tuple(w0) + (0.0,) * 3)[:3])
+    W = [w0[0] + 2 * x2 * (1 - x1**2), w0[1] - 2 * x1 * (1 - x2**2)]
+    if grid.d == 3:
+        W.append(np.full(grid.n_x, w0[2]))
+    return W
+
+
+def _upwind_field(grid: Grid, W) -> sp.csr_matrix:
+    """First-order upwind by the sign of the LOCAL wind (discretize.py:96-104
+    applied node by node): row q gets |w_a(q)|/h on the diagonal and
+    -|w_a(q)|/h on its upstream neighbour along each axis."""
+    n, N, h = grid.n_side, grid.n_x, grid.h
+    idx = np.arange(N)
+    comp = [idx % n, (idx // n) % n, idx // (n * n)]
+    stride = [1, n, n * n]
+    rows, cols, vals = [idx], [idx], [np.sum([np.abs(w) for w in W], axis=0) / h]
+    for a, w in enumerate(W):
+        m = (w > 0) & (comp[a] > 0)
+        rows.append(idx[m]); cols.append(idx[m] - stride[a]); vals.append(-w[m] / h)
+        m = (w < 0) & (comp[a] < n - 1)
+        rows.append(idx[m]); cols.append(idx[m] + stride[a]); vals.append(w[m] / h)
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(N, N))
+
+
+def assemble_convdiff(grid: Grid, nu: float, wind, field: str = "const") -> SpatialOperator:
+    """-nu Δ + w·∇ with first-order upwind (discretize.py:115-127).  field
+    "rotating" (config extension) adds the C3/C5 rotating field to `wind` and
+    upwinds node by node."""
     if nu <= 0:
         raise InvalidConfigError(f"viscosity nu must be positive, got {nu}")
+    if field not in ("const", "rotating"):
+        raise InvalidConfigError(f"unknown wind field {field!r}")
+    if field == "rotating":
+        w3 = tuple(float(x) for x in (tuple(wind) + (0.0,) * 3)[:3])
+        lap = _assemble_3d(grid, float(nu)) if grid.d == 3 else \
+            float(nu) * _assemble(grid, stencil_coefficients("heat", grid.h))
+        L = sp.csr_matrix(lap + _upwind_field(grid, rotating_wind(grid, w3)))
+        return SpatialOperator(kind="convdiff", grid=grid, L=L, nu=float(nu),
+                               wind=w3 if grid.d == 3 else w3[:2], wind_field="rotating")
     if grid.d == 3:
         w3 = tuple(float(x) for x in (tuple(wind) + (0.0,) * 3)[:3])
         return SpatialOperator(kind="convdiff", grid=grid, L=_assemble_3d(grid, float(nu), w3),

@@ -206,14 +206,27 @@ def main():
         return sp.csr_matrix(sp.kron(I, sp.kron(I, A)) + sp.kron(I, sp.kron(A, I))
                              + sp.kron(A, sp.kron(I, I)))
 
+    def rot_matrix(n, h, dim, nu, w0):
+        # rotating-field convection diffusion; the assembly is the oracle's own
+        # (test infrastructure): this fixture pins the reference pipeline run on it
+        sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+        from oracle import lrk_oracle as O
+        return O.config_operator(n, dim, "fd", "convdiff", nu, w0, "rotating")[0]
+
+    s3 = 1.0 / math.sqrt(3.0)
     for name, (n_side, dim, stencil, n_t, sens, every, delta, gp, sigma, rmax, seed) in {
         "cfg_q1": (15, 2, "q1", 16, 5, 1, 1.0, 0.05, 0.01, None, 11),
         "cfg_q1b": (24, 2, "q1", 12, 8, 1, 1.0, 0.1, 0.01, 12, 12),
         "cfg_3d": (7, 3, "fd", 12, 3, 4, 1.0, 0.02, 0.005, None, 13),
+        "cfg_rot": (14, 2, ("rot", 0.05, (0.0, 0.0, 0.0)), 12, 4, 1, 1.0, 0.05, 0.01, None, 14),
+        "cfg_rot3": (6, 3, ("rot", 0.02, (s3, s3, s3)), 8, 3, 1, 1.0, 0.02, 0.005, None, 15),
     }.items():
         h = 1.0 / (n_side + 1)
         m = h ** dim
-        L = q1_matrix(n_side, h) if stencil == "q1" else fd3_matrix(n_side, h)
+        if isinstance(stencil, tuple):
+            L = rot_matrix(n_side, h, dim, stencil[1], stencil[2])
+        else:
+            L = q1_matrix(n_side, h) if stencil == "q1" else fd3_matrix(n_side, h)
         n_x = n_side ** dim
         grid = SimpleNamespace(n_x=n_x, m_scale=m, n_side=n_side, h=h, d=dim)
         spatial = SimpleNamespace(grid=grid, L=L, m_scale=m, kind="heat")
@@ -231,7 +244,9 @@ def main():
         beta_noise = 1.0 / (sigma**2 * tau * m)  # w = 1/sigma^2
         cov = hs.CovarianceSpec(beta_noise=beta_noise, beta_prior=1.0, gamma_prior=1.0)
         pol = lp.TruncationPolicy(1e-8, rmax)
-        P = spla.splu((delta * sp.identity(n_x) + gp * L).tocsc())
+        Lprior = L if not isinstance(stencil, tuple) else \
+            (fd3_matrix(n_side, h) if dim == 3 else lp.assemble_heat(lp.build_grid(n_side)).L)
+        P = spla.splu((delta * sp.identity(n_x) + gp * Lprior).tocsc())
         inj = InitInjection(K)
 
         def apply(v):
@@ -250,8 +265,10 @@ def main():
         V = np.random.default_rng(seed).standard_normal((n_x, 2))
         V /= np.linalg.norm(V, axis=0)
         res = [apply(V[:, j]) for j in range(2)]
-        out[f"{name}_meta"] = np.array([n_side, dim, 1 if stencil == "q1" else 0, n_t, every,
-                                        delta, gp, beta_noise, -1 if rmax is None else rmax])
+        kind_code = 2 if isinstance(stencil, tuple) else (1 if stencil == "q1" else 0)
+        nu_w = stencil[1:] if isinstance(stencil, tuple) else (0.0, (0.0, 0.0, 0.0))
+        out[f"{name}_meta"] = np.array([n_side, dim, kind_code, n_t, every, delta, gp, beta_noise,
+                                        -1 if rmax is None else rmax, nu_w[0], *nu_w[1]])
         out[f"{name}_mask"] = mask
         out[f"{name}_V"] = V
         out[f"{name}_O"] = np.column_stack([r[0] for r in res])

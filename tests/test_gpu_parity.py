@@ -315,9 +315,12 @@ def test_diagonal_operator_arnoldi_numpy_callable():
 
 # ------------------------------------------------- config extensions
 def _cfg_ctx(golden, name):
-    n_side, dim, q1, n_t, every, delta, gp, bn, rmax = golden[f"{name}_meta"]
+    n_side, dim, code, n_t, every, delta, gp, bn, rmax, nu, w0, w1, w2 = golden[f"{name}_meta"]
     grid = lp.build_grid(int(n_side), int(dim))
-    op = lp.assemble_heat(grid, "q1" if q1 else "fd")
+    if code == 2:
+        op = lp.assemble_convdiff(grid, nu, (w0, w1, w2), field="rotating")
+    else:
+        op = lp.assemble_heat(grid, "q1" if code == 1 else "fd")
     K = lp.SpaceTimeOperator(op, lp.build_time_grid(int(n_t)))
     cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=float(delta), prior_gamma=float(gp))
     layout = lp.SensorLayout(patches=(), mask=golden[f"{name}_mask"].astype(bool),
@@ -326,7 +329,7 @@ def _cfg_ctx(golden, name):
     return lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=pol)
 
 
-@pytest.mark.parametrize("name", ["cfg_q1", "cfg_q1b", "cfg_3d"])
+@pytest.mark.parametrize("name", ["cfg_q1", "cfg_q1b", "cfg_3d", "cfg_rot", "cfg_rot3"])
 def test_config_hessian_ic_vs_reference(golden, name):
     """Q1-lumped / 3-D 7-point operators, (δI+γL)⁻¹ prior and time-subsampled
     sensors against the reference pipeline run on the same matrices."""
@@ -342,7 +345,10 @@ def test_config_stencil_apply_is_the_dense_operator():
     """Matrix-free Q1 9-point and 3-D 7-point SpMM (+ upwind) vs the assembled S."""
     rng = np.random.default_rng(21)
     for op in (lp.assemble_heat(lp.build_grid(7), "q1"), lp.assemble_heat(lp.build_grid(5, 3)),
-               lp.assemble_convdiff(lp.build_grid(5, 3), 0.02, (0.5, -1.0, 0.25))):
+               lp.assemble_convdiff(lp.build_grid(5, 3), 0.02, (0.5, -1.0, 0.25)),
+               lp.assemble_convdiff(lp.build_grid(8), 0.05, (0.0, 0.0), field="rotating"),
+               lp.assemble_convdiff(lp.build_grid(5, 3), 0.02, (0.577, 0.577, 0.577),
+                                    field="rotating")):
         K = lp.SpaceTimeOperator(op, lp.build_time_grid(4))
         Y = lp.LowRankMat(rng.standard_normal((op.grid.n_x, 2)), rng.standard_normal((4, 2)))
         Yd = _dense(Y)
@@ -472,3 +478,29 @@ def test_convdiff_hessian_mid_size_vs_oracle_and_adjointness():
     assert ctx.rank_trace[-1] == r
     Hu = ctx.apply(u)
     assert abs(u @ Hv - Hu @ v) <= 1e-7 * abs(u @ Hv)
+
+
+def test_rotating_wind_step_solve_and_c3_shape_hessian():
+    """C3 physics (rotating field, ν = 1/20) at reduced size: step solves and
+    their transposes vs SuperLU, and the IC Hessian vs the oracle."""
+    n_side, n_t, nu = 48, 48, 0.05
+    grid = lp.build_grid(n_side)
+    op = lp.assemble_convdiff(grid, nu, (0.0, 0.0), field="rotating")
+    K = lp.SpaceTimeOperator(op, lp.build_time_grid(n_t))
+    solver = O.StepSolver(op.L, grid.m_scale, 1.0 / n_t, n_t)
+    B = np.random.default_rng(41).standard_normal((grid.n_x, 2))
+    for adj in (False, True):
+        ref = solver.solve(B, adjoint=adj)
+        assert np.linalg.norm(K.solve_step(B, adjoint=adj) - ref) <= 1e-11 * np.linalg.norm(ref)
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    layout = lp.make_sensor_subgrid(grid, 6)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                            pol=lp.TruncationPolicy(1e-8, 48))
+    P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, 48, kind="convdiff", nu=nu,
+                  wind=(0.0, 0.0), wind_field="rotating", prior=(1.0, 0.05))
+    v = np.random.default_rng(42).standard_normal(grid.n_x)
+    ref, r = O.hessian_ic(P, v)
+    out = ctx.apply(v)
+    assert np.linalg.norm(out - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert ctx.rank_trace[-1] == r

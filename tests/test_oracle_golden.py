@@ -82,14 +82,15 @@ def test_hessian_ic_matches_reference(golden, name):
     assert ranks == golden[f"{name}_ranks"].tolist()
 
 
-CFG = ["cfg_q1", "cfg_q1b", "cfg_3d"]
+CFG = ["cfg_q1", "cfg_q1b", "cfg_3d", "cfg_rot", "cfg_rot3"]
 
 
 def cfg_problem(golden, name):
-    n_side, dim, q1, n_t, every, delta, gp, bn, rmax = golden[f"{name}_meta"]
+    n_side, dim, code, n_t, every, delta, gp, bn, rmax, nu, w0, w1, w2 = golden[f"{name}_meta"]
+    extra = dict(kind="convdiff", nu=nu, wind=(w0, w1, w2), wind_field="rotating") if code == 2 else {}
     return O.Problem(int(n_side), int(n_t), golden[f"{name}_mask"], bn, 1.0, 1e-8, _rmax(rmax),
-                     dim=int(dim), stencil="q1" if q1 else "fd", prior=(delta, gp),
-                     obs_every=int(every))
+                     dim=int(dim), stencil="q1" if code == 1 else "fd", prior=(delta, gp),
+                     obs_every=int(every), **extra)
 
 
 @pytest.mark.parametrize("name", CFG)
