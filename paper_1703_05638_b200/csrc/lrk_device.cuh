@@ -352,25 +352,28 @@ __device__ __forceinline__ void small_pivoted_qr(double* A, int q, double* X, in
 }
 
 // _rank_cut (lowrank.py:98-111) on descending s[0..n); single thread.
+// tail[r] = sqrt(sum_{i>=r} s_i^2) accumulated from the end (as np.cumsum on
+// the reversed array); keep = smallest r with tail[r] <= eps0*tail[0].  Two
+// backward passes with the same summation order (no local-memory array):
+// the first gives tail[0], the second walks the suffix {r : tail[r] <= thr}.
 __device__ __forceinline__ int rank_cut_dev(const double* s, int n, double eps0, int r_max) {
   if (n == 0 || !(s[0] > 0.0)) return 0;
   const double floor_v = NOISE_FLOOR * s[0];
-  // tail[r] = sqrt(sum_{i>=r} s_i^2) accumulated from the end (as np.cumsum on
-  // the reversed array); keep = smallest r with tail[r] <= eps0*tail[0].
-  double tail[NMAX + 1];
   double acc = 0.0;
   int nnz = 0;
-  tail[n] = 0.0;
+#pragma unroll 8
   for (int i = n - 1; i >= 0; --i) {
-    double si = s[i] < floor_v ? 0.0 : s[i];
-    if (si != 0.0) ++nnz;
+    const double si = s[i] < floor_v ? 0.0 : s[i];
+    nnz += si != 0.0;
     acc += si * si;
-    tail[i] = sqrt(acc);
   }
-  const double thr = eps0 * tail[0];
-  int keep = n;  // searchsorted(-tail, -thr, 'left') over indices 0..n-1
-  for (int i = 0; i < n; ++i) {
-    if (!(tail[i] > thr)) { keep = i; break; }
+  const double thr = eps0 * sqrt(acc);
+  int keep = 0;  // searchsorted(-tail, -thr, 'left') over indices 0..n-1
+  acc = 0.0;
+  for (int i = n - 1; i >= 0; --i) {
+    const double si = s[i] < floor_v ? 0.0 : s[i];
+    acc += si * si;
+    if (sqrt(acc) > thr) { keep = i + 1; break; }
   }
   if (keep > nnz) keep = nnz;
   if (r_max >= 0 && keep > r_max) keep = r_max;

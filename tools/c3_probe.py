@@ -9,7 +9,8 @@ import paper_1703_05638_b200 as lp
 n_side = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 n_t = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 grid = lp.build_grid(n_side)
-K = lp.SpaceTimeOperator(lp.assemble_convdiff(grid, 0.05, (1.0, -0.5)), lp.build_time_grid(n_t))
+field = sys.argv[3] if len(sys.argv) > 3 else "rotating"
+K = lp.SpaceTimeOperator(lp.assemble_convdiff(grid, 0.05, (0.0, 0.0) if field == "rotating" else (1.0, -0.5), field=field), lp.build_time_grid(n_t))
 bn = 1.0 / (0.01 ** 2 * K.time.tau * grid.m_scale)
 cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
 layout = lp.make_sensor_subgrid(grid, min(64, n_side // 2))
