@@ -193,6 +193,12 @@ int64_t lrk_launch_count(const lrk_ctx* ctx);
 /* Instrumentation for the roofline: when enabled, every sweep launch is
  * bracketed by CUDA events on its stream and its algorithmic bytes (DESIGN.md
  * §Roofline) are accumulated once the apply's ranks are known. */
+/* Run every subsequent sweep of this context as nshard n_x shards (the
+ * multi-GPU decomposition of SURVEY §8(e): global CTA rows, partials read
+ * through a per-shard table, one shared barrier) emulated as nshard groups of
+ * ONE cooperative launch on this device.  Results are bit-identical to the
+ * unsharded sweep when the CTA count divides evenly; used by the tests. */
+int lrk_set_emulated_shards(lrk_ctx* ctx, int nshard);
 int lrk_profile_enable(lrk_ctx* ctx, int enable);
 int lrk_profile_read(lrk_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,
                      double* sweep_alg_bytes, int reset);

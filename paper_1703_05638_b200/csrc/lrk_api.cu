@@ -44,6 +44,7 @@ struct lrk_ctx {
   double* dE0 = nullptr;      // n_t: e_0
   double* dInvLam = nullptr;  // n_x: 1/lambda (steady Poisson solve)
   double* dLam = nullptr;     // n_x: lambda (config prior (delta + gamma lambda)^{-1})
+  int emu_shards = 1;         // sweeps as G emulated n_x shards (one launch, tests)
   int rich_it = 0;            // physical step solves: Richardson sweeps (0 unknown, -1 GMRES)
   double rich_q = 1.0;        // measured contraction of I - P^{-1} S
   // observation
@@ -285,6 +286,11 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   WS(double, ybuf, "sw_ybuf", nx * (int64_t)p);
   WS(double, qbuf, "sw_qbuf", nx * (int64_t)p);
   WS(double, yprev, "sw_yprev", nx);
+  // emulated n_x shards (lrk_set_emulated_shards): G groups of one launch
+  // acting as G GPUs of a sharded sweep, ncta/G CTAs each
+  int G = std::max(1, std::min(c->emu_shards, SHARD_MAX));
+  if (ncta % G != 0 || ncta / G < 1) G = 1;
+  const int ncg = ncta / G;
   const int64_t pst = sweep_part_stride();
   WS(double, part, "sw_part", 3 * (int64_t)ncta * pst);
   const int64_t sst = sweep_scratch_stride(ncta);
@@ -293,6 +299,8 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   SweepBatch batch{};
   batch.ngroups = 1;
   SweepArgs& a = batch.g[0];
+  a.nshard = 1; a.shard = 0; a.sys_fence = 0;
+  a.spart[0] = part; a.gbar = bar;
   a.n_x = nx; a.n_t = nt; a.adjoint = adjoint; a.p = p; a.r_max = r_max; a.eps0 = eps0;
   a.theta = c->dTheta; a.rowscale = c->dThetaM;
   a.B = B; a.ldb = ldb; a.rb = rb; a.rb_dev = rb_dev;
@@ -310,6 +318,34 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   a.dbg = std::getenv("LRK_DEBUG") ? dbg : nullptr;
   o.dbg = dbg;
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
+  if (G > 1) {
+    // shard g: its own replicated time factor, sigma/info/trace and scratch;
+    // the n_x-row arrays are shared (disjoint rows), partials in one table
+    WS(double, Vg, tag + "Vsh", 2 * (int64_t)G * nt * ucap);
+    WS(double, sg, tag + "sigsh", (int64_t)G * NMAX);
+    WS(int, ig, tag + "infosh", 8 * G);
+    WS(int, tg, tag + "tracesh", (int64_t)G * (nflush + 1));
+    CK(cudaMemsetAsync(ig, 0, 8 * G * sizeof(int), s));
+    a.ncta = ncg;
+    a.nshard = G;
+    a.scratch_stride = sst;
+    sweep_plan(a, nx, ncg, ucap, p, (size_t)c->smem_optin, G);
+    a.ftz = std::getenv("LRK_FTZ") ? std::atof(std::getenv("LRK_FTZ")) : 0.0;
+    for (int g = 0; g < G; ++g) a.spart[g] = part + (int64_t)g * 3 * ncg * pst;
+    for (int g = 1; g < G; ++g) {
+      SweepArgs& b = batch.g[g];
+      b = a;
+      b.shard = g;
+      b.V0 = Vg + (int64_t)(2 * g) * nt * ucap;
+      b.V1 = Vg + (int64_t)(2 * g + 1) * nt * ucap;
+      b.sigma = sg + (int64_t)g * NMAX;
+      b.info = ig + 8 * g;
+      b.trace = tg + (int64_t)g * (nflush + 1);
+      b.scratch = scratch + (int64_t)g * ncg * sst;
+      b.dbg = nullptr;
+    }
+    batch.ngroups = G;
+  }
   const int slot = adjoint ? 1 : 0;
   if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
   CK(launch_sweep(batch, s));
@@ -589,6 +625,8 @@ int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t 
   a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
   a.bar = bar; a.ncta = ncta;
   a.yext = Yx; a.ldyext = nx;
+  a.nshard = 1; a.shard = 0; a.sys_fence = 0;
+  a.spart[0] = part; a.gbar = bar;
   sweep_plan(a, nx, ncta, ucap, p, (size_t)c->smem_optin);
   a.ftz = 0.0;
   WS(long long, dbg, tag + "dbg", 20);
@@ -908,6 +946,13 @@ void lrk_ctx_destroy(lrk_ctx* c) {
 const char* lrk_last_error(const lrk_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int64_t lrk_launch_count(const lrk_ctx* c) { return c ? c->launches : 0; }
+
+int lrk_set_emulated_shards(lrk_ctx* c, int nshard) {
+  if (!c) return LRK_ERR_CONFIG;
+  if (nshard < 1 || nshard > SHARD_MAX) return fail(c, LRK_ERR_CONFIG, "nshard must lie in [1, 8]");
+  c->emu_shards = nshard;
+  return LRK_OK;
+}
 
 int lrk_profile_enable(lrk_ctx* c, int enable) {
   if (!c) return LRK_ERR_CONFIG;

@@ -24,24 +24,38 @@ constexpr double NOISE_FLOOR = 1e-15;   // lowrank.py:20-22
 // ------------------------------------------------------------------ barrier
 // Sense-free generation barrier for the `ncta` CTAs of one group.
 // bar[0] = arrival count, bar[1] = generation.
-__device__ __forceinline__ void group_barrier(unsigned* bar, int ncta) {
+__device__ __forceinline__ void group_barrier(unsigned* bar, int ncta, bool sys = false) {
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* vgen = bar + 1;
     unsigned gen = *vgen;
-    __threadfence();
+    if (sys) __threadfence_system(); else __threadfence();
     unsigned arrived = atomicAdd(bar, 1u);
     if (arrived == (unsigned)ncta - 1u) {
       atomicExch(bar, 0u);
-      __threadfence();
+      if (sys) __threadfence_system(); else __threadfence();
       atomicAdd(bar + 1, 1u);
     } else {
       while (*vgen == gen) { __nanosleep(20); }
     }
-    __threadfence();
+    if (sys) __threadfence_system(); else __threadfence();
   }
   __syncthreads();
 }
+
+// Per-CTA partial buffers of a (possibly sharded) sweep: region k (0..2) of
+// global CTA c lives at p[c / ncta] + (k * ncta + c % ncta) * stride.
+struct PartTab {
+  double* const* p;
+  int ncta;        // CTAs per shard
+  int nshard;
+  int64_t stride;
+  __device__ __forceinline__ const double* at(int k, int c) const {
+    if (nshard <= 1) return p[0] + ((int64_t)k * ncta + c) * stride;
+    const int s = c / ncta, l = c - s * ncta;
+    return p[s] + ((int64_t)k * ncta + l) * stride;
+  }
+};
 
 // ------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
@@ -122,6 +136,45 @@ __device__ __forceinline__ void reduce_partials(const double* part, int64_t stri
     for (int o = tid; o < len; o += NT) {
       double acc = 0.0;
       for (int c = 0; c < ncta; ++c) acc += __ldcg(part + (int64_t)c * stride + o);
+      out[o] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// Same reduction over the partials of every CTA of a sharded sweep (fixed
+// order over global CTA ids, so every CTA of every shard gets identical sums).
+__device__ __forceinline__ void reduce_partials(const PartTab& t, int k, int ncta_all, int len,
+                                                double* out) {
+  if (t.nshard <= 1) {
+    reduce_partials(t.at(k, 0), t.stride, ncta_all, len, out);
+    return;
+  }
+  int lp = 1;
+  while (lp < 32 && lp * 2 * len <= NT) lp *= 2;
+  const int tid = threadIdx.x;
+  if (lp > 1) {
+    const int o = tid / lp, sub = tid % lp;
+    double acc = 0.0;
+    if (o < len) {
+      constexpr int B = 16;
+      for (int c0 = sub; c0 < ncta_all; c0 += B * lp) {
+        double v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          const int c = c0 + u * lp;
+          v[u] = (c < ncta_all) ? __ldcg(t.at(k, c) + o) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) acc += v[u];
+      }
+    }
+    for (int m = lp >> 1; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (o < len && sub == 0) out[o] = acc;
+  } else {
+    for (int o = tid; o < len; o += NT) {
+      double acc = 0.0;
+      for (int c = 0; c < ncta_all; ++c) acc += __ldcg(t.at(k, c) + o);
       out[o] = acc;
     }
   }

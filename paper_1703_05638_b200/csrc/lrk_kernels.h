@@ -7,6 +7,8 @@
 namespace lrk {
 
 // One low-rank sweep (forward.py:133-188) in the operator's eigenbasis.
+constexpr int SHARD_MAX = 8;
+
 struct SweepArgs {
   int64_t n_x;
   int n_t;
@@ -41,6 +43,15 @@ struct SweepArgs {
   // when yext != NULL the buffered columns are read from yext (column j = the
   // j-th step processed by this launch) instead of the spectral recurrence.
   const double* yext; int64_t ldyext;
+  // n_x sharding: nshard groups (one per GPU, or emulated as
+  // groups of one launch) form ONE logical sweep; global CTA = shard*ncta + cta
+  // owns rows row_range(n_x, gcta, nshard*ncta); partials of shard s live at
+  // spart[s] (peer memory across GPUs), all CTAs meet at the shared counter
+  // gbar; sys_fence selects system-scope fences (peer GPUs).  nshard <= 1:
+  // spart[0] = part, gbar = bar.
+  int nshard, shard, sys_fence;
+  double* spart[SHARD_MAX];
+  unsigned* gbar;
   // chunked execution: flushes [flush0, flush1) of the full schedule, resuming
   // from a pane of rank r_init held in U0 / V0 / sigma (r_init < 0: the rank
   // the previous chunk left in info[0]; every chunk must contain a flush)
@@ -56,7 +67,8 @@ struct SweepArgs {
 };
 
 // Shared-memory plan for a sweep over n_x rows with ncta CTAs per group.
-void sweep_plan(SweepArgs& a, int64_t n_x, int ncta, int ucap, int p, size_t smem_limit);
+void sweep_plan(SweepArgs& a, int64_t n_x, int ncta, int ucap, int p, size_t smem_limit,
+                int nshard = 1);
 
 // Independent sweeps launched together, one group of ncta CTAs each (passed
 // by value as a __grid_constant__ kernel parameter: no host->device copy).

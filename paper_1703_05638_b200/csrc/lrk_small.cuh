@@ -603,8 +603,8 @@ __device__ __forceinline__ void warp_apply_hh_regs(const double (&x)[ROWS][Q], i
 // Q (= Q_w * (rows of Q_top)) into Qout (both pc x pc row-major, shared).
 // Returns the owner warp.  Requires cpw*Q <= 32*ROWS and NWARP*Q <= 32.
 template <int Q, int ROWS>
-__device__ __forceinline__ int warp_stack_tsqr(const double* __restrict__ part, int64_t pstride,
-                                               int ncta, int pc, int me, double* __restrict__ sRw,
+__device__ __forceinline__ int warp_stack_tsqr(const PartTab& tab, int ncta, int pc, int me,
+                                               double* __restrict__ sRw,
                                                double* __restrict__ Rout,
                                                double* __restrict__ Qout) {
   static_assert(NWARP * Q <= 32, "top level must fit one warp");
@@ -620,7 +620,7 @@ __device__ __forceinline__ int warp_stack_tsqr(const double* __restrict__ part, 
   for (int k = 0; k < ROWS; ++k) {
     const int i = lane + 32 * k;
     const int o = i / pc, lr = i - o * pc;
-    const double* src = part + (int64_t)(b0 + o) * pstride + lr * pc;
+    const double* src = (i < rows) ? tab.at(2, b0 + o) + lr * pc : nullptr;
 #pragma unroll
     for (int c = 0; c < Q; ++c) x[k][c] = (i < rows && c < pc) ? __ldcg(src + c) : 0.0;
   }

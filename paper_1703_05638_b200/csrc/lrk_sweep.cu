@@ -123,11 +123,13 @@ __device__ __forceinline__ void update_time_rows(double* __restrict__ V, int64_t
 }
 }  // namespace
 
-void sweep_plan(SweepArgs& a, int64_t n_x, int ncta, int ucap, int p, size_t smem_limit) {
-  const int64_t mloc = (n_x + ncta - 1) / ncta;
+void sweep_plan(SweepArgs& a, int64_t n_x, int ncta, int ucap, int p, size_t smem_limit,
+                int nshard) {
+  const int nall = ncta * (nshard > 1 ? nshard : 1);  // CTAs of the logical sweep
+  const int64_t mloc = (n_x + nall - 1) / nall;
   const int mp = (int)(mloc | 1);
   Small sm(ucap, p);
-  const int stack = 2 * ncta * p * p;
+  const int stack = 2 * nall * p * p;
   const int64_t limit = (int64_t)(smem_limit / sizeof(double)) - 64;
   int scr = 0;
   int stack_smem = 0;
@@ -170,6 +172,12 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
   const SweepArgs& a = batch.g[blockIdx.x / ncta];
   const int cta = blockIdx.x % ncta;
   const int tid = threadIdx.x, warp = tid >> 5;
+  // sharding: this CTA's place in the logical sweep (SweepArgs::nshard)
+  const int nsh = a.nshard > 1 ? a.nshard : 1;
+  const int gcta = (nsh > 1 ? a.shard : 0) * ncta + cta;
+  const int ncta_all = nsh * ncta;
+  const PartTab tab{a.spart, ncta, nsh, a.pstride};
+  const bool sysf = a.sys_fence != 0;
 
   const int64_t n_x = a.n_x;
   const int n_t = a.n_t;
@@ -177,8 +185,8 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
   const int cap = a.ucap;
   const int rb = a.rb_dev ? min(a.rb, *a.rb_dev) : a.rb;
   int64_t r0, r1, t0, t1;
-  row_range(n_x, cta, ncta, r0, r1);
-  row_range(n_t, cta, ncta, t0, t1);
+  row_range(n_x, gcta, ncta_all, r0, r1);
+  row_range(n_t, cta, ncta, t0, t1);  // the time factor is replicated per shard
   const int m_loc = (int)(r1 - r0);
 
   // ---- storage: resident shared-memory blocks or global rows.  RES is a
@@ -236,9 +244,10 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
   int* iFlag = iPiv + PMAX;
 
   double* gscr = a.scratch + (int64_t)cta * a.scratch_stride;  // global per-CTA scratch
-  double* part1 = a.part;
-  double* part2 = a.part + (int64_t)ncta * a.pstride;
-  double* part3 = a.part + 2 * (int64_t)ncta * a.pstride;
+  // this CTA's own partial slots (regions 0..2 of its shard's buffer)
+  double* part1 = a.spart[nsh > 1 ? a.shard : 0] + (int64_t)cta * a.pstride;
+  double* part2 = part1 + (int64_t)ncta * a.pstride;
+  double* part3 = part2 + (int64_t)ncta * a.pstride;
   __syncthreads();
 
   const bool timing = a.dbg != nullptr && cta == 0 && tid == 0;
@@ -319,12 +328,12 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       if (tid < pc) sPart[r * pc + tid] = sTmp[tid];
     }
     __syncthreads();
-    for (int i = tid; i < r * pc + pc; i += NT) part1[(int64_t)cta * a.pstride + i] = sPart[i];
+    for (int i = tid; i < r * pc + pc; i += NT) part1[i] = sPart[i];
     LRK_TSTAMP(0);
-    group_barrier(a.bar, ncta);
+    group_barrier(a.gbar, ncta_all, sysf);
     LRK_TSTAMP(1);
     // ---------------- phase 2: block CGS2 against the orthonormal pane
-    reduce_partials(part1, a.pstride, ncta, r * pc + pc, sPart);
+    reduce_partials(tab, 0, ncta_all, r * pc + pc, sPart);
     for (int i = tid; i < pc; i += NT) sYn[i] = sPart[r * pc + i];
     for (int i = tid; i < r * pc; i += NT) sC[i] = sPart[i];
     __syncthreads();
@@ -333,11 +342,11 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
       __syncthreads();
       cta_tn(Ul, ldu, r, Yl, ldy, pc, m_loc, sPart, sScr);
-      for (int i = tid; i < r * pc; i += NT) part2[(int64_t)cta * a.pstride + i] = sPart[i];
+      for (int i = tid; i < r * pc; i += NT) part2[i] = sPart[i];
       LRK_TSTAMP(10);
-      group_barrier(a.bar, ncta);
+      group_barrier(a.gbar, ncta_all, sysf);
       LRK_TSTAMP(11);
-      reduce_partials(part2, a.pstride, ncta, r * pc, sPart);
+      reduce_partials(tab, 1, ncta_all, r * pc, sPart);
       rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sPart, m_loc);
       for (int i = tid; i < r * pc; i += NT) sC[i] += sPart[i];
       __syncthreads();
@@ -345,22 +354,22 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     LRK_TSTAMP(2);
     // ---------------- phase 3: local Householder QR of the remainder
     block_qr_t<Q>(Yl, ldy, m_loc, pc, sTau, sR, sRed, sTmp);
-    for (int i = tid; i < pc * pc; i += NT) part3[(int64_t)cta * a.pstride + i] = sR[i];
+    for (int i = tid; i < pc * pc; i += NT) part3[i] = sR[i];
     LRK_TSTAMP(3);
-    group_barrier(a.bar, ncta);
+    group_barrier(a.gbar, ncta_all, sysf);
     LRK_TSTAMP(4);
     // ---------------- phase 4 (every CTA, redundantly): finish the TSQR
-    const int ms = ncta * pc;
+    const int ms = ncta_all * pc;
     double* stack;
     if constexpr (RES) stack = sm + a.off_scr;
     else stack = a.stack_smem ? sm + a.off_scr : gscr;
     double* stackY = stack + ms * pc;
     // register two-level TSQR when the stacked blocks fit 3 rows per lane
-    const bool fast_stack = (Q <= 4) && ((ncta + NWARP - 1) / NWARP) * pc <= 96;
+    const bool fast_stack = (Q <= 4) && ((ncta_all + NWARP - 1) / NWARP) * pc <= 96;
     int tail_tid = 0;
     if (fast_stack) {
       if constexpr (Q <= 4) {
-        const int wo = warp_stack_tsqr<Q, 3>(part3, a.pstride, ncta, pc, cta, sCore, sRp, sQs);
+        const int wo = warp_stack_tsqr<Q, 3>(tab, ncta_all, pc, gcta, sCore, sRp, sQs);
         tail_tid = wo * 32;
       }
       LRK_TSTAMP(13);
@@ -373,7 +382,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
 #pragma unroll
         for (int u = 0; u < BATCH; ++u) {
           const int idx = base + u * NT + tid;
-          v[u] = (idx < tot) ? __ldcg(part3 + (int64_t)(idx / pp) * a.pstride + idx % pp) : 0.0;
+          v[u] = (idx < tot) ? __ldcg(tab.at(2, idx / pp) + idx % pp) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < BATCH; ++u) {
@@ -390,7 +399,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       block_qr_t<Q>(stack, ms, ms, pc, sTauT, sRp, sRed, sTmp);
       LRK_TSTAMP(14);
       block_apply_q_t<Q>(stack, ms, ms, pc, sTauT, sI, stackY, ms, sRed, sTmp);
-      for (int i = tid; i < pc * pc; i += NT) sQs[i] = stackY[(cta * pc + i / pc) + (i % pc) * ms];
+      for (int i = tid; i < pc * pc; i += NT) sQs[i] = stackY[(gcta * pc + i / pc) + (i % pc) * ms];
       __syncthreads();
       LRK_TSTAMP(15);
     }
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       }
       __syncthreads();
     } else {
-      double* Aj = gscr + 2 * (int64_t)ncta * PMAX * PMAX;
+      double* Aj = gscr + 2 * (int64_t)ncta_all * PMAX * PMAX;
       double* Vj = Aj + (int64_t)NMAX * NMAX;
       for (int idx = tid; idx < n * n; idx += NT) {
         const int i = idx % n, j = idx / n;
