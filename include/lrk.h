@@ -193,6 +193,14 @@ int64_t lrk_launch_count(const lrk_ctx* ctx);
 /* Instrumentation for the roofline: when enabled, every sweep launch is
  * bracketed by CUDA events on its stream and its algorithmic bytes (DESIGN.md
  * §Roofline) are accumulated once the apply's ranks are known. */
+/* Config prior on physical rows:
+ * Y = (delta I + gamma L)^{-power} X (power 1 or 2), and its diagonal
+ * out[n_x] = diag((delta I + gamma L)^{-power}) (posterior variance with a
+ * non-scalar prior: diag(G_post) = g [diag(P^2) - sum_i l~_i (P v_i)^2]). */
+int lrk_prior_apply(lrk_ctx* ctx, double delta, double gamma, int power, const double* X,
+                    int64_t ldx, int ncols, double* Y, int64_t ldy, void* stream);
+int lrk_prior_diag(lrk_ctx* ctx, double delta, double gamma, int power, double* out,
+                   void* stream);
 /* Run every subsequent sweep of this context as nshard n_x shards (the
  * multi-GPU decomposition of SURVEY §8(e): global CTA rows, partials read
  * through a per-shard table, one shared barrier) emulated as nshard groups of

@@ -451,16 +451,21 @@ def ritz_vectors(H, basis):
     return vals, out
 
 
-def posterior_variance(vals, vecs, gamma, eps_eig):
-    """SMW variance diag γ(1 - Σ λ̃ v²) with QR re-orthonormalisation (posterior.py:56-111)."""
+def posterior_variance(vals, vecs, gamma, eps_eig, prior_matrix=None):
+    """SMW variance diag γ(1 - Σ λ̃ v²) with QR re-orthonormalisation (posterior.py:56-111).
+    Config prior: prior_matrix = dense P = (δI+γ_pL)⁻¹ and
+    diag = γ(diag(P²) - Σ λ̃ (P v)²)."""
     real = np.asarray(vals).real
     keep = [i for i in np.argsort(-real) if real[i] >= eps_eig]
+    base = 1.0 if prior_matrix is None else np.sum(prior_matrix * prior_matrix, axis=0)
     if not keep:
-        return np.full(len(vecs[0]), gamma)
+        return gamma * base * np.ones(len(vecs[0]))
     V = np.column_stack([vecs[i] / np.linalg.norm(vecs[i]) for i in keep])
     V = np.linalg.qr(V)[0]
+    if prior_matrix is not None:
+        V = prior_matrix @ V
     lam = real[keep]
-    return gamma * (1.0 - (V**2) @ (lam / (lam + 1.0)))
+    return gamma * (base - (V**2) @ (lam / (lam + 1.0)))
 
 
 # ------------------------------------------------------------- closed forms

@@ -77,6 +77,9 @@ _SIGNATURES = {
     "lrk_launch_count": (c_int64, [c_void_p]),
     "lrk_profile_enable": (c_int, [c_void_p, c_int]),
     "lrk_set_emulated_shards": (c_int, [c_void_p, c_int]),
+    "lrk_prior_apply": (c_int, [c_void_p, c_double, c_double, c_int, c_void_p, c_int64, c_int,
+                                c_void_p, c_int64, c_void_p]),
+    "lrk_prior_diag": (c_int, [c_void_p, c_double, c_double, c_int, c_void_p, c_void_p]),
     "lrk_profile_read": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int64), POINTER(c_double),
                                  c_int]),
     "lrk_last_traces": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), c_int, POINTER(c_int),

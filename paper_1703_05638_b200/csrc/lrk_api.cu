@@ -39,6 +39,7 @@ struct lrk_ctx {
   int64_t n_x = 0;
   int n = 0;
   double* dS = nullptr;       // n x n DST-I (symmetric, orthogonal)
+  double* dSsq = nullptr;     // n x n elementwise square of the DST-I (operator diagonals)
   double* dTheta = nullptr;   // n_x: eigenvalues of S^{-1} M  = 1/(1+tau*lambda)
   double* dThetaM = nullptr;  // n_x: theta / m_scale (eigenvalues of S^{-1})
   double* dE0 = nullptr;      // n_t: e_0
@@ -65,7 +66,7 @@ struct lrk_ctx {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
     for (auto& kv : ws) cudaFree(kv.second.p);
     cudaFree(dS); cudaFree(dTheta); cudaFree(dThetaM); cudaFree(dE0); cudaFree(dInvLam);
-    cudaFree(dLam);
+    cudaFree(dLam); cudaFree(dSsq);
     cudaFree(dList); cudaFree(dS1T); cudaFree(dS2); cudaFree(dS1); cudaFree(dS2T);
   }
 };
@@ -165,27 +166,28 @@ int gemm(lrk_ctx* c, int M, int N, int K, const double* A, int64_t lda, int64_t 
 // (emul: an n_x array in the x1-fastest layout, shared by all columns).
 int dst2(lrk_ctx* c, const double* X, int64_t ldx, double* Y, int64_t ldy, int ncols,
          const int* ncols_dev, double alpha, cudaStream_t s, const double* emul = nullptr,
-         double beta = 0.0) {
+         double beta = 0.0, const double* Smat = nullptr) {
   if (ncols <= 0) return LRK_OK;
   const int n = c->n;
   const int64_t nx = c->n_x;
+  const double* dS = Smat ? Smat : c->dS;  // per-axis transform (DST-I, or S∘S for diagonals)
   WS(double, T, "dst_T", nx * (int64_t)ncols);
   if (c->op.dim == 2) {
     // T_j = X_j S      (X_j: n x n row-major view of column j)
-    TRY(gemm(c, n, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
+    TRY(gemm(c, n, n, n, X, n, ldx, dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
     // Y_j = alpha S T_j
-    TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s, 1, emul,
+    TRY(gemm(c, n, n, n, dS, n, 0, T, n, nx, Y, n, ldy, alpha, ncols, ncols_dev, s, 1, emul,
              n, beta));
     return LRK_OK;
   }
   const int64_t pl = (int64_t)n * n;
   WS(double, T2, "dst_T2", nx * (int64_t)ncols);
   // x1: T_j = X_j S, X_j viewed as (n^2) x n row-major
-  TRY(gemm(c, (int)pl, n, n, X, n, ldx, c->dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
+  TRY(gemm(c, (int)pl, n, n, X, n, ldx, dS, n, 0, T, n, nx, 1.0, ncols, ncols_dev, s));
   // x2: per (column, x3-plane) slice: T2 = S T_slice  (batch ncols * n, stride n^2)
-  TRY(gemm(c, n, n, n, c->dS, n, 0, T, n, pl, T2, n, pl, 1.0, ncols * n, ncols_dev, s, n));
+  TRY(gemm(c, n, n, n, dS, n, 0, T, n, pl, T2, n, pl, 1.0, ncols * n, ncols_dev, s, n));
   // x3: Y_j = alpha S T2_j, T2_j viewed as n x (n^2) row-major
-  TRY(gemm(c, n, (int)pl, n, c->dS, n, 0, T2, pl, nx, Y, pl, ldy, alpha, ncols, ncols_dev, s, 1,
+  TRY(gemm(c, n, (int)pl, n, dS, n, 0, T2, pl, nx, Y, pl, ldy, alpha, ncols, ncols_dev, s, 1,
            emul, pl, beta));
   return LRK_OK;
 }
@@ -947,6 +949,51 @@ const char* lrk_last_error(const lrk_ctx* c) { return c ? c->err.c_str() : "null
 
 int64_t lrk_launch_count(const lrk_ctx* c) { return c ? c->launches : 0; }
 
+// Config prior: Y = (delta I + gamma L)^{-power} X
+// through the DST-I (physical rows in and out).
+int lrk_prior_apply(lrk_ctx* c, double delta, double gamma, int power, const double* X,
+                    int64_t ldx, int ncols, double* Y, int64_t ldy, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  if (!c->has_op) return fail(c, LRK_ERR_CONFIG, "no operator installed");
+  if (!(delta > 0.0) || gamma < 0.0 || power < 1 || power > 2)
+    return fail(c, LRK_ERR_CONFIG, "prior needs delta > 0, gamma >= 0, power 1 or 2");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (ncols <= 0) return LRK_OK;
+  const int64_t nx = c->n_x;
+  WS(double, T, "pa_T", nx * (int64_t)ncols);
+  TRY(dst2(c, X, ldx, T, nx, ncols, nullptr, 1.0, s));
+  for (int k = 0; k < power; ++k) {
+    prior_scale_kernel<<<dim3(grid1(nx, 256, 1024), ncols), 256, 0, s>>>(
+        T, nx, c->dLam, nx, ncols, nullptr, 1.0, delta, gamma, T, nx);
+    CKL();
+  }
+  TRY(dst2(c, T, nx, Y, ldy, ncols, nullptr, 1.0, s));
+  return LRK_OK;
+}
+
+// diag((delta I + gamma L)^{-power}) = (Phi∘Phi) d, d_k = (delta + gamma lambda_k)^{-power}:
+// the DST passes with S∘S in place of S (separable, one GEMM per axis).
+int lrk_prior_diag(lrk_ctx* c, double delta, double gamma, int power, double* out, void* stream) {
+  if (!c) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  if (!c->has_op) return fail(c, LRK_ERR_CONFIG, "no operator installed");
+  if (!(delta > 0.0) || gamma < 0.0 || power < 1 || power > 2)
+    return fail(c, LRK_ERR_CONFIG, "prior needs delta > 0, gamma >= 0, power 1 or 2");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nx = c->n_x;
+  WS(double, d, "pd_d", nx);
+  fill_kernel<<<dim3(grid1(nx, 256, 1024), 1), 256, 0, s>>>(d, nx, nx, 1, 1.0);
+  CKL();
+  for (int k = 0; k < power; ++k) {
+    prior_scale_kernel<<<dim3(grid1(nx, 256, 1024), 1), 256, 0, s>>>(
+        d, nx, c->dLam, nx, 1, nullptr, 1.0, delta, gamma, d, nx);
+    CKL();
+  }
+  TRY(dst2(c, d, nx, out, nx, 1, nullptr, 1.0, s, nullptr, 0.0, c->dSsq));
+  return LRK_OK;
+}
+
 int lrk_set_emulated_shards(lrk_ctx* c, int nshard) {
   if (!c) return LRK_ERR_CONFIG;
   if (nshard < 1 || nshard > SHARD_MAX) return fail(c, LRK_ERR_CONFIG, "nshard must lie in [1, 8]");
@@ -1043,6 +1090,13 @@ int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
   CK(cudaMalloc(&c->dLam, nx * sizeof(double)));
   CK(cudaMemcpy(c->dLam, lm.data(), nx * sizeof(double), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&c->dS, S.size() * sizeof(double)));
+  {
+    std::vector<double> S2(S.size());
+    for (size_t k = 0; k < S.size(); ++k) S2[k] = S[k] * S[k];
+    cudaFree(c->dSsq);
+    CK(cudaMalloc(&c->dSsq, S2.size() * sizeof(double)));
+    CK(cudaMemcpy(c->dSsq, S2.data(), S2.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   CK(cudaMalloc(&c->dTheta, nx * sizeof(double)));
   CK(cudaMalloc(&c->dThetaM, nx * sizeof(double)));
   CK(cudaMalloc(&c->dE0, e0.size() * sizeof(double)));

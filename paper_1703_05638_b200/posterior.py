@@ -1,7 +1,10 @@
 """Low-rank posterior covariance via Sherman-Morrison-Woodbury (mirrors lrpostcov/posterior.py).
 
 Γ_post v = γ (v - V (λ̃ ∘ Vᵀv)),  diag(Γ_post) = γ (1 - Σ_i λ̃_i V[:, i]²),
-λ̃ = λ/(λ+1) (posterior.py:1-9).  Runs once after the Arnoldi recurrence on
+λ̃ = λ/(λ+1) (posterior.py:1-9).  With the config prior Γ^{1/2} = √γ P,
+P = (δI + γ_p L)⁻¹:
+Γ_post v = γ P (Pv - V(λ̃ ∘ VᵀPv)),  diag(Γ_post) = γ (diag(P²) - Σ_i λ̃_i (P v_i)²),
+with P·X and diag(P²) on the device (lrk_prior_apply / lrk_prior_diag).  Runs once after the Arnoldi recurrence on
 the n_x x k Ritz basis; the arithmetic is done with device tensors and the
 summary is returned as numpy arrays like the reference.
 """
@@ -30,6 +33,7 @@ class PosteriorSummary:
     V: np.ndarray
     gamma_prior: float
     variance_field: np.ndarray
+    prior: object = None  # config prior (hessian.ConfigPrior) or None for γ·I
 
     @property
     def k(self) -> int:
@@ -56,22 +60,33 @@ def _as_dev(V):
     return t.to("cuda")
 
 
-def variance_diag(eigenvalues, V, gamma_prior: float) -> np.ndarray:
-    """γ (1 - Σ λ̃ V²) after re-orthonormalising V (posterior.py:56-62)."""
+def _prior_terms(Vd, prior):
+    """(P V, diag(P²)) for the config prior, or (V, 1) for the scalar prior."""
+    if prior is None:
+        return Vd, 1.0
+    return prior.apply(Vd, 1), prior.diag(2)
+
+
+def variance_diag(eigenvalues, V, gamma_prior: float, prior=None) -> np.ndarray:
+    """γ (1 - Σ λ̃ V²) after re-orthonormalising V (posterior.py:56-62);
+    γ (diag(P²) - Σ λ̃ (P V)²) with the config prior."""
     torch = _torch()
     Vd = _as_dev(V)
     if Vd.ndim == 1:
         Vd = Vd.reshape(1, -1)
     Vd = _reorthonormalize_dev(Vd)
     filt = np.array([lambda_tilde(float(l)) for l in np.atleast_1d(eigenvalues)])
+    PV, dP2 = _prior_terms(Vd, prior)
     if Vd.shape[1] == 0:
-        return np.full(Vd.shape[0], gamma_prior)
+        base = dP2 if prior is not None else torch.ones(Vd.shape[0], dtype=torch.float64,
+                                                         device=Vd.device)
+        return (gamma_prior * base).cpu().numpy()
     f = torch.as_tensor(filt, device=Vd.device)
-    return (gamma_prior * (1.0 - (Vd * Vd) @ f)).cpu().numpy()
+    return (gamma_prior * (dP2 - (PV * PV) @ f)).cpu().numpy()
 
 
 def build_summary(ritz_values, ritz_vectors, gamma_prior: float, eps_eig: float | None = None,
-                  imag_rtol: float = 1e-6, n_x: int | None = None) -> PosteriorSummary:
+                  imag_rtol: float = 1e-6, n_x: int | None = None, prior=None) -> PosteriorSummary:
     """Retain λ >= eps_eig, normalise, re-orthonormalise, variance (posterior.py:65-111)."""
     torch = _torch()
     vals = np.asarray(ritz_values)
@@ -99,18 +114,30 @@ def build_summary(ritz_values, ritz_vectors, gamma_prior: float, eps_eig: float 
     Vd = _reorthonormalize_dev(Vd)
     lams = real[keep]
     filters = np.array([lambda_tilde(float(l)) for l in lams])
+    PV, dP2 = _prior_terms(Vd, prior)
     if Vd.shape[1]:
         f = torch.as_tensor(filters, device=Vd.device)
-        var = (gamma_prior * (1.0 - (Vd * Vd) @ f)).cpu().numpy()
+        var = (gamma_prior * (dP2 - (PV * PV) @ f)).cpu().numpy()
+    elif prior is not None:
+        var = (gamma_prior * dP2).cpu().numpy()
     else:
         var = np.full(Vd.shape[0], gamma_prior)
     return PosteriorSummary(eigenvalues=lams, filters=filters, V=Vd.cpu().numpy(),
-                            gamma_prior=gamma_prior, variance_field=var)
+                            gamma_prior=gamma_prior, variance_field=var, prior=prior)
 
 
 def posterior_apply(v, summary: PosteriorSummary) -> np.ndarray:
-    """Γ_post v (posterior.py:120-125)."""
+    """Γ_post v (posterior.py:120-125); γ P (Pv - V(λ̃ ∘ VᵀPv)) with the config prior."""
     v = np.asarray(v, dtype=float)
+    P = summary.prior
+    if P is not None:
+        torch = _torch()
+        pv = P.apply(_as_dev(v).reshape(-1, 1), 1)
+        if summary.k:
+            V = _as_dev(summary.V)
+            f = torch.as_tensor(summary.filters, device=V.device)
+            pv = pv - V @ (f[:, None] * (V.T @ pv))
+        return (summary.gamma_prior * P.apply(pv, 1)).reshape(-1).cpu().numpy()
     if summary.k == 0:
         return summary.gamma_prior * v
     V = summary.V

@@ -546,3 +546,44 @@ def test_emulated_nx_shards_hessian_c2_config():
     b = ctx.apply(v)
     assert np.array_equal(a, b)
     assert ctx.rank_trace[-1] == ctx.rank_trace[-2]
+
+
+def test_config_prior_arnoldi_and_posterior_variance_vs_oracle():
+    """C2-type configuration at reduced size (Q1-lumped, (I+0.05L)⁻² prior,
+    w = 1/σ², point subgrid): Arnoldi Ritz values (1e-6) and the posterior
+    variance diag(Γ_post) = γ(diag(P²) - Σ λ̃ (P v)²) (1e-5) against the oracle."""
+    n_side, n_t, m_a = 20, 16, 12
+    grid = lp.build_grid(n_side)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, "q1"), lp.build_time_grid(n_t))
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    layout = lp.make_sensor_subgrid(grid, 5)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=POL)
+    v1 = np.random.default_rng(70).standard_normal(grid.n_x)
+    v1 /= np.linalg.norm(v1)
+    res = lp.lr_arnoldi(ctx.apply, v1, POL, lp.StopRule(m_a=m_a, eps_eig=1e-1, check_every=100),
+                        rank_source=ctx.rank_trace)
+    P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, stencil="q1", prior=(1.0, 0.05))
+    H, basis, vals, iters = O.arnoldi_dense(lambda x: O.hessian_ic(P, x)[0], v1, m_a,
+                                            eps_eig=1e-1, check_every=100)
+    assert res.iterations == iters
+    lead = vals.real >= 1e-1
+    np.testing.assert_allclose(res.ritz_values.real[: lead.sum()], vals.real[lead], rtol=1e-6)
+    summ = lp.build_summary(res.ritz_values, res.ritz_vectors, 1.0, 1e-1, prior=ctx.prior)
+    rv, rvecs = O.ritz_vectors(H, basis)
+    L, _, _ = O.config_operator(n_side, 2, "q1")
+    Pm = np.linalg.inv(np.eye(grid.n_x) + 0.05 * L.toarray())
+    var_ref = O.posterior_variance(rv, rvecs, 1.0, 1e-1, prior_matrix=Pm)
+    np.testing.assert_allclose(summ.variance_field, var_ref, rtol=1e-5)
+    # diag(P²) and P·x on the device against the dense prior
+    np.testing.assert_allclose(ctx.prior.diag(2).cpu().numpy(), np.sum(Pm * Pm, axis=0),
+                               rtol=1e-12)
+    x = np.random.default_rng(71).standard_normal(grid.n_x)
+    np.testing.assert_allclose(ctx.prior.apply(x.reshape(-1, 1), 1).cpu().numpy()[:, 0], Pm @ x,
+                               rtol=1e-11, atol=1e-13)
+    # posterior_apply: γ P (Pv - V(λ̃ ∘ VᵀPv))
+    Vk = summ.V
+    pv = Pm @ x
+    ref_apply = Pm @ (pv - Vk @ (summ.filters * (Vk.T @ pv)))
+    np.testing.assert_allclose(lp.posterior_apply(x, summ), ref_apply, rtol=1e-10,
+                               atol=1e-12 * np.abs(ref_apply).max())
