@@ -26,6 +26,7 @@ __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, 
     double s[Q];
 #pragma unroll
     for (int k = 0; k < Q; ++k) s[k] = 0.0;
+#pragma unroll 4
     for (int i = j + 1 + tid; i < m; i += NT) {
       const double xj = X[i + (int64_t)j * ldx];
 #pragma unroll
@@ -56,6 +57,7 @@ __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, 
 #pragma unroll
     for (int k = 0; k < Q; ++k) f[k] = (k > j && k < q) ? t * (xr[k] + scale * s[k]) : 0.0;
     __syncthreads();  // row j read by everyone before it changes
+#pragma unroll 4
     for (int i = j + 1 + tid; i < m; i += NT) {
       const double vi = X[i + (int64_t)j * ldx] * scale;
       double x[Q];
@@ -104,6 +106,7 @@ __device__ __forceinline__ void block_apply_q_t(const double* __restrict__ X, in
     double w[Q];
 #pragma unroll
     for (int c = 0; c < Q; ++c) w[c] = 0.0;
+#pragma unroll 4
     for (int i = j + 1 + tid; i < m; i += NT) {
       const double vi = X[i + (int64_t)j * ldx];
 #pragma unroll
@@ -115,6 +118,7 @@ __device__ __forceinline__ void block_apply_q_t(const double* __restrict__ X, in
 #pragma unroll
     for (int c = 0; c < Q; ++c) f[c] = (c < q) ? t * (w[c] + Y[j + (int64_t)c * ldy]) : 0.0;
     __syncthreads();
+#pragma unroll 4
     for (int i = j + 1 + tid; i < m; i += NT) {
       const double vi = X[i + (int64_t)j * ldx];
 #pragma unroll
@@ -130,24 +134,156 @@ __device__ __forceinline__ void block_apply_q_t(const double* __restrict__ X, in
   }
 }
 
+// Y (m x q) = H_0 ... H_{q-1} [G; 0] in ONE pass over the rows via the compact
+// WY form H_0...H_{q-1} = I - V T V^T (LAPACK larft, forward columnwise):
+// Y = [G; 0] - V M,  M = T (V_top^T G),  V unit lower-trapezoidal (the
+// reflectors left below the diagonal of X by block_qr_t).  One reduction pass
+// forms V^T V; T and M are q x q on one thread.  wsm: 3*Q*Q shared doubles.
+template <int Q>  // Q <= 4 (block_sum scratch: NWARP * Q(Q+1)/2 <= NWARP * PMAX)
+__device__ __forceinline__ void block_apply_q_wy(const double* __restrict__ X, int64_t ldx, int m,
+                                                 int q, const double* __restrict__ tau,
+                                                 const double* __restrict__ G,
+                                                 double* __restrict__ Y, int64_t ldy,
+                                                 double* __restrict__ red, double* __restrict__ tmp,
+                                                 double* __restrict__ wsm) {
+  constexpr int NP = Q * (Q + 1) / 2;
+  const int tid = threadIdx.x;
+  // V^T V (upper triangle, packed): rows >= q only; the q x q top is added below
+  double acc[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) acc[k] = 0.0;
+#pragma unroll 4
+  for (int i = q + tid; i < m; i += NT) {
+    double v[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) v[c] = (c < q) ? X[i + (int64_t)c * ldx] : 0.0;
+    int k = 0;
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+      for (int b = a; b < Q; ++b) acc[k++] += v[a] * v[b];
+  }
+  block_sum<NP>(acc, red, tmp);  // tmp[0..NP) = packed V_bot^T V_bot (all threads see acc)
+  double* T = wsm;
+  double* M = wsm + Q * Q;
+  if (tid == 0) {
+    double Vt[Q][Q];  // V_top (unit lower)
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+      for (int c = 0; c < Q; ++c)
+        Vt[i][c] = (i < q && i < m && c < q) ? (i == c ? 1.0 : (i > c ? X[i + (int64_t)c * ldx] : 0.0)) : 0.0;
+    double VV[Q][Q];
+    {
+      int k = 0;
+#pragma unroll
+      for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int b = a; b < Q; ++b) {
+          double sv = acc[k++];
+#pragma unroll
+          for (int i = 0; i < Q; ++i) sv += Vt[i][a] * Vt[i][b];
+          VV[a][b] = sv;
+          VV[b][a] = sv;
+        }
+    }
+    double Tm[Q][Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+#pragma unroll
+      for (int j = 0; j < Q; ++j) Tm[i][j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      if (j >= q) break;
+      const double tj = tau[j];
+      Tm[j][j] = tj;
+      // T[0:j, j] = -tau_j T[0:j, 0:j] (V^T v_j)[0:j]
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        if (i >= j) break;
+        double sv = 0.0;
+#pragma unroll
+        for (int l = 0; l < Q; ++l)
+          if (l >= i && l < j) sv += Tm[i][l] * VV[l][j];
+        Tm[i][j] = -tj * sv;
+      }
+    }
+    // M = T (V_top^T G)
+    double W[Q][Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        double sv = 0.0;
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+          if (i < q && c < q) sv += Vt[i][a] * G[i * q + c];
+        W[a][c] = sv;
+      }
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        double sv = 0.0;
+#pragma unroll
+        for (int l = 0; l < Q; ++l) sv += Tm[a][l] * W[l][c];
+        M[a * Q + c] = sv;
+      }
+  }
+  __syncthreads();
+  double Mr[Q][Q];
+#pragma unroll
+  for (int a = 0; a < Q; ++a)
+#pragma unroll
+    for (int c = 0; c < Q; ++c) Mr[a][c] = M[a * Q + c];
+#pragma unroll 4
+  for (int i = tid; i < m; i += NT) {
+    double v[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c)
+      v[c] = (c < q) ? (i == c ? 1.0 : (i > c ? X[i + (int64_t)c * ldx] : 0.0)) : 0.0;
+#pragma unroll
+    for (int c = 0; c < Q; ++c) {
+      if (c >= q) break;
+      double y = (i < q) ? G[i * q + c] : 0.0;
+#pragma unroll
+      for (int a = 0; a < Q; ++a) y -= v[a] * Mr[a][c];
+      Y[i + (int64_t)c * ldy] = y;
+    }
+  }
+  __syncthreads();
+}
+
 // X[:, 0..nx) -= A[:, 0..na) Cm, Cm na x nx row-major (shared); nx <= Q.
 template <int Q>
 __device__ __forceinline__ void rows_sub_t(double* __restrict__ X, int64_t ldx, int nx,
                            const double* __restrict__ A, int64_t lda, int na,
                            const double* __restrict__ Cm, int nrows) {
-  for (int t = threadIdx.x; t < nrows; t += NT) {
-    double acc[Q];
+  // two rows per thread iteration (independent load streams)
+  for (int t = threadIdx.x; t < nrows; t += 2 * NT) {
+    const int t2 = t + NT;
+    const bool two = t2 < nrows;
+    double acc[Q], acc2[Q];
 #pragma unroll
-    for (int j = 0; j < Q; ++j) acc[j] = 0.0;
+    for (int j = 0; j < Q; ++j) acc[j] = acc2[j] = 0.0;
+#pragma unroll 8
     for (int i = 0; i < na; ++i) {
       const double a = A[t + (int64_t)i * lda];
+      const double a2 = two ? A[t2 + (int64_t)i * lda] : 0.0;
 #pragma unroll
       for (int j = 0; j < Q; ++j)
-        if (j < nx) acc[j] += a * Cm[i * nx + j];
+        if (j < nx) {
+          const double c = Cm[i * nx + j];
+          acc[j] += a * c;
+          acc2[j] += a2 * c;
+        }
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j)
-      if (j < nx) X[t + (int64_t)j * ldx] -= acc[j];
+      if (j < nx) {
+        X[t + (int64_t)j * ldx] -= acc[j];
+        if (two) X[t2 + (int64_t)j * ldx] -= acc2[j];
+      }
   }
 }
 
@@ -313,34 +449,104 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
                                                  int m) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int n = na + nb;
+  const int n = na + nb;  // <= 32: every operand of a row tile is loaded up front
   const int ntile = (m + 7) >> 3;
-  for (int tile = warp; tile < ntile; tile += NWARP) {
-    const int row = tile * 8 + g;
-    double acc[NT8][2];
+  // two row tiles per warp iteration: 16 independent loads in flight per lane
+  for (int tile0 = warp * 2; tile0 < ntile; tile0 += NWARP * 2) {
+    double av[2][8];
 #pragma unroll
-    for (int j = 0; j < NT8; ++j) acc[j][0] = acc[j][1] = 0.0;
-    for (int k0 = 0; k0 < n; k0 += 4) {
-      const int k = k0 + t;
-      double a = 0.0;
-      if (row < m && k < n) a = (k < na) ? A[row + (int64_t)k * lda] : B[row + (int64_t)(k - na) * ldb];
+    for (int h = 0; h < 2; ++h) {
+      const int row = (tile0 + h) * 8 + g;
 #pragma unroll
-      for (int j = 0; j < NT8; ++j) {
-        const int col = j * 8 + g;
-        const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
-        dmma884(acc[j][0], acc[j][1], a, b);
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = kk * 4 + t;
+        av[h][kk] = 0.0;
+        if (row < m && k < n) av[h][kk] = (k < na) ? A[row + (int64_t)k * lda] : B[row + (int64_t)(k - na) * ldb];
       }
     }
-    __syncwarp();
 #pragma unroll
-    for (int j = 0; j < NT8; ++j) {
-      const int c0 = j * 8 + 2 * t;
-      if (row < m) {
-        if (c0 < rn) A[row + (int64_t)c0 * lda] = acc[j][0];
-        if (c0 + 1 < rn) A[row + (int64_t)(c0 + 1) * lda] = acc[j][1];
+    for (int h = 0; h < 2; ++h) {
+      const int row = (tile0 + h) * 8 + g;
+      double acc[NT8][2];
+#pragma unroll
+      for (int j = 0; j < NT8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (kk * 4 >= n) break;
+        const int k = kk * 4 + t;
+#pragma unroll
+        for (int j = 0; j < NT8; ++j) {
+          const int col = j * 8 + g;
+          const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
+          dmma884(acc[j][0], acc[j][1], av[h][kk], b);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < NT8; ++j) {
+        const int c0 = j * 8 + 2 * t;
+        if (row < m) {
+          if (c0 < rn) A[row + (int64_t)c0 * lda] = acc[j][0];
+          if (c0 + 1 < rn) A[row + (int64_t)(c0 + 1) * lda] = acc[j][1];
+        }
       }
     }
   }
+}
+
+// CTA partial of A^T B (na <= 8*NI, nb <= 8) on the FP64 tensor pipe:
+// warp w takes a contiguous row chunk; m8n8k4 with the A-operand = rows k..k+3
+// of 8 columns of A (lane (g,t) reads A[k+t, 8i+g]: fully used 32-byte
+// sectors) and the B-operand = B[k+t, g]; U k-steps of loads are issued
+// before their DMMAs.  Per-warp partials meet in wbuf (NWARP*na*nb shared
+// doubles) and are summed in warp order into out[i*nb + j].
+template <int NI>
+__device__ __forceinline__ void cta_tn_dmma(const double* __restrict__ A, int64_t lda, int na,
+                                            const double* __restrict__ B, int64_t ldb, int nb,
+                                            int nrows, double* __restrict__ out,
+                                            double* __restrict__ wbuf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int chunk = (((nrows + NWARP - 1) / NWARP) + 3) & ~3;
+  const int r0 = warp * chunk;
+  const int r1 = min(nrows, r0 + chunk);
+  double acc[NI][2];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) acc[i][0] = acc[i][1] = 0.0;
+  constexpr int U = 8 / (NI > 4 ? 2 : 1);  // k-steps of loads in flight
+  for (int k0 = r0; k0 < r1; k0 += 4 * U) {
+    double av[U][NI], bv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + 4 * u + t;
+      const bool ok = k < r1;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int col = 8 * i + g;
+        av[u][i] = (ok && col < na) ? A[k + (int64_t)col * lda] : 0.0;
+      }
+      bv[u] = (ok && g < nb) ? B[k + (int64_t)g * ldb] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) dmma884(acc[i][0], acc[i][1], av[u][i], bv[u]);
+  }
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ii = 8 * i + g, jj = 2 * t + h;
+      if (ii < na && jj < nb) wbuf[(warp * na + ii) * nb + jj] = acc[i][h];
+    }
+  __syncthreads();
+  for (int o = threadIdx.x; o < na * nb; o += NT) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) s += wbuf[w * na * nb + o];
+    out[o] = s;
+  }
+  __syncthreads();
 }
 
 // Column-pivoted Householder QR of the q x q (q <= Q) matrix A held in

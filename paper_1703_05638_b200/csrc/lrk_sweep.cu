@@ -260,6 +260,18 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     tprev = t_;                     \
   }
 
+  // U^T Y projections of the CGS passes: DMMA with per-warp partials in the
+  // (then idle) stack scratch; scalar fallback for very wide panes
+  double* const wbuf = a.stack_smem ? sm + a.off_scr : gscr;
+  const int wcap = a.stack_smem ? 2 * ncta_all * p * p : (int)a.scratch_stride;
+  auto proj = [&](int rr, int pcc, double* outp) {
+    if (rr <= 32 && NWARP * rr * pcc <= wcap)
+      cta_tn_dmma<4>(Ul, ldu, rr, Yl, ldy, pcc, m_loc, outp, wbuf);
+    else if (rr <= 64 && NWARP * rr * pcc <= wcap)
+      cta_tn_dmma<8>(Ul, ldu, rr, Yl, ldy, pcc, m_loc, outp, wbuf);
+    else
+      cta_tn(Ul, ldu, rr, Yl, ldy, pcc, m_loc, outp, sScr);
+  };
   int r = a.r_init >= 0 ? a.r_init : a.info[0];  // < 0: rank left by the previous chunk
   int jac_sweeps = 0;
   const int nflush = (n_t + p - 1) / p;
@@ -292,6 +304,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
         double acc[Q];
 #pragma unroll
         for (int s = 0; s < Q; ++s) acc[s] = 0.0;
+#pragma unroll 4
         for (int j = 0; j < rb; ++j) {
           const double b = a.B[r0 + i + (int64_t)j * a.ldb];
           const double* w2 = a.W2 + (int64_t)j * a.ldw2;
@@ -314,7 +327,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       }
     }
     __syncthreads();
-    if (r > 0) cta_tn(Ul, ldu, r, Yl, ldy, pc, m_loc, sPart, sScr);
+    if (r > 0) proj(r, pc, sPart);
     {
       double v[Q];
 #pragma unroll
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     if (r > 0) {
       rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
       __syncthreads();
-      cta_tn(Ul, ldu, r, Yl, ldy, pc, m_loc, sPart, sScr);
+      proj(r, pc, sPart);
       for (int i = tid; i < r * pc; i += NT) part2[i] = sPart[i];
       LRK_TSTAMP(10);
       group_barrier(a.gbar, ncta_all, sysf);
@@ -459,7 +472,8 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     __syncthreads();
     LRK_TSTAMP(5);
     // explicit Q~ rows of this CTA: Q_loc * G
-    block_apply_q_t<Q>(Yl, ldy, m_loc, pc, sTau, sG, Ql, ldq, sRed, sTmp);
+    if constexpr (Q <= 4) block_apply_q_wy<Q>(Yl, ldy, m_loc, pc, sTau, sG, Ql, ldq, sRed, sTmp, sCore);
+    else block_apply_q_t<Q>(Yl, ldy, m_loc, pc, sTau, sG, Ql, ldq, sRed, sTmp);
     LRK_TSTAMP(6);
     // ---------------- core SVD: [[diag(sig), C], [0, Rblock]]
     const int n = r + pc;
