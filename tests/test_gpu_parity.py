@@ -587,3 +587,43 @@ def test_config_prior_arnoldi_and_posterior_variance_vs_oracle():
     ref_apply = Pm @ (pv - Vk @ (summ.filters * (Vk.T @ pv)))
     np.testing.assert_allclose(lp.posterior_apply(x, summ), ref_apply, rtol=1e-10,
                                atol=1e-12 * np.abs(ref_apply).max())
+
+
+# ------------------------------------------------- flush widths and ragged schedules
+@pytest.mark.parametrize("p,n_side,n_t,adjoint,resident", [
+    (1, 15, 9, False, True), (2, 15, 11, True, True), (3, 20, 13, False, True),
+    (8, 24, 29, False, True), (8, 24, 29, True, True), (16, 24, 37, False, True),
+    (4, 400, 10, False, False), (2, 400, 7, True, False), (8, 400, 19, False, False),
+])
+def test_sweep_flush_widths_vs_oracle(p, n_side, n_t, adjoint, resident):
+    """compress_every in {1, 2, 3, 8, 16} (the Q=1/2/4/8/16 kernel variants),
+    n_t not a multiple of p, forward and adjoint, resident (SMEM) and global
+    rows (n_x = 160,000): rank traces and fields against the oracle."""
+    grid, K = _heat(n_side, n_t)
+    rng = np.random.default_rng(80 + p + n_t)
+    R1 = rng.standard_normal((grid.n_x, 2)) * np.array([1.0, 1e-3])
+    R2 = rng.standard_normal((n_t, 2))
+    L, h, m = O.fd_operator(n_side)
+    solver = O.StepSolver(L, m, 1.0 / n_t, n_t)
+    Y1, Y2, tr_ref = O.sweep(solver, R1, R2, 1e-8, None, adjoint, p)
+    tr = []
+    Y = lp.st_solve_sweep(K, lp.LowRankMat(R1, R2), POL, adjoint=adjoint, compress_every=p, trace=tr)
+    assert tr == tr_ref
+    ref = Y1 @ Y2.T
+    assert np.linalg.norm(_dense(Y) - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("rmax", [1, 3])
+def test_sweep_rank_cap_vs_oracle(rmax):
+    """Rank cap binding at every flush (the r_max branch of _rank_cut)."""
+    n_side, n_t = 20, 16
+    grid, K = _heat(n_side, n_t)
+    rng = np.random.default_rng(90 + rmax)
+    R1, R2 = rng.standard_normal((grid.n_x, 3)), rng.standard_normal((n_t, 3))
+    L, h, m = O.fd_operator(n_side)
+    Y1, Y2, tr_ref = O.sweep(O.StepSolver(L, m, 1.0 / n_t, n_t), R1, R2, 1e-8, rmax, False, 4)
+    tr = []
+    Y = lp.st_solve_sweep(K, lp.LowRankMat(R1, R2), lp.TruncationPolicy(1e-8, rmax), trace=tr)
+    assert tr == tr_ref and max(tr) <= rmax
+    ref = Y1 @ Y2.T
+    assert np.linalg.norm(_dense(Y) - ref) <= 1e-10 * np.linalg.norm(ref)
