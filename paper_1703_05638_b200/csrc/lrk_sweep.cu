@@ -494,14 +494,15 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
         double v = 0.0;
         if (i < r) v = (j < r) ? (i == j ? sSig[i] : 0.0) : sC[i * pc + (j - r)];
         else if (j >= r) v = sRp[(i - r) * pc + (j - r)];
-        sCore[i + j * 33] = v;
+        sCore[j + i * 33] = v;  // K^T: Jacobi on the rows of the core
       }
       __syncthreads();
       if (warp < 4) {  // 4-warp register Jacobi (named barrier 1), sScr = gbuf
-        if (n <= 8) jac_sweeps += multi_warp_jacobi<8, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
-        else if (n <= 16) jac_sweeps += multi_warp_jacobi<16, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
-        else if (n <= 24) jac_sweeps += multi_warp_jacobi<24, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
-        else jac_sweeps += multi_warp_jacobi<32, 4>(sCore, 33, n, Uc, Vc, ldc, sS, iPerm, sScr);
+        // K^T = Vk S Uk^T: the routine's left vectors are K's right ones
+        if (n <= 8) jac_sweeps += multi_warp_jacobi<8, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
+        else if (n <= 16) jac_sweeps += multi_warp_jacobi<16, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
+        else if (n <= 24) jac_sweeps += multi_warp_jacobi<24, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
+        else jac_sweeps += multi_warp_jacobi<32, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
       }
       __syncthreads();
     } else {
