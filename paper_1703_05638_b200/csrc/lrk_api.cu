@@ -349,10 +349,27 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
     batch.ngroups = G;
   }
   const int slot = adjoint ? 1 : 0;
+  const char* dump = std::getenv("LRK_DUMP_CORES");  // diagnostics (tools/jacobi_bench)
+  const int64_t dsz = (int64_t)nflush * (1 + 32 * 33);
+  WS(double, cd, tag + "cdump", dump ? dsz : 1);
+  if (dump) {
+    CK(cudaMemsetAsync(cd, 0, dsz * sizeof(double), s));
+    for (int g = 0; g < batch.ngroups; ++g) batch.g[g].cdump = g == 0 ? cd : nullptr;
+  }
   if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
   CK(launch_sweep(batch, s));
   if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
   ++c->launches;
+  if (dump) {
+    std::vector<double> h(dsz);
+    CK(cudaMemcpyAsync(h.data(), cd, dsz * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const std::string path = std::string(dump) + (adjoint ? ".bwd" : ".fwd");
+    if (FILE* fp = std::fopen(path.c_str(), "wb")) {
+      std::fwrite(h.data(), sizeof(double), h.size(), fp);
+      std::fclose(fp);
+    }
+  }
   o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
   o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
   return LRK_OK;

@@ -57,6 +57,70 @@ struct PartTab {
   }
 };
 
+// ------------------------------------------------ fast fp64 special functions
+// The library sqrt / rsqrt / division of fp64 cost ~75-210 cycles of
+// dependent latency on sm_100a (tools/lat_bench.cu); the MUFU seeds plus
+// Newton steps below cost ~40-50 and are accurate to the last bit or two in
+// the normal range (no denormal / inf handling: callers keep operands normal).
+// out-of-range fallbacks: one out-of-line copy each (keeps callers compact)
+static __device__ __noinline__ double rcp_slow(double x) { return 1.0 / x; }
+static __device__ __noinline__ double rsqrt_slow(double x) { return rsqrt(x); }
+static __device__ __noinline__ double sqrt_slow(double x) { return sqrt(x); }
+__device__ __forceinline__ double rcp_fast(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-300 && ax < 1e300)) return rcp_slow(x);  // denormal / huge / 0 / inf / nan
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  if (!(x > 1e-300 && x < 1e300)) return rsqrt_slow(x);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+// sqrt(x), x >= 0
+__device__ __forceinline__ double sqrt_fast(double x) {
+  if (!(x > 1e-300 && x < 1e300)) return sqrt_slow(x);
+  return x * rsqrt_fast(x);
+}
+// Unchecked (branch-free) variants for operands known to be normal and in
+// range (e.g. after an exact power-of-two rescale): no slow-path branch, so
+// unrolled independent calls overlap instead of serialising at each branch.
+__device__ __forceinline__ double rcp_u(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_u(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+// sqrt for x >= 0 in range or exactly 0
+__device__ __forceinline__ double sqrt_u(double x) {
+  const double r = x * rsqrt_u(x);
+  return x > 0.0 ? r : 0.0;
+}
+// 2^e exactly (|e| < 1023)
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+// floor(log2(x)) for a normal positive x
+__device__ __forceinline__ int ilog2_normal(double x) {
+  return (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023;
+}
+
 // ------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -423,10 +487,13 @@ __device__ __forceinline__ int rank_cut_dev(const double* s, int n, double eps0,
   const double thr = eps0 * sqrt(acc);
   int keep = 0;  // searchsorted(-tail, -thr, 'left') over indices 0..n-1
   acc = 0.0;
+  // sqrt(acc) > thr decided on squares; the IEEE sqrt only inside a guard
+  // band around thr^2 (keeps the exact decision, no sqrt latency per step)
+  const double thr2 = thr * thr, hi2 = thr2 * (1.0 + 1e-13), lo2 = thr2 * (1.0 - 1e-13);
   for (int i = n - 1; i >= 0; --i) {
     const double si = s[i] < floor_v ? 0.0 : s[i];
     acc += si * si;
-    if (sqrt(acc) > thr) { keep = i + 1; break; }
+    if (acc > hi2 || (acc >= lo2 && sqrt(acc) > thr)) { keep = i + 1; break; }
   }
   if (keep > nnz) keep = nnz;
   if (r_max >= 0 && keep > r_max) keep = r_max;

@@ -47,10 +47,10 @@ __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, 
     if (sig == 0.0) {
       t = 0.0; beta = alpha; scale = 0.0;
     } else {
-      const double nrm = sqrt(alpha * alpha + sig);
+      const double nrm = sqrt_fast(alpha * alpha + sig);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      t = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
+      t = (beta - alpha) * rcp_fast(beta);
+      scale = rcp_fast(alpha - beta);
     }
     // w_k = x_jk + scale * (x_j . x_k)  for k > j  (v_i = scale x_ij, v_j = 1)
     double f[Q];
@@ -381,7 +381,7 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
           }
           t = (double)tf;
           const double t2 = t * t;
-          c = (t2 < 1e-8) ? 1.0 - t2 * (0.5 - 0.375 * t2) : rsqrt(1.0 + t2);
+          c = (t2 < 1e-8) ? 1.0 - t2 * (0.5 - 0.375 * t2) : rsqrt_u(1.0 + t2);
           s = c * t;
           rot = true;
         }
@@ -406,7 +406,7 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
     for (int o = 16; o > 0; o >>= 1) maxcos2 = fmax(maxcos2, __shfl_xor_sync(full, maxcos2, o));
     if (!rotated || maxcos2 <= 1e-16) break;
   }
-  double sv = own ? sqrt(colnorm()) : 0.0;
+  double sv = own ? sqrt_fast(colnorm()) : 0.0;
   int rk = 0;
   for (int j = 0; j < n; ++j) {
     const double sj = __shfl_sync(full, sv, j);
@@ -415,7 +415,7 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
   if (own) {
     perm[rk] = lane;
     s_sorted[rk] = sv;
-    const double inv = sv > 0.0 ? 1.0 / sv : 0.0;
+    const double inv = sv > 0.0 ? rcp_fast(sv) : 0.0;
 #pragma unroll
     for (int i = 0; i < NJ; ++i)
       if (i < n) {
@@ -592,10 +592,10 @@ __device__ __forceinline__ void pivoted_qr_reg(double (&A)[Q][Q], int q, double 
       if (i == j) alpha = A[i][j];
     }
     if (sig == 0.0) continue;
-    const double nrm = sqrt(alpha * alpha + sig);
+    const double nrm = sqrt_fast(alpha * alpha + sig);
     const double beta = alpha >= 0.0 ? -nrm : nrm;
-    const double tau = (beta - alpha) / beta;
-    const double sc = 1.0 / (alpha - beta);
+    const double tau = (beta - alpha) * rcp_fast(beta);
+    const double sc = rcp_fast(alpha - beta);
     double v[Q];
 #pragma unroll
     for (int i = 0; i < Q; ++i) v[i] = (i == j) ? 1.0 : ((i > j && i < q) ? A[i][j] * sc : 0.0);
@@ -670,10 +670,10 @@ __device__ __forceinline__ void warp_qr_cols(double (&a)[NJ], int n, double* __r
     }
     double beta = alpha, t = 0.0, scale = 0.0;
     if (sig != 0.0) {
-      const double nrm = sqrt(alpha * alpha + sig);
+      const double nrm = sqrt_fast(alpha * alpha + sig);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      t = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
+      t = (beta - alpha) * rcp_fast(beta);
+      scale = rcp_fast(alpha - beta);
     }
     // v_i = x_i * scale (i > j), v_j = 1
     if (lane > j && lane < n) {
@@ -739,10 +739,10 @@ __device__ __forceinline__ void warp_hh_regs(double (&x)[ROWS][Q], int q, double
     const double alpha = xr[j], sig = s[j];
     double beta = alpha, t = 0.0, scale = 0.0;
     if (sig != 0.0) {
-      const double nrm = sqrt(alpha * alpha + sig);
+      const double nrm = sqrt_fast(alpha * alpha + sig);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      t = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
+      t = (beta - alpha) * rcp_fast(beta);
+      scale = rcp_fast(alpha - beta);
     }
     double f[Q];
 #pragma unroll
@@ -969,30 +969,27 @@ __device__ __forceinline__ int multi_warp_jacobi(const double* __restrict__ Ain,
       // reduce identical values in the same order
       const double g = xsum(g0 + g1);
       const double al = lo ? nrm : np, be = lo ? np : nrm;
-      double c = 1.0, sl = 0.0, t = 0.0;
-      bool rot = false;
-      if (act && al > tiny && be > tiny) {
-        const double g2 = g * g, ab = al * be;
-        if (g2 > 1e-16 * ab) big = true;
-        if (g2 > tol2 * ab) {
-          const double d = be - al;
-          const double m = fmax(fabs(d), fabs(g));
-          const int e = ((int)(__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
-          const double sc = __longlong_as_double((long long)(1023 - e) << 52);
-          const float df = (float)(d * sc), gf = (float)(g * sc);
-          float tf;
-          if (fabsf(gf) < 1e-4f * fabsf(df)) tf = __fdividef(gf, df);
-          else {
-            tf = __fdividef(2.0f * gf, fabsf(df) + sqrtf(df * df + 4.0f * gf * gf));
-            if (df < 0.0f) tf = -tf;
-          }
-          t = (double)tf;
-          const double t2 = t * t;
-          c = (t2 < 1e-8) ? 1.0 - t2 * (0.5 - 0.375 * t2) : rsqrt(1.0 + t2);
-          sl = lo ? -c * t : c * t;
-          rot = true;
-        }
-      }
+      // rotation parameters computed without branches (selects only): the
+      // tangent in fp32 after an exact power-of-two rescale (only its
+      // convergence effect depends on its accuracy), c in fp64 so that
+      // c^2 + s^2 = 1 to working precision; t = 0 gives c = 1, s = 0 exactly
+      const double g2 = g * g, ab = al * be;
+      const bool ok = act && al > tiny && be > tiny;
+      big = big || (ok && g2 > 1e-16 * ab);
+      const bool rot = ok && g2 > tol2 * ab;
+      const double d = be - al;
+      int e = ilog2_normal(fmax(fmax(fabs(d), fabs(g)), 1e-300));
+      e = e > 1000 ? 1000 : e;
+      const double scl = pow2i(-e);
+      const float df = (float)(d * scl), gf = (float)(g * scl);
+      const float hyp = df * df + 4.0f * gf * gf;
+      const float tb = __fdividef(2.0f * gf, fabsf(df) + hyp * rsqrtf(hyp));
+      const float tf = (fabsf(gf) < 1e-4f * fabsf(df)) ? __fdividef(gf, df) : (df < 0.0f ? -tb : tb);
+      const double t = rot ? (double)tf : 0.0;
+      const double t2 = t * t;
+      const double cser = 1.0 - t2 * (0.5 - 0.375 * t2);
+      const double c = (t2 < 1e-8) ? cser : rsqrt_u(1.0 + t2);
+      const double sl = lo ? -c * t : c * t;
       // unconditional update (c = 1, sl = 0 leaves a column bit-identical):
       // shuffles outside data-dependent branches compile to plain SHFL
 #pragma unroll
@@ -1001,16 +998,15 @@ __device__ __forceinline__ int multi_warp_jacobi(const double* __restrict__ Ain,
         const double vp = __shfl_sync(full, v[k], p & 31);
         v[k] = c * v[k] + sl * vp;
       }
-      if (rot) {
-        nrm = lo ? (al - t * g) : (be + t * g);
-        rotated = true;
-      }
+      const double nn = lo ? (al - t * g) : (be + t * g);
+      nrm = rot ? nn : nrm;
+      rotated = rotated || rot;
     }
     ++nsweep;
     if (!__any_sync(full, rotated) || !__any_sync(full, big)) break;
   }
   const double nfin = xsum(colnorm_part());  // every lane takes part in the barrier
-  const double sv = own ? sqrt(nfin) : 0.0;
+  const double sv = own ? sqrt_fast(nfin) : 0.0;
   int rk = 0;
   for (int j = 0; j < n; ++j) {
     const double sj = __shfl_sync(full, sv, j);
@@ -1021,7 +1017,7 @@ __device__ __forceinline__ int multi_warp_jacobi(const double* __restrict__ Ain,
       perm[rk] = lane;
       s_sorted[rk] = sv;
     }
-    const double inv = sv > 0.0 ? 1.0 / sv : 0.0;
+    const double inv = sv > 0.0 ? rcp_fast(sv) : 0.0;
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
       const int i = row0 + k;

@@ -497,6 +497,11 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
         sCore[j + i * 33] = v;  // K^T: Jacobi on the rows of the core
       }
       __syncthreads();
+      if (a.cdump && cta == 0) {  // diagnostics: the cores the Jacobi sees
+        double* d = a.cdump + (int64_t)f * (1 + 32 * 33);
+        if (tid == 0) d[0] = n;
+        for (int idx = tid; idx < 32 * 33; idx += NT) d[1 + idx] = sCore[idx];
+      }
       if (warp < 4) {  // 4-warp register Jacobi (named barrier 1), sScr = gbuf
         // K^T = Vk S Uk^T: the routine's left vectors are K's right ones
         if (n <= 8) jac_sweeps += multi_warp_jacobi<8, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
