@@ -318,6 +318,7 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   a.ftz = std::getenv("LRK_FTZ") ? std::atof(std::getenv("LRK_FTZ")) : 0.0;
   WS(long long, dbg, tag + "dbg", 20);
   a.dbg = std::getenv("LRK_DEBUG") ? dbg : nullptr;
+  a.nopipe = std::getenv("LRK_NOPIPE") ? 1 : 0;
   o.dbg = dbg;
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
   if (G > 1) {
@@ -650,6 +651,7 @@ int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t 
   a.ftz = 0.0;
   WS(long long, dbg, tag + "dbg", 20);
   a.dbg = std::getenv("LRK_DEBUG") ? dbg : nullptr;
+  a.nopipe = std::getenv("LRK_NOPIPE") ? 1 : 0;
   o.dbg = dbg;
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
   const double m = c->op.m_scale;

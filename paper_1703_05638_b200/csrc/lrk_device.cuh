@@ -43,6 +43,27 @@ __device__ __forceinline__ void group_barrier(unsigned* bar, int ncta, bool sys 
   __syncthreads();
 }
 
+// Split form of group_barrier for a barrier whose arrival and wait happen at
+// different points (one thread each, after the arriving threads have synced):
+// arrive returns the generation to wait on.
+__device__ __forceinline__ unsigned group_arrive(unsigned* bar, int ncta, bool sys) {
+  volatile unsigned* vgen = bar + 1;
+  const unsigned gen = *vgen;
+  if (sys) __threadfence_system(); else __threadfence();
+  const unsigned arrived = atomicAdd(bar, 1u);
+  if (arrived == (unsigned)ncta - 1u) {
+    atomicExch(bar, 0u);
+    if (sys) __threadfence_system(); else __threadfence();
+    atomicAdd(bar + 1, 1u);
+  }
+  return gen;
+}
+__device__ __forceinline__ void group_wait(unsigned* bar, unsigned gen, bool sys) {
+  volatile unsigned* vgen = bar + 1;
+  while (*vgen == gen) { __nanosleep(20); }
+  if (sys) __threadfence_system(); else __threadfence();
+}
+
 // Per-CTA partial buffers of a (possibly sharded) sweep: region k (0..2) of
 // global CTA c lives at p[c / ncta] + (k * ncta + c % ncta) * stride.
 struct PartTab {

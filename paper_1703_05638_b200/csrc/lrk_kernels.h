@@ -40,6 +40,7 @@ struct SweepArgs {
   int ncta;
   long long* dbg;          // optional per-phase cycle counters (10), CTA 0
   double* cdump;           // optional (LRK_DUMP_CORES): per flush [n, core 32x33] from CTA 0
+  int nopipe;              // 1: no overlap of the next flush's phase 1 with the Jacobi (LRK_NOPIPE)
   // external-trajectory mode (physical-space solvers, e.g. convection-diffusion):
   // when yext != NULL the buffered columns are read from yext (column j = the
   // j-th step processed by this launch) instead of the spectral recurrence.

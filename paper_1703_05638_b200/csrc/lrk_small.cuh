@@ -500,14 +500,23 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
 // sectors) and the B-operand = B[k+t, g]; U k-steps of loads are issued
 // before their DMMAs.  Per-warp partials meet in wbuf (NWARP*na*nb shared
 // doubles) and are summed in warp order into out[i*nb + j].
-template <int NI>
+// Warp-group synchronisation: the whole CTA (GW == NWARP) or the GW warps
+// starting at warp WOFF on named barrier 2 (barrier 1 belongs to the Jacobi).
+template <int GW, int WOFF>
+__device__ __forceinline__ void grp_sync() {
+  if constexpr (GW == NWARP) __syncthreads();
+  else asm volatile("bar.sync 2, %0;" ::"r"(GW * 32));
+}
+
+// Executed by the GW warps [WOFF, WOFF+GW) (default: the whole CTA).
+template <int NI, int GW = NWARP, int WOFF = 0>
 __device__ __forceinline__ void cta_tn_dmma(const double* __restrict__ A, int64_t lda, int na,
                                             const double* __restrict__ B, int64_t ldb, int nb,
                                             int nrows, double* __restrict__ out,
                                             double* __restrict__ wbuf) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) - WOFF;
   const int g = lane >> 2, t = lane & 3;
-  const int chunk = (((nrows + NWARP - 1) / NWARP) + 3) & ~3;
+  const int chunk = (((nrows + GW - 1) / GW) + 3) & ~3;
   const int r0 = warp * chunk;
   const int r1 = min(nrows, r0 + chunk);
   double acc[NI][2];
@@ -539,14 +548,14 @@ __device__ __forceinline__ void cta_tn_dmma(const double* __restrict__ A, int64_
       const int ii = 8 * i + g, jj = 2 * t + h;
       if (ii < na && jj < nb) wbuf[(warp * na + ii) * nb + jj] = acc[i][h];
     }
-  __syncthreads();
-  for (int o = threadIdx.x; o < na * nb; o += NT) {
+  grp_sync<GW, WOFF>();
+  for (int o = threadIdx.x - 32 * WOFF; o < na * nb; o += 32 * GW) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < NWARP; ++w) s += wbuf[w * na * nb + o];
+    for (int w = 0; w < GW; ++w) s += wbuf[w * na * nb + o];
     out[o] = s;
   }
-  __syncthreads();
+  grp_sync<GW, WOFF>();
 }
 
 // Column-pivoted Householder QR of the q x q (q <= Q) matrix A held in

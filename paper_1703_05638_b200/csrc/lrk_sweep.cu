@@ -43,13 +43,19 @@ namespace lrk {
 namespace {
 constexpr int NINT = NMAX + PMAX + 8;
 
+// a warp group: GW warps starting at warp WOFF
+template <int GW_, int WOFF_>
+struct Grp {
+  static constexpr int GW = GW_, WOFF = WOFF_;
+};
+
 struct Small {  // offsets inside the small region, sized by (cap, pc)
   int C, Part, Yn, R, Rp, X, G, I, Qs, Rb, Tau, TauT, Cn, Sig, S, Red, Tmp, Scr, Uc, Vc, Core, Int,
       total;
   __host__ __device__ Small(int cap, int pc) {
     int o = 0;
     C = o; o += cap * pc;
-    Part = o; o += cap * pc + pc + 8;
+    Part = o; o += (cap + pc + 1) * pc + 8;  // pipelined partials: [U, Q~] rows
     Yn = o; o += pc;
     R = o; o += pc * pc;
     Rp = o; o += pc * pc;
@@ -285,22 +291,28 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       }
     __syncthreads();
   }
-  for (int f = a.flush0; f < a.flush1; ++f) {
-    const int start = f * p;
-    const int pc = (n_t - start) < p ? (n_t - start) : p;
-    // ---------------- phase 1: buffered columns (row-local) + projections
+  // Phase 1 of a flush (buffered columns + projections + norms -> partial
+  // slot 1).  Executed by the whole CTA, or — pipelined — by warps 4..7 for
+  // the NEXT flush while warps 0..3 run the core Jacobi: the projection is
+  // then taken against [U, Q~] of the current flush (rows nU + nQ), and the
+  // next flush maps it to the updated pane with the core's vectors.
+  auto phase1 = [&](auto grp, int fi, int nU, int nQ) {
+    constexpr int GW = decltype(grp)::GW, WOFF = decltype(grp)::WOFF;
+    const int gt = tid - 32 * WOFF;
+    const int st = fi * p;
+    const int pcn = (n_t - st) < p ? (n_t - st) : p;
     if (a.yext) {
-      const double* ye = a.yext + r0 + (int64_t)(start - a.flush0 * p) * a.ldyext;
-      for (int i = tid; i < m_loc; i += NT) {
+      const double* ye = a.yext + r0 + (int64_t)(st - a.flush0 * p) * a.ldyext;
+      for (int i = gt; i < m_loc; i += 32 * GW) {
 #pragma unroll
         for (int s = 0; s < Q; ++s)
-          if (s < pc) Yl[i + (int64_t)s * ldy] = ye[i + (int64_t)s * a.ldyext];
+          if (s < pcn) Yl[i + (int64_t)s * ldy] = ye[i + (int64_t)s * a.ldyext];
       }
     } else {
       int ks[Q];
 #pragma unroll
-      for (int s = 0; s < Q; ++s) ks[s] = a.adjoint ? (n_t - 1 - (start + s)) : (start + s);
-      for (int i = tid; i < m_loc; i += NT) {
+      for (int s = 0; s < Q; ++s) ks[s] = a.adjoint ? (n_t - 1 - (st + s)) : (st + s);
+      for (int i = gt; i < m_loc; i += 32 * GW) {
         double acc[Q];
 #pragma unroll
         for (int s = 0; s < Q; ++s) acc[s] = 0.0;
@@ -310,14 +322,14 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
           const double* w2 = a.W2 + (int64_t)j * a.ldw2;
 #pragma unroll
           for (int s = 0; s < Q; ++s)
-            if (s < pc) acc[s] += b * w2[ks[s]];
+            if (s < pcn) acc[s] += b * w2[ks[s]];
         }
         const double tv = th[i];
         const double rs = rsc ? rsc[i] : 1.0;
         double y = yp[i];
 #pragma unroll
         for (int s = 0; s < Q; ++s) {
-          if (s < pc) {
+          if (s < pcn) {
             y = tv * y + rs * acc[s];
             if (fabs(y) < a.ftz) y = 0.0;
             Yl[i + (int64_t)s * ldy] = y;
@@ -326,29 +338,80 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
         yp[i] = y;
       }
     }
-    __syncthreads();
-    if (r > 0) proj(r, pc, sPart);
+    grp_sync<GW, WOFF>();
+    // projections straight into this CTA's partial slot (rows nU of U, then
+    // nQ of Q~), squared norms after them
+    if (nU > 0) {
+      if (nU <= 32 && GW * nU * pcn <= wcap)
+        cta_tn_dmma<4, GW, WOFF>(Ul, ldu, nU, Yl, ldy, pcn, m_loc, part1, wbuf);
+      else if (nU <= 64 && GW * nU * pcn <= wcap)
+        cta_tn_dmma<8, GW, WOFF>(Ul, ldu, nU, Yl, ldy, pcn, m_loc, part1, wbuf);
+      else if constexpr (GW == NWARP)
+        cta_tn(Ul, ldu, nU, Yl, ldy, pcn, m_loc, part1, sScr);
+    }
+    if (nQ > 0) cta_tn_dmma<2, GW, WOFF>(Ql, ldq, nQ, Yl, ldy, pcn, m_loc, part1 + nU * pcn, wbuf);
     {
       double v[Q];
 #pragma unroll
       for (int s = 0; s < Q; ++s) v[s] = 0.0;
-      for (int i = tid; i < m_loc; i += NT) {
+      for (int i = gt; i < m_loc; i += 32 * GW) {
 #pragma unroll
         for (int s = 0; s < Q; ++s)
-          if (s < pc) { const double y = Yl[i + (int64_t)s * ldy]; v[s] += y * y; }
+          if (s < pcn) { const double y = Yl[i + (int64_t)s * ldy]; v[s] += y * y; }
       }
-      block_sum<Q>(v, sRed, sTmp);
-      if (tid < pc) sPart[r * pc + tid] = sTmp[tid];
+#pragma unroll
+      for (int s = 0; s < Q; ++s) v[s] = warp_sum(v[s]);
+      double* red = sRed;  // GW * Q <= NWARP * PMAX doubles (unused by the Jacobi warps)
+      if ((tid & 31) == 0) {
+#pragma unroll
+        for (int s = 0; s < Q; ++s) red[(tid / 32 - WOFF) * Q + s] = v[s];
+      }
+      grp_sync<GW, WOFF>();
+      if (gt < pcn) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < GW; ++w) sum += red[w * Q + gt];
+        part1[(nU + nQ) * pcn + gt] = sum;
+      }
+      grp_sync<GW, WOFF>();
     }
-    __syncthreads();
-    for (int i = tid; i < r * pc + pc; i += NT) part1[i] = sPart[i];
-    LRK_TSTAMP(0);
-    group_barrier(a.gbar, ncta_all, sysf);
+  };
+  // pipelining state: the next flush's phase 1 was done during the Jacobi
+  bool have_next = false;
+  int rP = 0, ldcP = 0;  // rows of its basis [U, Q~]; leading dim of the core vectors
+  for (int f = a.flush0; f < a.flush1; ++f) {
+    const int start = f * p;
+    const int pc = (n_t - start) < p ? (n_t - start) : p;
+    int rows_in = r;
+    if (!have_next) {
+      // ---------------- phase 1 (whole CTA) + barrier 1
+      phase1(Grp<NWARP, 0>{}, f, r, 0);
+      LRK_TSTAMP(0);
+      group_barrier(a.gbar, ncta_all, sysf);
+    } else {
+      rows_in = rP;
+      LRK_TSTAMP(0);
+      if (tid == 0) group_wait(a.gbar, (unsigned)iFlag[3], sysf);
+      __syncthreads();
+    }
     LRK_TSTAMP(1);
     // ---------------- phase 2: block CGS2 against the orthonormal pane
-    reduce_partials(tab, 0, ncta_all, r * pc + pc, sPart);
-    for (int i = tid; i < pc; i += NT) sYn[i] = sPart[r * pc + i];
-    for (int i = tid; i < r * pc; i += NT) sC[i] = sPart[i];
+    reduce_partials(tab, 0, ncta_all, rows_in * pc + pc, sPart);
+    for (int i = tid; i < pc; i += NT) sYn[i] = sPart[rows_in * pc + i];
+    if (!have_next) {
+      for (int i = tid; i < r * pc; i += NT) sC[i] = sPart[i];
+    } else {
+      // C = W^T P: the projection onto [U_prev, Q~_prev] mapped to the pane
+      // U = [U_prev, Q~_prev] W (W = the previous core's first r vectors)
+      const double* Wp = small + L.Uc;
+      for (int o = tid; o < r * pc; o += NT) {
+        const int i = o / pc, sI = o - i * pc;
+        double acc = 0.0;
+        for (int k = 0; k < rP; ++k) acc += Wp[k + i * ldcP] * sPart[k * pc + sI];
+        sC[o] = acc;
+      }
+    }
+    have_next = false;
     __syncthreads();
     LRK_TSTAMP(9);
     if (r > 0) {
@@ -501,15 +564,24 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
         double* d = a.cdump + (int64_t)f * (1 + 32 * 33);
         if (tid == 0) d[0] = n;
         for (int idx = tid; idx < 32 * 33; idx += NT) d[1 + idx] = sCore[idx];
+        __syncthreads();
       }
+      // the next flush's phase 1 overlaps the Jacobi when its projection
+      // fits the tensor-core path of the 4-warp group
+      const bool pipe = !a.nopipe && (f + 1 < a.flush1) && (n <= 32) && (pc <= 4) &&
+                        (NWARP / 2) * n * p <= wcap;
       if (warp < 4) {  // 4-warp register Jacobi (named barrier 1), sScr = gbuf
         // K^T = Vk S Uk^T: the routine's left vectors are K's right ones
         if (n <= 8) jac_sweeps += multi_warp_jacobi<8, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
         else if (n <= 16) jac_sweeps += multi_warp_jacobi<16, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
         else if (n <= 24) jac_sweeps += multi_warp_jacobi<24, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
         else jac_sweeps += multi_warp_jacobi<32, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
+      } else if (pipe) {
+        phase1(Grp<NWARP / 2, NWARP / 2>{}, f + 1, r, pc);
+        if (tid == 32 * (NWARP / 2)) iFlag[3] = (int)group_arrive(a.gbar, ncta_all, sysf);
       }
       __syncthreads();
+      if (pipe) { have_next = true; rP = n; ldcP = ldc; }
     } else {
       double* Aj = gscr + 2 * (int64_t)ncta_all * PMAX * PMAX;
       double* Vj = Aj + (int64_t)NMAX * NMAX;
