@@ -401,7 +401,7 @@ int precond_apply(lrk_ctx* c, const double* b, double* x, cudaStream_t s, double
 int step_apply(lrk_ctx* c, const double* x, double* y, bool adjoint, cudaStream_t s) {
   StencilArgs a = make_stencil(c->op, adjoint);
   a.X = x; a.ldx = c->n_x; a.Y = y; a.ldy = c->n_x; a.ncols = 1;
-  stencil_kernel<<<dim3(grid1(c->n_x, 256, 1 << 30), 1), 256, 0, s>>>(a);
+  launch_stencil(a, s);
   CKL();
   ++c->launches;
   return LRK_OK;
@@ -500,13 +500,13 @@ int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, 
   StencilArgs a = make_stencil(c->op, adjoint);
   a.X = x; a.ldx = nx; a.Y = r; a.ldy = nx; a.ncols = 1; a.Bres = b; a.ldbres = nx;
   for (int it = 0; it < c->rich_it; ++it) {
-    stencil_kernel<<<dim3(grid1(nx, 256, 1 << 30), 1), 256, 0, s>>>(a);
+    launch_stencil(a, s);
     CKL();
     ++c->launches;
     TRY(precond_apply(c, r, x, s, 1.0));
   }
   if (flag) {
-    stencil_kernel<<<dim3(grid1(nx, 256, 1 << 30), 1), 256, 0, s>>>(a);
+    launch_stencil(a, s);
     CKL();
     resid_flag_kernel<<<296, 256, 0, s>>>(r, b, nx, STEP_RTOL * STEP_RTOL, part, cnt, flag);
     CKL();
@@ -537,7 +537,7 @@ int rich_setup(lrk_ctx* c, cudaStream_t s) {
   a.X = x; a.ldx = nx; a.Y = r; a.ldy = nx; a.ncols = 1; a.Bres = b; a.ldbres = nx;
   std::vector<double> res;
   for (int it = 0; it < 10; ++it) {
-    stencil_kernel<<<dim3(grid1(nx, 256, 1 << 30), 1), 256, 0, s>>>(a);
+    launch_stencil(a, s);
     CKL();
     double nr = 0.0;
     TRY(lrk_cgs2(c, nullptr, nx, 0, r, (int)nx, nullptr, &nr, s));
@@ -1242,16 +1242,24 @@ int lrk_dot(lrk_ctx* c, const lrk_lr* A, const lrk_lr* B, double* out, void* str
   if (A->n_x != B->n_x || A->n_t != B->n_t) return fail(c, LRK_ERR_SHAPE, "shape mismatch");
   if (A->r == 0 || B->r == 0) { *out = 0.0; return LRK_OK; }
   const int na = A->r, nb = B->r, nout = na * nb;
-  const int g1 = grid1(A->n_x, 4096, 2 * c->num_sms), g2 = grid1(A->n_t, 4096, 32);
+  // Gram blocks A1^T B1 (n_x rows) and A2^T B2 (n_t rows) on the FP64 tensor
+  // pipe, per-CTA partials reduced in parallel over the outputs, then the
+  // Hadamard sum (lowrank.py:163-168)
+  const int g1 = grid1(A->n_x, 4096, c->num_sms), g2 = grid1(A->n_t, 64, c->num_sms / 4);
+  const int gd = (nout + 255) / 256;
   WS(double, p1, "dot_p1", (int64_t)g1 * nout);
   WS(double, p2, "dot_p2", (int64_t)g2 * nout);
+  WS(double, pd, "dot_pd", gd);
   WS(double, res, "dot_res", 1);
-  gram_partial_kernel<<<g1, NT, 0, s>>>(A->W1, A->ld1, na, B->W1, B->ld1, nb, A->n_x, p1);
+  launch_gram(A->W1, A->ld1, na, B->W1, B->ld1, nb, A->n_x, p1, g1, s);
   CKL();
-  gram_partial_kernel<<<g2, NT, 0, s>>>(A->W2, A->ld2, na, B->W2, B->ld2, nb, A->n_t, p2);
+  launch_gram(A->W2, A->ld2, na, B->W2, B->ld2, nb, A->n_t, p2, g2, s);
   CKL();
-  dot_finalize_kernel<<<1, 256, 0, s>>>(p1, g1, p2, g2, nout, res);
+  dot_parts_kernel<<<gd, 256, 0, s>>>(p1, g1, p2, g2, nout, pd);
   CKL();
+  dot_sum_kernel<<<1, 32, 0, s>>>(pd, gd, res);
+  CKL();
+  c->launches += 4;
   CK(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return LRK_OK;
@@ -1314,15 +1322,17 @@ int lrk_operator_apply(lrk_ctx* c, const lrk_lr* Y, int adjoint, lrk_lr* out, vo
   const lrk_operator_desc& op = c->op;
   StencilArgs a = make_stencil(op, adjoint != 0);
   a.X = Y->W1; a.ldx = Y->ld1; a.Y = out->W1; a.ldy = out->ld1; a.ncols = r;
-  stencil_kernel<<<dim3(grid1(c->n_x, 256, 1 << 30), r), 256, 0, s>>>(a);
+  // (-M W1) into the second r columns in the same pass over W1
+  a.Ycopy = out->W1 + (int64_t)r * out->ld1; a.ldycopy = out->ld1; a.copy_scale = -op.m_scale;
+  launch_stencil(a, s);
   CKL();
-  // W2 copy into the first r columns; shift + (-M W1) into the second r
+  // W2 copy into the first r columns; shifted W2 into the second r
   scale_cols_kernel<<<dim3(grid1(Y->n_t, 256, 64), r), 256, 0, s>>>(Y->W2, Y->ld2, Y->n_t, nullptr,
                                                                      nullptr, r, 1.0, out->W2, out->ld2);
   CKL();
-  shift_kernel<<<dim3(grid1(std::max<int64_t>(c->n_x, Y->n_t), 256, 1 << 30), r), 256, 0, s>>>(
+  shift_kernel<<<dim3(grid1(Y->n_t, 256, 1 << 30), r), 256, 0, s>>>(
       Y->W2, Y->ld2, Y->n_t, r, adjoint, out->W2 + (int64_t)r * out->ld2, out->ld2, Y->W1, Y->ld1,
-      c->n_x, -op.m_scale, out->W1 + (int64_t)r * out->ld1, out->ld1);
+      0, -op.m_scale, out->W1 + (int64_t)r * out->ld1, out->ld1);
   CKL();
   out->r = 2 * r;
   return LRK_OK;
@@ -1488,14 +1498,14 @@ int lrk_cgs2(lrk_ctx* c, const double* Q, int64_t ldq, int k, double* w, int n, 
   WS(double, hacc, "cg_hacc", kk + 1);
   CK(cudaMemsetAsync(hacc, 0, (kk + 1) * sizeof(double), s));
   for (int pass = 0; pass < 2 && k > 0; ++pass) {
-    gram_partial_kernel<<<g, NT, 0, s>>>(Q, ldq, k, w, n, 1, n, part);
+    launch_gram(Q, ldq, k, w, n, 1, n, part, g, s);
     CKL();
     reduce_parts_kernel<<<grid1(k, 256, 64), 256, 0, s>>>(part, g, k, hp, hacc);
     CKL();
     sub_qh_kernel<<<grid1(n, 256, 2048), 256, 0, s>>>(Q, ldq, k, hp, w, n);
     CKL();
   }
-  gram_partial_kernel<<<g, NT, 0, s>>>(w, n, 1, w, n, 1, n, part);
+  launch_gram(w, n, 1, w, n, 1, n, part, g, s);
   CKL();
   reduce_parts_kernel<<<1, 256, 0, s>>>(part, g, 1, hacc + kk, nullptr);
   CKL();

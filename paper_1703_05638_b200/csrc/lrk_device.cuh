@@ -142,6 +142,16 @@ __device__ __forceinline__ int ilog2_normal(double x) {
   return (int)((__double_as_longlong(x) >> 52) & 0x7ff) - 1023;
 }
 
+// FP64 tensor-core MMA (sm_100a has no tcgen05 f64 kind; this is SASS DMMA):
+// D(8x8) += A(8x4, row) * B(4x8, col).  Fragments: a = A[g][t], b = B[t][g],
+// d0,d1 = D[g][2t], D[g][2t+1] with g = lane>>2, t = lane&3.  Not volatile:
+// the scheduler may interleave it with the loads feeding the next step.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
 // ------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -79,6 +79,162 @@ __global__ void stencil_kernel(StencilArgs a) {
   if (a.wind_field) lx += var_upwind(a, x, i, i1, i2, i3, plane);
   const double sx = a.m_scale * (xc + a.tau * lx);
   a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
+  if (a.Ycopy) a.Ycopy[i + (int64_t)c * a.ldycopy] = a.copy_scale * xc;
+}
+
+// Upwind terms from the six axis neighbours (xm[a] = x_{i - e_a}, xp[a] =
+// x_{i + e_a}, zero outside the domain: the Dirichlet data), same arithmetic
+// as var_upwind.
+__device__ __forceinline__ double upwind_nb(const StencilArgs& a, int i1, int i2, double xc,
+                                            const double (&xm)[3], const double (&xp)[3]) {
+  const double ih = 1.0 / a.h;
+  double acc = 0.0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    if (ax >= a.dim) break;
+    const double w = wind_at(a, ax, i1, i2);
+    acc += fabs(w) * ih * xc;
+    if (!a.adjoint) {
+      if (w > 0.0) acc -= w * ih * xm[ax];
+      if (w < 0.0) acc += w * ih * xp[ax];
+    } else {
+      const double wp = wind_at(a, ax, i1 + (ax == 0), i2 + (ax == 1));
+      if (wp > 0.0) acc -= wp * ih * xp[ax];
+      const double wm = wind_at(a, ax, i1 - (ax == 0), i2 - (ax == 1));
+      if (wm < 0.0) acc += wm * ih * xm[ax];
+    }
+  }
+  return acc;
+}
+
+// 2-D box stencil (5- or 9-point, optional upwind wind) on a shared-memory
+// tile: CTA = 32 x 8 threads, 32 x 32 outputs (4 rows per thread); the tile
+// with its one-node halo is staged once (coalesced rows, zero padding = the
+// Dirichlet data), so every input is read from HBM once; 16 B per output.
+constexpr int ST2 = 32;
+__global__ void __launch_bounds__(256) stencil2d_kernel(StencilArgs a) {
+  __shared__ double tile[ST2 + 2][ST2 + 3];
+  const int c = blockIdx.z;
+  const int n = a.n;
+  const int x0 = blockIdx.x * ST2, y0 = blockIdx.y * ST2;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const double* x = a.X + (int64_t)c * a.ldx;
+  for (int idx = tid; idx < (ST2 + 2) * (ST2 + 2); idx += 256) {
+    const int ly = idx / (ST2 + 2), lx = idx - ly * (ST2 + 2);
+    const int gx = x0 + lx - 1, gy = y0 + ly - 1;
+    tile[ly][lx] = (gx >= 0 && gx < n && gy >= 0 && gy < n) ? x[(int64_t)gy * n + gx] : 0.0;
+  }
+  __syncthreads();
+  double cf[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) cf[q] = a.coef[9 + q];
+  const int gx = x0 + tx;
+#pragma unroll
+  for (int rr = 0; rr < ST2 / 8; ++rr) {
+    const int ly = ty + 8 * rr, gy = y0 + ly;
+    if (gx >= n || gy >= n) continue;
+    double lx = 0.0;
+#pragma unroll
+    for (int d2 = 0; d2 < 3; ++d2)
+#pragma unroll
+      for (int d1 = 0; d1 < 3; ++d1) lx += cf[d2 * 3 + d1] * tile[ly + d2][tx + d1];
+    const double xc = tile[ly + 1][tx + 1];
+    if (a.wind_field) {
+      const double xm[3] = {tile[ly + 1][tx], tile[ly][tx + 1], 0.0};
+      const double xp[3] = {tile[ly + 1][tx + 2], tile[ly + 2][tx + 1], 0.0};
+      lx += upwind_nb(a, gx, gy, xc, xm, xp);
+    }
+    const double sx = a.m_scale * (xc + a.tau * lx);
+    const int64_t i = (int64_t)gy * n + gx;
+    a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
+    if (a.Ycopy) a.Ycopy[i + (int64_t)c * a.ldycopy] = a.copy_scale * xc;
+  }
+}
+
+// 3-D 7-point stencil (optional upwind wind): CTA = 32 x 8 threads over an
+// (x1, x2) tile, marching ST3Z planes along x3 with the x3 neighbours in
+// registers and the current plane (+ halo) in shared memory; 16 B per output.
+constexpr int ST3Z = 16;
+__global__ void __launch_bounds__(256) stencil3d7_kernel(StencilArgs a, int nzb) {
+  __shared__ double tile[8 + 2][32 + 3];
+  const int zb = blockIdx.z % nzb, c = blockIdx.z / nzb;
+  const int n = a.n;
+  const int64_t plane = (int64_t)n * n;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool in = gx < n && gy < n;
+  const double* x = a.X + (int64_t)c * a.ldx;
+  const int z0 = zb * ST3Z, z1 = min(n, z0 + ST3Z);
+  const double cxm = a.coef[12], cxp = a.coef[14], cym = a.coef[10], cyp = a.coef[16];
+  const double czm = a.coef[4], czp = a.coef[22], cc = a.coef[13];
+  const int64_t col = (int64_t)gy * n + gx;
+  // x3 neighbours in a register queue, loads issued two planes ahead (and
+  // the halo one plane ahead) so each thread keeps several loads in flight
+  auto ld = [&](int z) { return (in && z >= 0 && z < n) ? x[(int64_t)z * plane + col] : 0.0; };
+  double below = ld(z0 - 1), cur = ld(z0), a1 = ld(z0 + 1);
+  // halo slot of this thread (84 of the 340 tile entries; threads < 84)
+  const bool hh = tid < 2 * 34 + 2 * 8;
+  int hy = 0, hx = 0;
+  if (tid < 34) { hy = 0; hx = tid; }
+  else if (tid < 68) { hy = 9; hx = tid - 34; }
+  else if (tid < 76) { hy = tid - 68 + 1; hx = 0; }
+  else if (hh) { hy = tid - 76 + 1; hx = 33; }
+  const int hgx = x0 + hx - 1, hgy = y0 + hy - 1;
+  const bool hin = hh && hgx >= 0 && hgx < n && hgy >= 0 && hgy < n;
+  const int64_t hcol = (int64_t)hgy * n + hgx;
+  double hv = hin ? x[(int64_t)z0 * plane + hcol] : 0.0;
+  for (int z = z0; z < z1; ++z) {
+    const double a2 = ld(z + 2);
+    const double hvn = (hin && z + 1 < z1) ? x[(int64_t)(z + 1) * plane + hcol] : 0.0;
+    __syncthreads();  // the previous plane's tile is consumed
+    tile[ty + 1][tx + 1] = cur;
+    if (hh) tile[hy][hx] = hv;
+    __syncthreads();
+    if (in) {
+      const double xl = tile[ty + 1][tx], xr = tile[ty + 1][tx + 2];
+      const double xd = tile[ty][tx + 1], xu = tile[ty + 2][tx + 1];
+      double lx = cc * cur + cxm * xl + cxp * xr + cym * xd + cyp * xu + czm * below + czp * a1;
+      if (a.wind_field) {
+        const double xm[3] = {xl, xd, below};
+        const double xp[3] = {xr, xu, a1};
+        lx += upwind_nb(a, gx, gy, cur, xm, xp);
+      }
+      const double sx = a.m_scale * (cur + a.tau * lx);
+      const int64_t i = (int64_t)z * plane + col;
+      a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
+      if (a.Ycopy) a.Ycopy[i + (int64_t)c * a.ldycopy] = a.copy_scale * cur;
+    }
+    below = cur;
+    cur = a1;
+    a1 = a2;
+    hv = hvn;
+  }
+}
+
+// Launch the tiled kernel that fits the operator (2-D box; 3-D 7-point),
+// the generic one otherwise.  a.ncols columns.
+void launch_stencil(const StencilArgs& a, cudaStream_t s) {
+  const int n = a.n;
+  if (a.dim == 2) {
+    dim3 grid((n + ST2 - 1) / ST2, (n + ST2 - 1) / ST2, a.ncols);
+    stencil2d_kernel<<<grid, dim3(32, 8), 0, s>>>(a);
+    return;
+  }
+  bool seven = true;
+  for (int q = 0; q < 27; ++q) {
+    const int d3 = q / 9, d2 = (q / 3) % 3, d1 = q % 3;
+    const int nnz_axes = (d3 != 1) + (d2 != 1) + (d1 != 1);
+    if (nnz_axes > 1 && a.coef[q] != 0.0) seven = false;
+  }
+  if (seven) {
+    const int nzb = (n + ST3Z - 1) / ST3Z;
+    dim3 grid((n + 31) / 32, (n + 7) / 8, nzb * a.ncols);
+    stencil3d7_kernel<<<grid, dim3(32, 8), 0, s>>>(a, nzb);
+    return;
+  }
+  const int64_t nx = (int64_t)n * n * n;
+  stencil_kernel<<<dim3((unsigned)((nx + 255) / 256), a.ncols), 256, 0, s>>>(a);
 }
 
 // out2[:, c] = shift(W2[:, c]) (forward: down one row; adjoint: up one row)
@@ -325,6 +481,131 @@ __global__ void __launch_bounds__(NT) gram_partial_kernel(const double* A, int64
   }
 }
 
+// ---------------------------------------------- Gram partials (DMMA)
+// part[blockIdx.x * pstride + i*ldo + j] = sum over the CTA's rows of
+// A[:, i] B[:, j]  (i < na <= 8*TA, j < nb <= 8*TB).  Every warp streams its
+// own contiguous slice of the CTA's rows — each row of A and B is read once
+// from HBM, in 4-row k-steps with U steps of loads in flight — and
+// accumulates ALL TA x TB output tiles with m8n8k4 DMMA (lane (g,t) loads
+// A[k+t, 8i+g] and B[k+t, 8j+g]: every 32-byte sector fully used).  The
+// warp partials meet in shared memory in warp order (deterministic).
+// Bound: HBM for r <~ 40, the FP64 tensor pipe beyond (2 n r_a r_b flops
+// per 8 n (r_a + r_b) bytes).
+template <int TA, int TB>
+__global__ void __launch_bounds__(NT, 1)
+    gram_dmma_kernel(const double* __restrict__ A, int64_t lda, int na,
+                     const double* __restrict__ B, int64_t ldb, int nb, int64_t n,
+                     double* __restrict__ part, int ldo, int64_t pstride) {
+  // the 64-tile case splits the B tiles over two warp halves (64 accumulators
+  // per thread instead of 128: no spills); the halves read the same rows of A
+  // at the same time (L1 hits)
+  constexpr int WB = (TA * TB >= 64) ? 2 : 1;
+  constexpr int TBW = TB / WB;
+  constexpr int NS = NWARP / WB;  // row slices
+  __shared__ double buf[64 * 64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int half = warp % WB, slice = warp / WB;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = per * blockIdx.x, hi = min(n, lo + per);
+  const int64_t cnt = hi > lo ? hi - lo : 0;
+  const int64_t wchunk = (((cnt + NS - 1) / NS) + 3) & ~int64_t(3);
+  const int64_t w0 = lo + slice * wchunk, w1 = min(hi, w0 + wchunk);
+  // column 8i+g of A is Ab + i*la8 (one base pointer per operand)
+  const double* Ab = A + (int64_t)g * lda;
+  const double* Bb = B + (int64_t)(8 * TBW * half + g) * ldb;
+  const int64_t la8 = 8 * lda, lb8 = 8 * ldb;
+  const int jb0 = 8 * TBW * half;
+  double acc[TA][TBW][2];
+#pragma unroll
+  for (int i = 0; i < TA; ++i)
+#pragma unroll
+    for (int j = 0; j < TBW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  constexpr int U = (TA * TBW >= 32) ? 1 : (TA * TBW >= 8 ? 2 : 4);
+  // software pipeline: the fragments of the next U k-steps are loaded while
+  // the DMMAs of the current ones issue
+  double av[U][TA], bv[U][TBW];
+  auto load = [&](int64_t kb, double (&xa)[U][TA], double (&xb)[U][TBW]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = kb + 4 * u + t;
+      const bool ok = k < w1;
+#pragma unroll
+      for (int i = 0; i < TA; ++i) xa[u][i] = (ok && 8 * i + g < na) ? __ldg(Ab + i * la8 + k) : 0.0;
+#pragma unroll
+      for (int j = 0; j < TBW; ++j)
+        xb[u][j] = (ok && jb0 + 8 * j + g < nb) ? __ldg(Bb + j * lb8 + k) : 0.0;
+    }
+  };
+  if (w0 < w1) load(w0, av, bv);
+  for (int64_t k0 = w0; k0 < w1; k0 += 4 * U) {
+    double an[U][TA], bn[U][TBW];
+    load(k0 + 4 * U, an, bn);  // predicated off past w1
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < TA; ++i)
+#pragma unroll
+        for (int j = 0; j < TBW; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[u][i], bv[u][j]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int i = 0; i < TA; ++i) av[u][i] = an[u][i];
+#pragma unroll
+      for (int j = 0; j < TBW; ++j) bv[u][j] = bn[u][j];
+    }
+  }
+  // warp partials in slice order (each output element has exactly NS adds)
+  for (int sl = 0; sl < NS; ++sl) {
+    if (slice == sl) {
+#pragma unroll
+      for (int i = 0; i < TA; ++i)
+#pragma unroll
+        for (int j = 0; j < TBW; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ii = 8 * i + g, jj = jb0 + 8 * j + 2 * t + h;
+            if (ii < na && jj < nb) {
+              const double v = acc[i][j][h];
+              buf[ii * nb + jj] = (sl == 0) ? v : buf[ii * nb + jj] + v;
+            }
+          }
+    }
+    __syncthreads();
+  }
+  for (int o = threadIdx.x; o < na * nb; o += NT)
+    part[(int64_t)blockIdx.x * pstride + (int64_t)(o / nb) * ldo + (o % nb)] = buf[o];
+}
+
+template <int TA>
+static void gram_tb(int tb, const double* A, int64_t lda, int na, const double* B, int64_t ldb,
+                    int nb, int64_t n, double* part, int ldo, int64_t pstride, int nparts,
+                    cudaStream_t s) {
+  if (tb <= 1) gram_dmma_kernel<TA, 1><<<nparts, NT, 0, s>>>(A, lda, na, B, ldb, nb, n, part, ldo, pstride);
+  else if (tb <= 2) gram_dmma_kernel<TA, 2><<<nparts, NT, 0, s>>>(A, lda, na, B, ldb, nb, n, part, ldo, pstride);
+  else if (tb <= 4) gram_dmma_kernel<TA, 4><<<nparts, NT, 0, s>>>(A, lda, na, B, ldb, nb, n, part, ldo, pstride);
+  else gram_dmma_kernel<TA, 8><<<nparts, NT, 0, s>>>(A, lda, na, B, ldb, nb, n, part, ldo, pstride);
+}
+
+// nparts x (na*nb) partials of A^T B over n rows (row-major i*nb + j per
+// part); column blocks of 64 beyond the kernel's tile bound.
+void launch_gram(const double* A, int64_t lda, int na, const double* B, int64_t ldb, int nb,
+                 int64_t n, double* part, int nparts, cudaStream_t s) {
+  const int64_t pstride = (int64_t)na * nb;
+  for (int a0 = 0; a0 < na; a0 += 64)
+    for (int b0 = 0; b0 < nb; b0 += 64) {
+      const int ca = na - a0 < 64 ? na - a0 : 64, cb = nb - b0 < 64 ? nb - b0 : 64;
+      const int ta = (ca + 7) / 8, tb = (cb + 7) / 8;
+      const double* Ab = A + (int64_t)a0 * lda;
+      const double* Bb = B + (int64_t)b0 * ldb;
+      double* pb = part + (int64_t)a0 * nb + b0;
+      if (ta <= 1) gram_tb<1>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
+      else if (ta <= 2) gram_tb<2>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
+      else if (ta <= 4) gram_tb<4>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
+      else gram_tb<8>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
+    }
+}
+
 // dot = sum_{ij} G1[ij] * G2[ij] with G1, G2 the reduced partials.
 __global__ void dot_finalize_kernel(const double* p1, int n1, const double* p2, int n2, int nout,
                                     double* out) {
@@ -342,6 +623,40 @@ __global__ void dot_finalize_kernel(const double* p1, int n1, const double* p2, 
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    *out = s;
+  }
+}
+
+// lr_dot tail: G1 = sum of the n1 partials, G2 = sum of the n2 partials,
+// per-CTA partial of sum(G1 .* G2) (block order, deterministic) -> part;
+// dot_finalize_kernel(part, 1, ...) is not needed: dot_sum_kernel adds them.
+__global__ void __launch_bounds__(256) dot_parts_kernel(const double* __restrict__ p1, int n1,
+                                                        const double* __restrict__ p2, int n2,
+                                                        int nout, double* __restrict__ part) {
+  __shared__ double red[8];
+  const int o = blockIdx.x * 256 + threadIdx.x;
+  double prod = 0.0;
+  if (o < nout) {
+    double g1 = 0.0, g2 = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < n1; ++k) g1 += p1[(int64_t)k * nout + o];
+#pragma unroll 8
+    for (int k = 0; k < n2; ++k) g2 += p2[(int64_t)k * nout + o];
+    prod = g1 * g2;
+  }
+  prod = warp_sum(prod);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = prod;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
+}
+__global__ void dot_sum_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += part[k];
     *out = s;
   }
 }

@@ -23,9 +23,13 @@ struct StencilArgs {
   int adjoint;
   double w0[3];
   double h;
+  // optional fused copy: Ycopy[:, c] = copy_scale * X[:, c] (K.apply's -M W1 block)
+  double* Ycopy; int64_t ldycopy; double copy_scale;
 };
 
 __global__ void stencil_kernel(StencilArgs a);
+// tiled kernels (2-D box, 3-D 7-point) or the generic one; a.ncols columns
+void launch_stencil(const StencilArgs& a, cudaStream_t s);
 __global__ void shift_kernel(const double* W2, int64_t ld2, int n_t, int ncols, int adjoint,
                              double* out, int64_t ldo, const double* W1, int64_t ld1,
                              int64_t n_x, double neg_m, double* out1, int64_t ldo1);
@@ -60,6 +64,13 @@ __global__ void flip_apply_kernel(double* U, int64_t ldu, int64_t n_x, double* V
                                   int nparts);
 __global__ void gram_partial_kernel(const double* A, int64_t lda, int na, const double* B,
                                     int64_t ldb, int nb, int64_t n, double* part);
+// nparts x (na*nb) partials of A^T B over n rows on the FP64 tensor pipe
+// (row-major i*nb + j per part); launches enqueue on s.
+void launch_gram(const double* A, int64_t lda, int na, const double* B, int64_t ldb, int nb,
+                 int64_t n, double* part, int nparts, cudaStream_t s);
+__global__ void dot_parts_kernel(const double* p1, int n1, const double* p2, int n2, int nout,
+                                 double* part);
+__global__ void dot_sum_kernel(const double* part, int n, double* out);
 __global__ void dot_finalize_kernel(const double* p1, int n1, const double* p2, int n2, int nout,
                                     double* out);
 __global__ void reduce_parts_kernel(const double* p, int nparts, int nout, double* out,

@@ -428,14 +428,7 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
 }
 
 // ----------------------------------------------------------- DMMA helpers
-// FP64 tensor-core MMA (sm_100a has no tcgen05 f64 kind; this is SASS DMMA):
-// D(8x8) += A(8x4, row) * B(4x8, col).  Fragments: a = A[g][t], b = B[t][g],
-// d0,d1 = D[g][2t], D[g][2t+1] with g = lane>>2, t = lane&3.
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
+// (dmma884 lives in lrk_device.cuh)
 
 // In-place row update on the tensor pipe: rows [0, m) of X = [A (na cols) | B
 // (nb cols)] (column-major, lda/ldb) times W (n x rn, col-major ld ldw) are
