@@ -566,9 +566,11 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
         for (int idx = tid; idx < 32 * 33; idx += NT) d[1 + idx] = sCore[idx];
         __syncthreads();
       }
-      // the next flush's phase 1 overlaps the Jacobi when its projection
-      // fits the tensor-core path of the 4-warp group
-      const bool pipe = !a.nopipe && (f + 1 < a.flush1) && (n <= 32) && (pc <= 4) &&
+      // the next flush's phase 1 overlaps the Jacobi when the rows are
+      // resident (with global rows, C4-sized, the 4-warp row pass is longer
+      // than the Jacobi: 305 -> 377 ms per apply measured) and its
+      // projection fits the tensor-core path of the 4-warp group
+      const bool pipe = RES && !a.nopipe && (f + 1 < a.flush1) && (n <= 32) && (pc <= 4) &&
                         (NWARP / 2) * n * p <= wcap;
       if (warp < 4) {  // 4-warp register Jacobi (named barrier 1), sScr = gbuf
         // K^T = Vk S Uk^T: the routine's left vectors are K's right ones
