@@ -23,45 +23,60 @@ constexpr double NOISE_FLOOR = 1e-15;   // lowrank.py:20-22
 
 // ------------------------------------------------------------------ barrier
 // Sense-free generation barrier for the `ncta` CTAs of one group.
-// bar[0] = arrival count, bar[1] = generation.
-__device__ __forceinline__ void group_barrier(unsigned* bar, int ncta, bool sys = false) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    unsigned gen = *vgen;
-    if (sys) __threadfence_system(); else __threadfence();
-    unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == (unsigned)ncta - 1u) {
-      atomicExch(bar, 0u);
-      if (sys) __threadfence_system(); else __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) { __nanosleep(20); }
-    }
-    if (sys) __threadfence_system(); else __threadfence();
-  }
-  __syncthreads();
+// bar[0] = arrival count, bar[1] = generation.  PTX memory-model form: the
+// arrival is one acq_rel atomic (it releases the CTA's writes, cumulative
+// through the preceding bar.sync, and acquires the earlier arrivals'), the
+// last arriver resets the count and publishes the new generation with a
+// release store, the others poll it with acquire loads; no separate fences.
+// sys selects .sys scope (peer GPUs of a sharded sweep), else .gpu.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p, bool sys) {
+  unsigned v;
+  if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p, bool sys) {
+  unsigned v;
+  if (sys) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned* p, unsigned x, bool sys) {
+  unsigned v;
+  if (sys) asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "r"(x) : "memory");
+  else asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "r"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned x, bool sys) {
+  if (sys) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+  else asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned x, bool sys) {
+  if (sys) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+  else asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
 }
 
-// Split form of group_barrier for a barrier whose arrival and wait happen at
-// different points (one thread each, after the arriving threads have synced):
-// arrive returns the generation to wait on.
+// Split form for a barrier whose arrival and wait happen at different points
+// (one thread each, after the arriving threads have synced): arrive returns
+// the generation to wait on.
 __device__ __forceinline__ unsigned group_arrive(unsigned* bar, int ncta, bool sys) {
-  volatile unsigned* vgen = bar + 1;
-  const unsigned gen = *vgen;
-  if (sys) __threadfence_system(); else __threadfence();
-  const unsigned arrived = atomicAdd(bar, 1u);
+  const unsigned gen = ld_relaxed_u32(bar + 1, sys);
+  const unsigned arrived = atom_add_acq_rel_u32(bar, 1u, sys);
   if (arrived == (unsigned)ncta - 1u) {
-    atomicExch(bar, 0u);
-    if (sys) __threadfence_system(); else __threadfence();
-    atomicAdd(bar + 1, 1u);
+    st_relaxed_u32(bar, 0u, sys);
+    st_release_u32(bar + 1, gen + 1u, sys);
   }
   return gen;
 }
 __device__ __forceinline__ void group_wait(unsigned* bar, unsigned gen, bool sys) {
-  volatile unsigned* vgen = bar + 1;
-  while (*vgen == gen) { __nanosleep(20); }
-  if (sys) __threadfence_system(); else __threadfence();
+  while (ld_acquire_u32(bar + 1, sys) == gen) {
+  }
+}
+
+__device__ __forceinline__ void group_barrier(unsigned* bar, int ncta, bool sys = false) {
+  __syncthreads();
+  if (threadIdx.x == 0) group_wait(bar, group_arrive(bar, ncta, sys), sys);
+  __syncthreads();
 }
 
 // Per-CTA partial buffers of a (possibly sharded) sweep: region k (0..2) of

@@ -11,19 +11,20 @@
 namespace lrk {
 
 namespace {
-constexpr int TK = 16, GT = 128;
+constexpr int GT = 128;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile(
-      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
 }  // namespace
 
 // TM x TN CTA tile (64x64 or 32x32), 4 warps each owning a (TM/2)x(TN/2)
-// sub-tile of FI x FJ m8n8 fragments.
-template <int TM, int TN>
+// sub-tile of FI x FJ m8n8 fragments; K-step TK (the next K-step's global
+// loads are in flight while the current one computes, so a longer step hides
+// more of the load latency in the latency-bound small-grid case).
+template <int TM, int TN, int TK>
 __global__ void __launch_bounds__(GT) gemm_kernel(GemmArgs g) {
   constexpr int SP = TM + 4;  // padded k-major stride (conflict-free fragments)
   constexpr int SPN = TN + 4;
@@ -134,10 +135,11 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t s) {
   const int64_t tiles64 = (int64_t)((g.N + 63) / 64) * ((g.M + 63) / 64) * g.batch;
   if (tiles64 >= 2 * 148) {
     dim3 grid((g.N + 63) / 64, (g.M + 63) / 64, g.batch);
-    gemm_kernel<64, 64><<<grid, GT, 0, s>>>(g);
-  } else {  // under-filled grid (e.g. one 512^2 DST column): 4x more CTAs
+    gemm_kernel<64, 64, 16><<<grid, GT, 0, s>>>(g);
+  } else {  // under-filled grid (e.g. one 512^2 DST column): 4x more CTAs,
+            // K-step 32 (half the latency-bound K iterations)
     dim3 grid((g.N + 31) / 32, (g.M + 31) / 32, g.batch);
-    gemm_kernel<32, 32><<<grid, GT, 0, s>>>(g);
+    gemm_kernel<32, 32, 32><<<grid, GT, 0, s>>>(g);
   }
   return cudaGetLastError();
 }
