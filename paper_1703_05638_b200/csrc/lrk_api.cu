@@ -918,7 +918,7 @@ int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOu
     const char* names[20] = {"gen+proj1", "barrier1", "reduce2+sub2", "hh_local", "barrier3",
                              "stack_tail", "apply_q", "core+jacobi", "update", "reduce1",
                              "sub1+tn2", "barrier2", "rankcut", "stack_copy", "stack_qr",
-                             "stack_q", "stack_copy_warm", "x17", "x18", "x19"};
+                             "stack_q", "upd_U", "upd_V", "x18", "x19"};
     std::fprintf(stderr, "[lrk] cycles/flush (fwd | bwd):");
     for (int k = 0; k < 20; ++k)
       std::fprintf(stderr, " %s %lld|%lld", names[k], fd[k] / std::max(1, f.nflush),

@@ -457,30 +457,34 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
         if (row < m && k < n) av[h][kk] = (k < na) ? A[row + (int64_t)k * lda] : B[row + (int64_t)(k - na) * ldb];
       }
     }
+    // both row tiles advance together: 2*NT8 independent DMMA chains
+    double acc[2][NT8][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < NT8; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      if (kk * 4 >= n) break;
+      const int k = kk * 4 + t;
+#pragma unroll
+      for (int j = 0; j < NT8; ++j) {
+        const int col = j * 8 + g;
+        const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) dmma884(acc[h][j][0], acc[h][j][1], av[h][kk], b);
+      }
+    }
+    __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int row = (tile0 + h) * 8 + g;
-      double acc[NT8][2];
-#pragma unroll
-      for (int j = 0; j < NT8; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        if (kk * 4 >= n) break;
-        const int k = kk * 4 + t;
-#pragma unroll
-        for (int j = 0; j < NT8; ++j) {
-          const int col = j * 8 + g;
-          const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
-          dmma884(acc[j][0], acc[j][1], av[h][kk], b);
-        }
-      }
-      __syncwarp();
 #pragma unroll
       for (int j = 0; j < NT8; ++j) {
         const int c0 = j * 8 + 2 * t;
         if (row < m) {
-          if (c0 < rn) A[row + (int64_t)c0 * lda] = acc[j][0];
-          if (c0 + 1 < rn) A[row + (int64_t)(c0 + 1) * lda] = acc[j][1];
+          if (c0 < rn) A[row + (int64_t)c0 * lda] = acc[h][j][0];
+          if (c0 + 1 < rn) A[row + (int64_t)(c0 + 1) * lda] = acc[h][j][1];
         }
       }
     }

@@ -106,25 +106,41 @@ __device__ __forceinline__ void update_rows(double* __restrict__ A, int64_t lda,
 
 // Time rows: V'[t] = V[t, :r] W[:r, :rn] + [t visited at slot s] W[r+s, :rn]
 // (V points at this CTA's first time row t0; local row index tl = t - t0.)
+// One thread per output (t, c): the CTA's few time rows x rn columns run in
+// parallel (a thread per row would chain rn x r dependent loads); results are
+// staged in registers and written after a CTA barrier (the update is in place).
 template <int RA>
 __device__ __forceinline__ void update_time_rows(double* __restrict__ V, int64_t ldv, int r, const double* __restrict__ W,
                                  int ldw, int rn, int64_t t0, int64_t t1, int adjoint, int n_t,
                                  int start, int pc) {
-  for (int64_t t = t0 + threadIdx.x; t < t1; t += NT) {
-    const int64_t tl = t - t0;
-    int sel = adjoint ? (n_t - 1 - start) - (int)t : (int)t - start;
-    double acc[RA];
+  (void)RA;
+  const int nrow = (int)(t1 - t0);
+  if (rn <= 0) return;
+  constexpr int PER = 2;  // outputs per thread per chunk
+  const int rc = (PER * NT) / rn > 0 ? (PER * NT) / rn : 1;  // whole rows per chunk
+  for (int rb = 0; rb < nrow; rb += rc) {  // uniform trip count (CTA barriers inside)
+    const int nr = nrow - rb < rc ? nrow - rb : rc;
+    const int total = nr * rn;
+    double res[PER];
 #pragma unroll
-    for (int c = 0; c < RA; ++c) acc[c] = (sel >= 0 && sel < pc && c < rn) ? W[(r + sel) + c * ldw] : 0.0;
-    for (int k = 0; k < r; ++k) {
-      const double x = V[tl + (int64_t)k * ldv];
-#pragma unroll
-      for (int c = 0; c < RA; ++c)
-        if (c < rn) acc[c] += x * W[k + c * ldw];
+    for (int q = 0; q < PER; ++q) {
+      const int o = threadIdx.x + q * NT;
+      res[q] = 0.0;
+      if (o < total) {
+        const int tl = rb + o / rn, c = o % rn;
+        const int64_t t = t0 + tl;
+        const int sel = adjoint ? (n_t - 1 - start) - (int)t : (int)t - start;
+        double acc = (sel >= 0 && sel < pc) ? W[(r + sel) + c * ldw] : 0.0;
+        for (int k = 0; k < r; ++k) acc += V[tl + (int64_t)k * ldv] * W[k + c * ldw];
+        res[q] = acc;
+      }
     }
+    __syncthreads();  // every read of these rows precedes the in-place writes
 #pragma unroll
-    for (int c = 0; c < RA; ++c)
-      if (c < rn) V[tl + (int64_t)c * ldv] = acc[c];
+    for (int q = 0; q < PER; ++q) {
+      const int o = threadIdx.x + q * NT;
+      if (o < total) V[(rb + o / rn) + (int64_t)(o % rn) * ldv] = res[q];
+    }
   }
 }
 }  // namespace
@@ -624,7 +640,9 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     // ---------------- basis update in place: U' = [U, Q~] Uc[:, :rn]
     if (n <= 32 && rn <= 16) {
       update_rows_dmma<2>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      LRK_TSTAMP(16);
       update_time_rows<16>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
+      LRK_TSTAMP(17);
     } else if (n <= 32) {
       update_rows_dmma<4>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
       update_time_rows<32>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
