@@ -606,6 +606,35 @@ def test_emulated_nx_shards_hessian_c2_config():
     assert ctx.rank_trace[-1] == ctx.rank_trace[-2]
 
 
+def test_pipelined_phase1_matches_unpipelined(monkeypatch):
+    """The next flush's phase 1 on warps 4-7 during the Jacobi (projection onto
+    [U, Q~] mapped by C = W^T P) against the in-order flush (LRK_NOPIPE): same
+    rank traces, fields equal to rounding, at the C2 configuration."""
+    n_side, n_t = 256, 96
+    grid = lp.build_grid(n_side)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, "q1"), lp.build_time_grid(n_t))
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.make_sensor_subgrid(grid, 32),
+                            cov=cov, pol=lp.TruncationPolicy(1e-8, 32))
+    v = np.random.default_rng(61).standard_normal(grid.n_x)
+    a = ctx.apply(v)
+    tr_a = ctx.rank_trace[-1]
+    monkeypatch.setenv("LRK_NOPIPE", "1")
+    b = ctx.apply(v)
+    assert ctx.rank_trace[-1] == tr_a
+    assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
+    rng = np.random.default_rng(62)
+    rhs = lp.LowRankMat(rng.standard_normal((grid.n_x, 3)), rng.standard_normal((n_t, 3)))
+    tr1, tr2 = [], []
+    Y2 = lp.st_solve_sweep(K, rhs, POL, trace=tr2)
+    monkeypatch.delenv("LRK_NOPIPE")
+    Y1 = lp.st_solve_sweep(K, rhs, POL, trace=tr1)
+    assert tr1 == tr2
+    d1, d2 = _dense(Y1), _dense(Y2)
+    assert np.linalg.norm(d1 - d2) <= 1e-13 * np.linalg.norm(d2)
+
+
 def test_config_prior_arnoldi_and_posterior_variance_vs_oracle():
     """C2-type configuration at reduced size (Q1-lumped, (I+0.05L)⁻² prior,
     w = 1/σ², point subgrid): Arnoldi Ritz values (1e-6) and the posterior
