@@ -555,6 +555,92 @@ __device__ __forceinline__ void cta_tn_dmma(const double* __restrict__ A, int64_
   grp_sync<GW, WOFF>();
 }
 
+// Fused first CGS pass, one sweep over the rows: Y -= U Cm (in place), then
+// the CTA partial of U^T Y (na <= 8*NI, nb <= 4) on the FP64 tensor pipe.
+// Lane (g,t) holds U[k+t, 8i+g]; the 8 lanes sharing t together hold row k+t,
+// so the row's (U Cm)[k+t, :] is a 3-level xor-shuffle sum of their partials
+// and lane (g,t) subtracts entry g from its Y[k+t, g] before that value
+// becomes the DMMA B-operand.  Halves the passes over U of rows_sub_t + cta_tn_dmma.
+template <int NI>
+__device__ __forceinline__ void cta_subtn_dmma(const double* __restrict__ A, int64_t lda, int na,
+                                               double* __restrict__ B, int64_t ldb, int nb,
+                                               const double* __restrict__ Cm, int nrows,
+                                               double* __restrict__ out,
+                                               double* __restrict__ wbuf) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const unsigned full = 0xffffffffu;
+  const int chunk = (((nrows + NWARP - 1) / NWARP) + 3) & ~3;
+  const int r0 = warp * chunk;
+  const int r1 = min(nrows, r0 + chunk);
+  // this lane's rows of Cm (rows 8i+g, nb <= 4 columns)
+  double cm[NI][4];
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) {
+      const int row = 8 * i + g;
+      cm[i][s2] = (row < na && s2 < nb) ? Cm[row * nb + s2] : 0.0;
+    }
+  double acc[NI][2];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) acc[i][0] = acc[i][1] = 0.0;
+  constexpr int U = 4 / (NI > 4 ? 2 : 1);
+  for (int k0 = r0; k0 < r1; k0 += 4 * U) {
+    double av[U][NI], yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + 4 * u + t;
+      const bool ok = k < r1;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int col = 8 * i + g;
+        av[u][i] = (ok && col < na) ? A[k + (int64_t)col * lda] : 0.0;
+      }
+      yv[u] = (ok && g < nb) ? B[k + (int64_t)g * ldb] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double ps[4];
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) v += av[u][i] * cm[i][s2];
+        ps[s2] = v;
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) ps[s2] += __shfl_xor_sync(full, ps[s2], o);
+      const double sub = g == 0 ? ps[0] : (g == 1 ? ps[1] : (g == 2 ? ps[2] : ps[3]));
+      const int k = k0 + 4 * u + t;
+      double y = 0.0;
+      if (k < r1 && g < nb) {
+        y = yv[u] - sub;
+        B[k + (int64_t)g * ldb] = y;
+      }
+#pragma unroll
+      for (int i = 0; i < NI; ++i) dmma884(acc[i][0], acc[i][1], av[u][i], y);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ii = 8 * i + g, jj = 2 * t + h;
+      if (ii < na && jj < nb) wbuf[(warp * na + ii) * nb + jj] = acc[i][h];
+    }
+  __syncthreads();
+  for (int o = threadIdx.x; o < na * nb; o += NT) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) s2 += wbuf[w * na * nb + o];
+    out[o] = s2;
+  }
+  __syncthreads();
+}
+
 // Column-pivoted Householder QR of the q x q (q <= Q) matrix A held in
 // registers by one thread (compile-time unrolled, no local memory):
 // A P = X Rt.  On exit A = Rt (upper), X orthogonal, perm[k] = source column

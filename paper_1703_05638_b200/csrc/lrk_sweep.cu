@@ -431,9 +431,19 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     __syncthreads();
     LRK_TSTAMP(9);
     if (r > 0) {
-      rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
-      __syncthreads();
-      proj(r, pc, sPart);
+      // first CGS pass: Y -= U C and the projection U^T Y in one pass over U
+      // when the rows stream from HBM (C4: 1.36 -> 1.21 s per apply); with
+      // resident rows the two shared-memory passes are faster (the fused
+      // pass's shuffles cost more than the second read: 6k vs 10.7k cycles)
+      if (!RES && Q <= 4 && r <= 32 && NWARP * r * pc <= wcap) {
+        cta_subtn_dmma<4>(Ul, ldu, r, Yl, ldy, pc, sC, m_loc, sPart, wbuf);
+      } else if (!RES && Q <= 4 && r <= 64 && NWARP * r * pc <= wcap) {
+        cta_subtn_dmma<8>(Ul, ldu, r, Yl, ldy, pc, sC, m_loc, sPart, wbuf);
+      } else {
+        rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
+        __syncthreads();
+        proj(r, pc, sPart);
+      }
       for (int i = tid; i < r * pc; i += NT) part2[i] = sPart[i];
       LRK_TSTAMP(10);
       group_barrier(a.gbar, ncta_all, sysf);
