@@ -12,6 +12,7 @@
 #include "../../include/lrk.h"
 #include "lrk_device.cuh"
 #include "lrk_kernels.h"
+#include "lrk_small.cuh"
 
 namespace lrk {
 
@@ -256,7 +257,25 @@ __global__ void __launch_bounds__(NT, 1) truncate_kernel(const __grid_constant__
     if (tid == 0) s.misc[0] = sqrt(v[0]) * sqrt(v[1]);
   }
   __syncthreads();
-  jacobi_svd(Aj, n, Vj, n, n, s.s, s.perm, s.nrm, s.flag, s.tmp);
+  // core SVD: the 4-warp register Jacobi of the sweep for n <= 32 (outputs
+  // normalised and sorted, U to the per-CTA global scratch), the CTA-wide
+  // Jacobi beyond
+  const bool reg_svd = n <= 32;
+  const double* Ucol = Aj;
+  if (reg_svd) {
+    if (tid < 128) {
+      if (n <= 8) multi_warp_jacobi<8, 4>(Aj, n, n, jacG, Vj, n, s.s, s.perm, s.scr);
+      else if (n <= 16) multi_warp_jacobi<16, 4>(Aj, n, n, jacG, Vj, n, s.s, s.perm, s.scr);
+      else if (n <= 24) multi_warp_jacobi<24, 4>(Aj, n, n, jacG, Vj, n, s.s, s.perm, s.scr);
+      else multi_warp_jacobi<32, 4>(Aj, n, n, jacG, Vj, n, s.s, s.perm, s.scr);
+    }
+    Ucol = jacG;
+    __syncthreads();
+    for (int k = tid; k < n; k += NT) s.perm[k] = k;
+    __syncthreads();
+  } else {
+    jacobi_svd(Aj, n, Vj, n, n, s.s, s.perm, s.nrm, s.flag, s.tmp);
+  }
   if (tid == 0) {
     int rn;
     if (n == 0 || s.s[0] <= NOISE_FLOOR * s.misc[0]) rn = 0;
@@ -281,11 +300,11 @@ __global__ void __launch_bounds__(NT, 1) truncate_kernel(const __grid_constant__
         const double x = Q1[row + (int64_t)i * ldq1];
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          if (c < cn) acc[c] += x * Aj[i + s.perm[c0 + c] * n];
+          if (c < cn) acc[c] += x * Ucol[i + s.perm[c0 + c] * n];
       }
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        if (c < cn) a.out1[row + (int64_t)(c0 + c) * a.ldo1] = acc[c] / s.s[c0 + c];
+        if (c < cn) a.out1[row + (int64_t)(c0 + c) * a.ldo1] = reg_svd ? acc[c] : acc[c] / s.s[c0 + c];
     }
     for (int64_t t = t0 + tid; t < t1; t += NT) {
       double acc[8];
