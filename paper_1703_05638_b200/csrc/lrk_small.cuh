@@ -718,6 +718,132 @@ __device__ __forceinline__ void pivoted_qr_reg(double (&A)[Q][Q], int q, double 
   }
 }
 
+// Warp form of the stacked-R fix-up (pivoted_qr_reg + rounding-floor drop +
+// G = Qs X), lane c holding column c of the pc x pc R (pc <= Q <= 4): the
+// column norms, the pivot argmax (xor-shuffle, first index on ties like the
+// serial scan), the swap and the reflector broadcast are shuffles; every lane
+// forms the reflectors redundantly.  Writes R (row j in the ORIGINAL column
+// order) back to Rp and G (row-major) — the same outputs as the one-thread
+// form, to rounding.  All 32 lanes of one warp call it.
+template <int Q>
+__device__ __forceinline__ void warp_pivqr_fixup(double* __restrict__ Rp,
+                                                 const double* __restrict__ Qs,
+                                                 double* __restrict__ G,
+                                                 const double* __restrict__ Yn, int pc) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const bool own = lane < pc;
+  double a[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) a[i] = (own && i < pc) ? Rp[i * pc + lane] : 0.0;
+  double ysq = 0.0;
+  for (int s2 = 0; s2 < pc; ++s2) ysq += Yn[s2];
+  const double delta = 16.0 * DEPS * sqrt(ysq);
+  int perm = lane;
+  double vs[Q][Q], taus[Q];
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    taus[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) vs[j][i] = 0.0;
+    if (j >= pc) continue;  // uniform
+    double sn = -1.0;
+    if (own && lane >= j) {
+      sn = 0.0;
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+        if (i >= j && i < pc) sn += a[i] * a[i];
+    }
+    double bs = sn;
+    int bi = lane;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double os = __shfl_xor_sync(full, bs, o);
+      const int oi = __shfl_xor_sync(full, bi, o);
+      if (os > bs || (os == bs && oi < bi)) { bs = os; bi = oi; }
+    }
+    const int piv = bi;
+    const int src = (lane == j) ? piv : ((lane == piv) ? j : lane);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) a[i] = __shfl_sync(full, a[i], src);
+    perm = __shfl_sync(full, perm, src);
+    double cj[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) cj[i] = __shfl_sync(full, a[i], j);
+    double sig = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i)
+      if (i > j && i < pc) sig += cj[i] * cj[i];
+    const double alpha = cj[j];
+    if (sig == 0.0) continue;  // uniform (same values in every lane)
+    const double nrm = sqrt_fast(alpha * alpha + sig);
+    const double beta = alpha >= 0.0 ? -nrm : nrm;
+    const double tau = (beta - alpha) * rcp_fast(beta);
+    const double sc = rcp_fast(alpha - beta);
+    double v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) v[i] = (i == j) ? 1.0 : ((i > j && i < pc) ? cj[i] * sc : 0.0);
+    if (own && lane >= j) {
+      double w = 0.0;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) w += v[i] * a[i];
+      w *= tau;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) a[i] -= w * v[i];
+    }
+    if (lane == j) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+        if (i > j) a[i] = 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) vs[j][i] = v[i];
+    taus[j] = tau;
+  }
+  // column `lane` of X = H_0 ... H_{pc-1}: the reflectors applied to e_lane, last first
+  double x[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int j = Q - 1; j >= 0; --j) {
+    if (taus[j] == 0.0) continue;
+    double w = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) w += vs[j][i] * x[i];
+    w *= taus[j];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) x[i] -= w * vs[j][i];
+  }
+  // rows of R at the block's rounding floor are dropped (with their X column)
+#pragma unroll
+  for (int j = 0; j < Q; ++j) {
+    const double dj = __shfl_sync(full, a[j], j);
+    if (j < pc && fabs(dj) <= delta) {
+      a[j] = 0.0;
+      if (lane == j) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) x[i] = 0.0;
+      }
+    }
+  }
+  __syncwarp();
+  if (own) {
+#pragma unroll
+    for (int j = 0; j < Q; ++j)
+      if (j < pc) Rp[j * pc + perm] = a[j];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      if (i >= pc) continue;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < Q; ++k)
+        if (k < pc) acc += Qs[i * pc + k] * x[k];
+      G[i * pc + lane] = acc;
+    }
+  }
+  __syncwarp();
+}
+
 // Householder QR (optionally with column pivoting) of an n x n matrix held by
 // ONE warp in registers, lane j = column j (a[i] = entry i, zero padded to
 // NJ).  On exit a[] holds column `lane` of R; the reflector of step j is

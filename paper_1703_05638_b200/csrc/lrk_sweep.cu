@@ -505,7 +505,11 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       __syncthreads();
       LRK_TSTAMP(15);
     }
-    if (tid == tail_tid) {
+    if constexpr (Q <= 4) {
+      // rank-revealing fix-up Rp P = X Rt by the warp that owns this CTA's
+      // rows of the stacked Q (shuffle form of the one-thread path below)
+      if ((tid >> 5) == (tail_tid >> 5)) warp_pivqr_fixup<Q>(sRp, sQs, sG, sYn, pc);
+    } else if (tid == tail_tid) {
       // rows of the stacked Q that belong to this CTA; rank-revealing fix-up
       // Rp P = X Rt (column pivoting); drop rows at the block's rounding floor
       double ysq = 0.0;
