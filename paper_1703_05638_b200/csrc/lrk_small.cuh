@@ -255,34 +255,37 @@ __device__ __forceinline__ void block_apply_q_wy(const double* __restrict__ X, i
 }
 
 // X[:, 0..nx) -= A[:, 0..na) Cm, Cm na x nx row-major (shared); nx <= Q.
-template <int Q>
+// RPI rows per thread iteration (independent load streams; 4 when the rows
+// stream from HBM).
+template <int Q, int RPI = 2>
 __device__ __forceinline__ void rows_sub_t(double* __restrict__ X, int64_t ldx, int nx,
                            const double* __restrict__ A, int64_t lda, int na,
                            const double* __restrict__ Cm, int nrows) {
-  // two rows per thread iteration (independent load streams)
-  for (int t = threadIdx.x; t < nrows; t += 2 * NT) {
-    const int t2 = t + NT;
-    const bool two = t2 < nrows;
-    double acc[Q], acc2[Q];
+  for (int t = threadIdx.x; t < nrows; t += RPI * NT) {
+    double acc[RPI][Q];
 #pragma unroll
-    for (int j = 0; j < Q; ++j) acc[j] = acc2[j] = 0.0;
+    for (int q = 0; q < RPI; ++q)
+#pragma unroll
+      for (int j = 0; j < Q; ++j) acc[q][j] = 0.0;
 #pragma unroll 8
     for (int i = 0; i < na; ++i) {
-      const double a = A[t + (int64_t)i * lda];
-      const double a2 = two ? A[t2 + (int64_t)i * lda] : 0.0;
+      double a[RPI];
+#pragma unroll
+      for (int q = 0; q < RPI; ++q) a[q] = (t + q * NT < nrows) ? A[t + q * NT + (int64_t)i * lda] : 0.0;
 #pragma unroll
       for (int j = 0; j < Q; ++j)
         if (j < nx) {
           const double c = Cm[i * nx + j];
-          acc[j] += a * c;
-          acc2[j] += a2 * c;
+#pragma unroll
+          for (int q = 0; q < RPI; ++q) acc[q][j] += a[q] * c;
         }
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j)
       if (j < nx) {
-        X[t + (int64_t)j * ldx] -= acc[j];
-        if (two) X[t2 + (int64_t)j * ldx] -= acc2[j];
+#pragma unroll
+        for (int q = 0; q < RPI; ++q)
+          if (t + q * NT < nrows) X[t + q * NT + (int64_t)j * ldx] -= acc[q][j];
       }
   }
 }
@@ -435,7 +438,7 @@ __device__ __forceinline__ int warp_jacobi_reg(const double* __restrict__ Ain, i
 // written into A's first rn columns (rn <= 8*NT8).  Each warp owns whole
 // 8-row tiles, so every row is read (into fragments) before the warp writes
 // it.  Called by all threads of the CTA.
-template <int NT8>
+template <int NT8, int TPI = 2>
 __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t lda, int na,
                                                  const double* __restrict__ B, int64_t ldb, int nb,
                                                  const double* __restrict__ W, int ldw, int rn,
@@ -444,11 +447,12 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
   const int g = lane >> 2, t = lane & 3;
   const int n = na + nb;  // <= 32: every operand of a row tile is loaded up front
   const int ntile = (m + 7) >> 3;
-  // two row tiles per warp iteration: 16 independent loads in flight per lane
-  for (int tile0 = warp * 2; tile0 < ntile; tile0 += NWARP * 2) {
-    double av[2][8];
+  // TPI row tiles per warp iteration: 8*TPI independent loads in flight per
+  // lane (TPI 4 when the rows stream from HBM)
+  for (int tile0 = warp * TPI; tile0 < ntile; tile0 += NWARP * TPI) {
+    double av[TPI][8];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < TPI; ++h) {
       const int row = (tile0 + h) * 8 + g;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
@@ -457,10 +461,10 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
         if (row < m && k < n) av[h][kk] = (k < na) ? A[row + (int64_t)k * lda] : B[row + (int64_t)(k - na) * ldb];
       }
     }
-    // both row tiles advance together: 2*NT8 independent DMMA chains
-    double acc[2][NT8][2];
+    // all row tiles advance together: TPI*NT8 independent DMMA chains
+    double acc[TPI][NT8][2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < TPI; ++h)
 #pragma unroll
       for (int j = 0; j < NT8; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
 #pragma unroll
@@ -472,12 +476,12 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
         const int col = j * 8 + g;
         const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) dmma884(acc[h][j][0], acc[h][j][1], av[h][kk], b);
+        for (int h = 0; h < TPI; ++h) dmma884(acc[h][j][0], acc[h][j][1], av[h][kk], b);
       }
     }
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < TPI; ++h) {
       const int row = (tile0 + h) * 8 + g;
 #pragma unroll
       for (int j = 0; j < NT8; ++j) {

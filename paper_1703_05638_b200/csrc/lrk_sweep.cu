@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       } else if (!RES && Q <= 4 && r <= 64 && NWARP * r * pc <= wcap) {
         cta_subtn_dmma<8>(Ul, ldu, r, Yl, ldy, pc, sC, m_loc, sPart, wbuf);
       } else {
-        rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
+        rows_sub_t<Q, RES ? 2 : 4>(Yl, ldy, pc, Ul, ldu, r, sC, m_loc);
         __syncthreads();
         proj(r, pc, sPart);
       }
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       group_barrier(a.gbar, ncta_all, sysf);
       LRK_TSTAMP(11);
       reduce_partials(tab, 1, ncta_all, r * pc, sPart);
-      rows_sub_t<Q>(Yl, ldy, pc, Ul, ldu, r, sPart, m_loc);
+      rows_sub_t<Q, RES ? 2 : 4>(Yl, ldy, pc, Ul, ldu, r, sPart, m_loc);
       for (int i = tid; i < r * pc; i += NT) sC[i] += sPart[i];
       __syncthreads();
     }
@@ -653,12 +653,12 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     LRK_TSTAMP(12);
     // ---------------- basis update in place: U' = [U, Q~] Uc[:, :rn]
     if (n <= 32 && rn <= 16) {
-      update_rows_dmma<2>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      update_rows_dmma<2, RES ? 2 : 4>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
       LRK_TSTAMP(16);
       update_time_rows<16>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
       LRK_TSTAMP(17);
     } else if (n <= 32) {
-      update_rows_dmma<4>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
+      update_rows_dmma<4, RES ? 2 : 4>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
       update_time_rows<32>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
     } else {
       // wide core: out of place through the global alternates, then copy back
