@@ -700,6 +700,25 @@ def test_sweep_flush_widths_vs_oracle(p, n_side, n_t, adjoint, resident):
     assert np.linalg.norm(_dense(Y) - ref) <= 1e-11 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("adjoint", [False, True])
+def test_sweep_wide_core_vs_oracle(adjoint):
+    """Pane ranks above 28 (core order r + p > 32: the CTA-wide Jacobi path of
+    the sweep, as reached by C4 at rank 39) against the oracle."""
+    n_side, n_t = 20, 56
+    grid, K = _heat(n_side, n_t)
+    rng = np.random.default_rng(95 + adjoint)
+    R1 = rng.standard_normal((grid.n_x, 40))
+    R2 = rng.standard_normal((n_t, 40))
+    L, h, m = O.fd_operator(n_side)
+    Y1, Y2, tr_ref = O.sweep(O.StepSolver(L, m, 1.0 / n_t, n_t), R1, R2, 1e-8, None, adjoint, 4)
+    assert max(tr_ref) > 28
+    tr = []
+    Y = lp.st_solve_sweep(K, lp.LowRankMat(R1, R2), POL, adjoint=adjoint, trace=tr)
+    assert tr == tr_ref
+    ref = Y1 @ Y2.T
+    assert np.linalg.norm(_dense(Y) - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
 @pytest.mark.parametrize("rmax", [1, 3])
 def test_sweep_rank_cap_vs_oracle(rmax):
     """Rank cap binding at every flush (the r_max branch of _rank_cut)."""
