@@ -604,8 +604,12 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
                         (NWARP / 2) * n * p <= wcap;
       if (warp < 4) {  // 4-warp register Jacobi (named barrier 1), sScr = gbuf
         // K^T = Vk S Uk^T: the routine's left vectors are K's right ones
+        // NJ (rows per warp NJ/4) tracks n closely: the padding rows cost the
+        // same instructions as live ones in every rotation round
         if (n <= 8) jac_sweeps += multi_warp_jacobi<8, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
+        else if (n <= 12) jac_sweeps += multi_warp_jacobi<12, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
         else if (n <= 16) jac_sweeps += multi_warp_jacobi<16, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
+        else if (n <= 20) jac_sweeps += multi_warp_jacobi<20, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
         else if (n <= 24) jac_sweeps += multi_warp_jacobi<24, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
         else jac_sweeps += multi_warp_jacobi<32, 4>(sCore, 33, n, Vc, Uc, ldc, sS, iPerm, sScr);
       } else if (pipe) {
