@@ -197,23 +197,6 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red, double* o
   __syncthreads();
 }
 
-// Runtime-length variant: per-thread values live in a per-thread stripe of
-// `vals` (vals[k*NT + tid], k < K); results to out[0..K).  red: NWARP*K.
-__device__ inline void block_sum_rt(double* vals, int K, double* red, double* out) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int k = 0; k < K; ++k) {
-    double s = warp_sum(vals[k * NT + threadIdx.x]);
-    if (lane == 0) red[w * K + k] = s;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += NT) {
-    double s = 0.0;
-    for (int ww = 0; ww < NWARP; ++ww) s += red[ww * K + k];
-    out[k] = s;
-  }
-  __syncthreads();
-}
-
 // Reduce per-CTA partials written by the ncta CTAs of a group:
 // out[o] = sum_c part[c*stride + o], o < len.  Reads through L2 (.cg) because
 // other SMs wrote the data.  Every CTA computes the same sums in the same

@@ -14,6 +14,7 @@
 #include <algorithm>
 
 #include "lrk_small.cuh"
+#include "jacobi_variants.cuh"
 #include "lrk_brand.cuh"  // tools/: experimental secular-equation core SVD
 
 using namespace lrk;

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <vector>
 #include "lrk_small.cuh"
+#include "jacobi_variants.cuh"
 
 using namespace lrk;
 
