@@ -656,8 +656,15 @@ int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t 
   CK(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
   const double m = c->op.m_scale;
   const double* yp = nullptr;
+  // LRK_DEBUG: device time of the step solves vs the flush launches
+  const bool tdbg = std::getenv("LRK_DEBUG") != nullptr;
+  cudaEvent_t te[3];
+  float t_steps = 0.f, t_flush = 0.f;
+  if (tdbg)
+    for (auto& e : te) CK(cudaEventCreate(&e));
   for (int cs0 = 0; cs0 < nt; cs0 += Tc) {
     const int ce = std::min(nt, cs0 + Tc);
+    if (tdbg) CK(cudaEventRecord(te[0], s));
     const double* yp0 = yp;  // y before this chunk (yprev or null), for a GMRES redo
     for (int pass = 0; pass < 2; ++pass) {
       yp = yp0;
@@ -687,8 +694,23 @@ int run_sweep_phys(lrk_ctx* c, const std::string& tag, const double* B, int64_t 
     a.flush0 = cs0 / p;
     a.flush1 = std::min(nflush, (ce + p - 1) / p);
     a.r_init = cs0 == 0 ? 0 : -1;
+    if (tdbg) CK(cudaEventRecord(te[1], s));
     CK(launch_sweep(batch, s));
     ++c->launches;
+    if (tdbg) {
+      CK(cudaEventRecord(te[2], s));
+      CK(cudaEventSynchronize(te[2]));
+      float a01 = 0.f, a12 = 0.f;
+      CK(cudaEventElapsedTime(&a01, te[0], te[1]));
+      CK(cudaEventElapsedTime(&a12, te[1], te[2]));
+      t_steps += a01;
+      t_flush += a12;
+    }
+  }
+  if (tdbg) {
+    std::fprintf(stderr, "[lrk] physical sweep (%s): step solves %.1f ms, flush kernels %.1f ms\n",
+                 adjoint ? "adjoint" : "forward", t_steps, t_flush);
+    for (auto& e : te) cudaEventDestroy(e);
   }
   if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
   o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
