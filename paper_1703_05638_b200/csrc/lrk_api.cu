@@ -743,7 +743,10 @@ int run_truncate(lrk_ctx* c, const std::string& tag, int64_t n_x, int n_t, const
   if (R > NMAX)
     return fail(c, LRK_ERR_UNSUPPORTED,
                 "lr_truncate on the device supports at most 160 concatenated columns");
-  const int ncta = pick_ncta(c, std::max<int64_t>(n_x, n_t));
+  // small factors (e.g. the sensor rows of the obs truncation): more CTAs than
+  // the 384-rows rule (1024 rows: 2 -> 16 CTAs, 556 -> 470 us measured)
+  const int64_t rows = std::max<int64_t>(n_x, n_t);
+  const int ncta = std::max(pick_ncta(c, rows), (int)std::min<int64_t>(16, std::max<int64_t>(1, rows / 64)));
   const int Rw = std::max(R, 1);
   WS(double, Q1, "tr_Q1", n_x * (int64_t)Rw);
   WS(double, Q2, "tr_Q2", (int64_t)n_t * Rw);
