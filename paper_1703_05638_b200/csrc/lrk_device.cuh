@@ -529,6 +529,39 @@ __device__ __forceinline__ int rank_cut_dev(const double* s, int n, double eps0,
   return keep;
 }
 
+// rank_cut_dev on one warp for n <= 32 (lane i holds s[i]): the total by a
+// warp tree sum and the tails by a suffix scan instead of two dependent
+// serial loops; the tail-vs-threshold decision keeps the guard band with an
+// IEEE sqrt inside it.  (Summation order differs from the serial loop at the
+// rounding level only; the reference's own numpy sums are pairwise.)
+__device__ __forceinline__ int rank_cut_warp(const double* s, int n, double eps0, int r_max) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const double s0 = s[0];
+  if (n == 0 || !(s0 > 0.0)) return 0;
+  const double floor_v = NOISE_FLOOR * s0;
+  const double v = lane < n ? s[lane] : 0.0;
+  const double si = v < floor_v ? 0.0 : v;
+  const int nnz = __popc(__ballot_sync(full, si != 0.0));
+  const double sq = si * si;
+  const double total = warp_sum(sq);
+  const double thr = eps0 * sqrt(total);
+  const double thr2 = thr * thr, hi2 = thr2 * (1.0 + 1e-13), lo2 = thr2 * (1.0 - 1e-13);
+  // inclusive suffix sum: tail[i] = sum_{j >= i} sq[j]
+  double tail = sq;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_down_sync(full, tail, o);
+    if (lane + o < 32) tail += t;
+  }
+  const bool over = lane < n && (tail > hi2 || (tail >= lo2 && sqrt(tail) > thr));
+  const unsigned m = __ballot_sync(full, over);
+  int keep = m ? (32 - __clz(m)) : 0;  // largest i with tail_i > thr, plus one
+  if (keep > nnz) keep = nnz;
+  if (r_max >= 0 && keep > r_max) keep = r_max;
+  return keep;
+}
+
 // --------------------------------------------------- one-sided Jacobi SVD
 // SVD of the n x n matrix held in A (col-major, lda) by cyclic one-sided
 // (Hestenes) Jacobi with a round-robin parallel ordering; one warp per

@@ -42,6 +42,7 @@ namespace lrk {
 
 namespace {
 constexpr int NINT = NMAX + PMAX + 8;
+__device__ __forceinline__ int lane_of(int t) { return t & 31; }
 
 // a warp group: GW warps starting at warp WOFF
 template <int GW_, int WOFF_>
@@ -641,7 +642,17 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       __syncthreads();
     }
     LRK_TSTAMP(7);
-    if (tid == 0) {
+    if (n <= 32 && r <= 32 && warp == 0) {
+      // zero test and _rank_cut (lowrank.py:98-144) on one warp
+      const double ysq = warp_sum(lane_of(tid) < pc ? sYn[lane_of(tid)] : 0.0);
+      const double sg = lane_of(tid) < r ? sSig[lane_of(tid)] : 0.0;
+      const double ssq = warp_sum(sg * sg);
+      const double fs = sqrt((double)r + ysq) * sqrt(ssq + (double)pc);
+      int rn = rank_cut_warp(sS, n, a.eps0, a.r_max);
+      if (sS[0] <= NOISE_FLOOR * fs) rn = 0;
+      if (rn > cap) { rn = cap; if (cta == 0 && tid == 0) a.info[2] = 2; }
+      if (tid == 0) iFlag[1] = rn;
+    } else if (!(n <= 32 && r <= 32) && tid == 0) {
       double ysq = 0.0, ssq = 0.0;
       for (int s = 0; s < pc; ++s) ysq += sYn[s];
       for (int i = 0; i < r; ++i) ssq += sSig[i] * sSig[i];
