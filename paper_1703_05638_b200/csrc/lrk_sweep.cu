@@ -420,12 +420,18 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     } else {
       // C = W^T P: the projection onto [U_prev, Q~_prev] mapped to the pane
       // U = [U_prev, Q~_prev] W (W = the previous core's first r vectors)
+      // (four lanes per entry, each summing every fourth k, then xor shuffles)
       const double* Wp = small + L.Uc;
-      for (int o = tid; o < r * pc; o += NT) {
-        const int i = o / pc, sI = o - i * pc;
+      for (int base = 0; base < r * pc * 4; base += NT) {
+        const int idx = base + tid, o = idx >> 2, sub = idx & 3;
         double acc = 0.0;
-        for (int k = 0; k < rP; ++k) acc += Wp[k + i * ldcP] * sPart[k * pc + sI];
-        sC[o] = acc;
+        if (o < r * pc) {
+          const int i = o / pc, sI = o - i * pc;
+          for (int k = sub; k < rP; k += 4) acc += Wp[k + i * ldcP] * sPart[k * pc + sI];
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (o < r * pc && sub == 0) sC[o] = acc;
       }
     }
     have_next = false;
