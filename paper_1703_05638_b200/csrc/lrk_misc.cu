@@ -107,118 +107,135 @@ __device__ __forceinline__ double upwind_nb(const StencilArgs& a, int i1, int i2
   return acc;
 }
 
-// 2-D box stencil (5- or 9-point, optional upwind wind) on a shared-memory
-// tile: CTA = 32 x 8 threads, 32 x 32 outputs (4 rows per thread); the tile
-// with its one-node halo is staged once (coalesced rows, zero padding = the
-// Dirichlet data), so every input is read from HBM once; 16 B per output.
-constexpr int ST2 = 32;
-__global__ void __launch_bounds__(256) stencil2d_kernel(StencilArgs a) {
-  __shared__ double tile[ST2 + 2][ST2 + 3];
-  const int c = blockIdx.z;
-  const int n = a.n;
-  const int x0 = blockIdx.x * ST2, y0 = blockIdx.y * ST2;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  const double* x = a.X + (int64_t)c * a.ldx;
-  for (int idx = tid; idx < (ST2 + 2) * (ST2 + 2); idx += 256) {
-    const int ly = idx / (ST2 + 2), lx = idx - ly * (ST2 + 2);
-    const int gx = x0 + lx - 1, gy = y0 + ly - 1;
-    tile[ly][lx] = (gx >= 0 && gx < n && gy >= 0 && gy < n) ? x[(int64_t)gy * n + gx] : 0.0;
-  }
-  __syncthreads();
-  double cf[9];
-#pragma unroll
-  for (int q = 0; q < 9; ++q) cf[q] = a.coef[9 + q];
-  const int gx = x0 + tx;
-#pragma unroll
-  for (int rr = 0; rr < ST2 / 8; ++rr) {
-    const int ly = ty + 8 * rr, gy = y0 + ly;
-    if (gx >= n || gy >= n) continue;
-    double lx = 0.0;
-#pragma unroll
-    for (int d2 = 0; d2 < 3; ++d2)
-#pragma unroll
-      for (int d1 = 0; d1 < 3; ++d1) lx += cf[d2 * 3 + d1] * tile[ly + d2][tx + d1];
-    const double xc = tile[ly + 1][tx + 1];
-    if (a.wind_field) {
-      const double xm[3] = {tile[ly + 1][tx], tile[ly][tx + 1], 0.0};
-      const double xp[3] = {tile[ly + 1][tx + 2], tile[ly + 2][tx + 1], 0.0};
-      lx += upwind_nb(a, gx, gy, xc, xm, xp);
-    }
-    const double sx = a.m_scale * (xc + a.tau * lx);
-    const int64_t i = (int64_t)gy * n + gx;
-    a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
-    if (a.Ycopy) a.Ycopy[i + (int64_t)c * a.ldycopy] = a.copy_scale * xc;
-  }
-}
+// Marching box stencils with a cp.async plane pipeline.  A CTA owns a TX x TY
+// in-plane tile and marches MZ planes along the slowest axis (x3 in 3-D, x2 in
+// 2-D, where a "plane" is a TX-wide row segment); planes (+ one-node halo,
+// zero-filled outside the domain = the Dirichlet data) stream into an NS-slot
+// shared-memory ring with 8-byte cp.async, NA planes ahead of the one being
+// computed, so each thread keeps several loads in flight without registers
+// and every input is read from HBM once (16 B per output + the z halo, which
+// L2 serves).  One __syncthreads per plane: the slot refilled at step z held
+// plane z - 2, read during step z - 1.
+//   D = 3: TX = 32, TY = 16, 7-point (+ optional upwind), 2 rows per thread.
+//   D = 2: TX = 256, TY = 1, 3 x 3 box (5- or 9-point, + optional upwind).
+template <int D> struct MarchShape;
+template <> struct MarchShape<3> { static constexpr int TX = 32, TY = 16, MZ = 32; };
+template <> struct MarchShape<2> { static constexpr int TX = 256, TY = 1, MZ = 32; };
+constexpr int MARCH_NA = 3;                 // planes in flight beyond z + 1
+constexpr int MARCH_NS = MARCH_NA + 3;      // ring slots: z-1, z, z+1, NA in flight
 
-// 3-D 7-point stencil (optional upwind wind): CTA = 32 x 8 threads over an
-// (x1, x2) tile, marching ST3Z planes along x3 with the x3 neighbours in
-// registers and the current plane (+ halo) in shared memory; 16 B per output.
-constexpr int ST3Z = 16;
-__global__ void __launch_bounds__(256) stencil3d7_kernel(StencilArgs a, int nzb) {
-  __shared__ double tile[8 + 2][32 + 3];
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 8 : 0;  // 0: zero-fill, nothing read
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int D, bool WIND>
+__global__ void __launch_bounds__(256, WIND ? 3 : 4) stencil_march_kernel(StencilArgs a, int nzb) {
+  constexpr int TX = MarchShape<D>::TX, TY = MarchShape<D>::TY, MZ = MarchShape<D>::MZ;
+  constexpr int PW = TX + 2, PH = D == 3 ? TY + 2 : 1, PS = PW * PH;  // plane slot (doubles)
+  constexpr int RPT = TY * TX / 256;                       // rows per thread
+  constexpr int NS = MARCH_NS, NA = MARCH_NA;
+  __shared__ __align__(16) double ring[NS * PS];
   const int zb = blockIdx.z % nzb, c = blockIdx.z / nzb;
   const int n = a.n;
-  const int64_t plane = (int64_t)n * n;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  const int gx = x0 + tx, gy = y0 + ty;
-  const bool in = gx < n && gy < n;
+  const int64_t pstride = D == 3 ? (int64_t)n * n : n;    // march-axis stride
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const double* x = a.X + (int64_t)c * a.ldx;
-  const int z0 = zb * ST3Z, z1 = min(n, z0 + ST3Z);
-  const double cxm = a.coef[12], cxp = a.coef[14], cym = a.coef[10], cyp = a.coef[16];
-  const double czm = a.coef[4], czp = a.coef[22], cc = a.coef[13];
-  const int64_t col = (int64_t)gy * n + gx;
-  // x3 neighbours in a register queue, loads issued two planes ahead (and
-  // the halo one plane ahead) so each thread keeps several loads in flight
-  auto ld = [&](int z) { return (in && z >= 0 && z < n) ? x[(int64_t)z * plane + col] : 0.0; };
-  double below = ld(z0 - 1), cur = ld(z0), a1 = ld(z0 + 1);
-  // halo slot of this thread (84 of the 340 tile entries; threads < 84)
-  const bool hh = tid < 2 * 34 + 2 * 8;
-  int hy = 0, hx = 0;
-  if (tid < 34) { hy = 0; hx = tid; }
-  else if (tid < 68) { hy = 9; hx = tid - 34; }
-  else if (tid < 76) { hy = tid - 68 + 1; hx = 0; }
-  else if (hh) { hy = tid - 76 + 1; hx = 33; }
-  const int hgx = x0 + hx - 1, hgy = y0 + hy - 1;
-  const bool hin = hh && hgx >= 0 && hgx < n && hgy >= 0 && hgy < n;
-  const int64_t hcol = (int64_t)hgy * n + hgx;
-  double hv = hin ? x[(int64_t)z0 * plane + hcol] : 0.0;
-  for (int z = z0; z < z1; ++z) {
-    const double a2 = ld(z + 2);
-    const double hvn = (hin && z + 1 < z1) ? x[(int64_t)(z + 1) * plane + hcol] : 0.0;
-    __syncthreads();  // the previous plane's tile is consumed
-    tile[ty + 1][tx + 1] = cur;
-    if (hh) tile[hy][hx] = hv;
-    __syncthreads();
-    if (in) {
-      const double xl = tile[ty + 1][tx], xr = tile[ty + 1][tx + 2];
-      const double xd = tile[ty][tx + 1], xu = tile[ty + 2][tx + 1];
-      double lx = cc * cur + cxm * xl + cxp * xr + cym * xd + cyp * xu + czm * below + czp * a1;
-      if (a.wind_field) {
-        const double xm[3] = {xl, xd, below};
-        const double xp[3] = {xr, xu, a1};
-        lx += upwind_nb(a, gx, gy, cur, xm, xp);
+  const int z0 = zb * MZ, z1 = min(n, z0 + MZ);
+  // load index q = 0, 1, ... is plane z0 - 1 + q, slot q % NS
+  auto issue = [&](int q) {
+    const int pz = z0 - 1 + q;
+    if (pz <= z1) {
+      double* slot = ring + (q % NS) * PS;
+      const bool zin = pz >= 0 && pz < n;
+      for (int e = tid; e < PS; e += 256) {
+        const int ly = e / PW, lx = e - ly * PW;
+        const int gx = x0 + lx - 1, gy = y0 + ly - 1;
+        const bool ok = zin && gx >= 0 && gx < n && (D == 2 || (gy >= 0 && gy < n));
+        const int64_t off = ok ? (int64_t)pz * pstride + (D == 3 ? (int64_t)gy * n : 0) + gx : 0;
+        cp_async8(slot + e, x + off, ok);
       }
-      const double sx = a.m_scale * (cur + a.tau * lx);
-      const int64_t i = (int64_t)z * plane + col;
+    }
+    cp_async_commit();  // one group per load index, empty past the end
+  };
+#pragma unroll
+  for (int q = 0; q < NA + 2; ++q) issue(q);
+  const int gx = x0 + (tid % TX);
+  const int lx = tid % TX + 1;
+  double cf[9];
+  if (D == 2) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) cf[q] = a.coef[9 + q];
+  } else {
+    cf[0] = a.coef[12]; cf[1] = a.coef[14]; cf[2] = a.coef[10]; cf[3] = a.coef[16];
+    cf[4] = a.coef[4]; cf[5] = a.coef[22]; cf[6] = a.coef[13];
+  }
+  for (int z = z0; z < z1; ++z) {
+    const int q = z - z0 + 1;           // load index of plane z
+    cp_async_wait<NA - 1>();            // own copies of plane z + 1 landed
+    __syncthreads();                    // everyone's, and plane z - 2 is consumed
+    issue(q + NA + 1);                  // plane z + NA + 1 into the slot of z - 2
+    const double* pm = ring + ((q - 1) % NS) * PS;
+    const double* p0 = ring + (q % NS) * PS;
+    const double* pp = ring + ((q + 1) % NS) * PS;
+#pragma unroll
+    for (int rr = 0; rr < RPT; ++rr) {
+      const int ly = D == 3 ? tid / TX + rr * (256 / TX) + 1 : 0;
+      const int gy = D == 3 ? y0 + ly - 1 : z;
+      if (gx >= n || gy >= n) continue;
+      const int k = ly * PW + lx;
+      const double cur = p0[k];
+      double lx_acc;
+      double xm[3], xp[3];
+      if (D == 3) {
+        xm[0] = p0[k - 1]; xp[0] = p0[k + 1];
+        xm[1] = p0[k - PW]; xp[1] = p0[k + PW];
+        xm[2] = pm[k]; xp[2] = pp[k];
+        lx_acc = cf[6] * cur + cf[0] * xm[0] + cf[1] * xp[0] + cf[2] * xm[1] + cf[3] * xp[1] +
+                 cf[4] * xm[2] + cf[5] * xp[2];
+      } else {
+        lx_acc = cf[0] * pm[k - 1] + cf[1] * pm[k] + cf[2] * pm[k + 1] +
+                 cf[3] * p0[k - 1] + cf[4] * cur + cf[5] * p0[k + 1] +
+                 cf[6] * pp[k - 1] + cf[7] * pp[k] + cf[8] * pp[k + 1];
+        xm[0] = p0[k - 1]; xp[0] = p0[k + 1];
+        xm[1] = pm[k]; xp[1] = pp[k];
+        xm[2] = 0.0; xp[2] = 0.0;
+      }
+      if (WIND) lx_acc += upwind_nb(a, gx, gy, cur, xm, xp);
+      const double sx = a.m_scale * (cur + a.tau * lx_acc);
+      const int64_t i = D == 3 ? (int64_t)z * pstride + (int64_t)gy * n + gx
+                               : (int64_t)gy * n + gx;
       a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
       if (a.Ycopy) a.Ycopy[i + (int64_t)c * a.ldycopy] = a.copy_scale * cur;
     }
-    below = cur;
-    cur = a1;
-    a1 = a2;
-    hv = hvn;
   }
+  cp_async_wait<0>();
 }
 
-// Launch the tiled kernel that fits the operator (2-D box; 3-D 7-point),
+template <int D>
+static void launch_march(const StencilArgs& a, cudaStream_t s) {
+  constexpr int TX = MarchShape<D>::TX, TY = MarchShape<D>::TY, MZ = MarchShape<D>::MZ;
+  const int n = a.n;
+  const int nzb = (n + MZ - 1) / MZ;
+  dim3 grid((n + TX - 1) / TX, D == 3 ? (n + TY - 1) / TY : 1, nzb * a.ncols);
+  if (a.wind_field)
+    stencil_march_kernel<D, true><<<grid, 256, 0, s>>>(a, nzb);
+  else
+    stencil_march_kernel<D, false><<<grid, 256, 0, s>>>(a, nzb);
+}
+
+// Launch the marching kernel that fits the operator (2-D box; 3-D 7-point),
 // the generic one otherwise.  a.ncols columns.
 void launch_stencil(const StencilArgs& a, cudaStream_t s) {
   const int n = a.n;
   if (a.dim == 2) {
-    dim3 grid((n + ST2 - 1) / ST2, (n + ST2 - 1) / ST2, a.ncols);
-    stencil2d_kernel<<<grid, dim3(32, 8), 0, s>>>(a);
+    launch_march<2>(a, s);
     return;
   }
   bool seven = true;
@@ -228,9 +245,7 @@ void launch_stencil(const StencilArgs& a, cudaStream_t s) {
     if (nnz_axes > 1 && a.coef[q] != 0.0) seven = false;
   }
   if (seven) {
-    const int nzb = (n + ST3Z - 1) / ST3Z;
-    dim3 grid((n + 31) / 32, (n + 7) / 8, nzb * a.ncols);
-    stencil3d7_kernel<<<grid, dim3(32, 8), 0, s>>>(a, nzb);
+    launch_march<3>(a, s);
     return;
   }
   const int64_t nx = (int64_t)n * n * n;

@@ -115,12 +115,14 @@ def test_stencil_apply_is_the_dense_operator():
 
 
 @pytest.mark.parametrize("case", ["fd2d_37", "q1_2d_33", "cd2d_rot_35", "cd2d_const_34",
-                                  "fd3d_19", "cd3d_rot_18", "cd3d_const_17"])
+                                  "q1_2d_261", "cd2d_rot_259",
+                                  "fd3d_19", "cd3d_rot_18", "cd3d_const_17",
+                                  "fd3d_37", "cd3d_rot_35"])
 def test_stencil_tiles_vs_sparse_operator(case):
-    """The tiled stencil kernels (2-D 32x32 tiles, 3-D 16-plane marching with
-    register x3 neighbours, fused -M W1 block) against the assembled sparse
-    operator: sizes that cut tiles and plane chunks, forward and adjoint,
-    constant and node-by-node (rotating) wind."""
+    """The marching stencil kernels (cp.async plane ring; 2-D: 256-wide row
+    segments, 3-D: 32x16 plane tiles; 32-plane chunks; fused -M W1 block)
+    against the assembled sparse operator: sizes that cut tiles and plane
+    chunks, forward and adjoint, constant and node-by-node (rotating) wind."""
     n = int(case.rsplit("_", 1)[1])
     d = 3 if "3d" in case else 2
     grid = lp.build_grid(n, d)
