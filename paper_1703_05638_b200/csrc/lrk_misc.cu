@@ -592,6 +592,111 @@ __global__ void __launch_bounds__(NT, 1)
     part[(int64_t)blockIdx.x * pstride + (int64_t)(o / nb) * ldo + (o % nb)] = buf[o];
 }
 
+// Staged variant for wide Grams (both sides > 32 columns, the FP64-tensor-
+// bound shape): the CTA streams chunks of GKC rows of up to 64 columns of A
+// and B into a GST-stage shared-memory ring with 16-byte cp.async (GST - 1
+// chunks, ~96 KB, in flight per SM: enough for HBM latency at the ridge
+// point), and its 8 warps split the 64 x 64 output 16 x 32 each, reading
+// their m8n8k4 fragments from shared memory (column stride GKC + 4 doubles:
+// two wavefronts per fragment load, conflict-free).  Each output element is
+// accumulated by one warp in row order (deterministic).  Requires lda, ldb
+// even and 16-byte-aligned bases (checked by the launcher).
+constexpr int GKC = 32, GST = 4, GSS = GKC + 4;
+__global__ void __launch_bounds__(NT, 1)
+    gram_staged_kernel(const double* __restrict__ A, int64_t lda, int na,
+                       const double* __restrict__ B, int64_t ldb, int nb, int64_t n,
+                       double* __restrict__ part, int ldo, int64_t pstride) {
+  extern __shared__ __align__(16) double gsm[];  // [GST][128 columns][GSS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  // CTA row range: whole GKC chunks (the 16-byte copies stay aligned)
+  const int64_t nch = (n + GKC - 1) / GKC;
+  const int64_t cper = (nch + gridDim.x - 1) / gridDim.x;
+  const int64_t c0 = cper * blockIdx.x, c1 = min(nch, c0 + cper);
+  const int nc = c1 > c0 ? (int)(c1 - c0) : 0;
+  auto issue = [&](int q) {
+    if (q < nc) {
+      double* st = gsm + (q % GST) * (128 * GSS);
+      const int64_t r0 = (c0 + q) * GKC;
+#pragma unroll
+      for (int m = 0; m < 128 * (GKC / 2) / NT; ++m) {
+        const int e = tid + NT * m;
+        const int col = e / (GKC / 2), seg = e % (GKC / 2);
+        const bool isa = col < 64;
+        const int cc = isa ? col : col - 64;
+        if (cc < (isa ? na : nb)) {
+          const int64_t row = r0 + 2 * seg;
+          const int64_t left = n - row;
+          const int bytes = left >= 2 ? 16 : (left == 1 ? 8 : 0);
+          const double* src = isa ? A + (int64_t)cc * lda : B + (int64_t)cc * ldb;
+          src += bytes ? row : 0;
+          const unsigned d = (unsigned)__cvta_generic_to_shared(st + col * GSS + 2 * seg);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int q = 0; q < GST - 1; ++q) issue(q);
+  const int ia = 16 * (warp >> 1), jb = 64 + 32 * (warp & 1);
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int q = 0; q < nc; ++q) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GST - 2) : "memory");
+    __syncthreads();       // chunk q visible; chunk q - 1's slot is free
+    issue(q + GST - 1);
+    const double* st = gsm + (q % GST) * (128 * GSS);
+    const double* pa = st + (ia + g) * GSS + t;
+    const double* pb = st + (jb + g) * GSS + t;
+#pragma unroll
+    for (int k = 0; k < GKC; k += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = pa[8 * i * GSS + k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = pb[8 * j * GSS + k];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  // a zero-filled tail contributes exact zeros; columns >= na / nb hold stale
+  // shared memory and only reach the masked outputs
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ii = ia + 8 * i + g, jj = jb - 64 + 8 * j + 2 * t + h;
+        if (ii < na && jj < nb)
+          part[(int64_t)blockIdx.x * pstride + (int64_t)ii * ldo + jj] = nc ? acc[i][j][h] : 0.0;
+      }
+}
+
+static bool gram_staged_ok(const double* A, int64_t lda, const double* B, int64_t ldb) {
+  return ((lda | ldb) & 1) == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0;
+}
+
+static void launch_gram_staged(const double* A, int64_t lda, int na, const double* B, int64_t ldb,
+                               int nb, int64_t n, double* part, int ldo, int64_t pstride,
+                               int nparts, cudaStream_t s) {
+  const int smem = GST * 128 * GSS * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  gram_staged_kernel<<<nparts, NT, smem, s>>>(A, lda, na, B, ldb, nb, n, part, ldo, pstride);
+}
+
 template <int TA>
 static void gram_tb(int tb, const double* A, int64_t lda, int na, const double* B, int64_t ldb,
                     int nb, int64_t n, double* part, int ldo, int64_t pstride, int nparts,
@@ -614,6 +719,10 @@ void launch_gram(const double* A, int64_t lda, int na, const double* B, int64_t 
       const double* Ab = A + (int64_t)a0 * lda;
       const double* Bb = B + (int64_t)b0 * ldb;
       double* pb = part + (int64_t)a0 * nb + b0;
+      if (ca > 32 && cb > 32 && gram_staged_ok(Ab, lda, Bb, ldb) && !getenv("LRK_GRAM_DIRECT")) {
+        launch_gram_staged(Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
+        continue;
+      }
       if (ta <= 1) gram_tb<1>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
       else if (ta <= 2) gram_tb<2>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);
       else if (ta <= 4) gram_tb<4>(tb, Ab, lda, ca, Bb, ldb, cb, n, pb, nb, pstride, nparts, s);

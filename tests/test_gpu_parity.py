@@ -174,6 +174,22 @@ def test_lr_dot_gram_tiles(ra, rb):
     assert abs(got - ref) <= 1e-12 * np.sqrt(np.sum((A1.T @ A1) * (A2.T @ A2)) * np.sum((B1.T @ B1) * (B2.T @ B2)))
 
 
+@pytest.mark.parametrize("ra,rb", [(64, 64), (48, 48), (40, 70), (33, 128), (64, 33)])
+def test_lr_dot_gram_staged(ra, rb):
+    """The cp.async-staged 64 x 64 DMMA Gram (both sides > 32 columns, even
+    leading dimensions) against numpy: row counts that cut the 32-row chunks
+    and the CTA ranges, column blocks beyond 64, masked tiles."""
+    rng = np.random.default_rng(ra * 1000 + rb)
+    n_x, n_t = 5002, 38
+    A = lp.LowRankMat(rng.standard_normal((n_x, ra)), rng.standard_normal((n_t, ra)))
+    B = lp.LowRankMat(rng.standard_normal((n_x, rb)), rng.standard_normal((n_t, rb)))
+    A1, A2 = A.numpy()
+    B1, B2 = B.numpy()
+    ref = float(np.sum((A1.T @ B1) * (A2.T @ B2)))
+    got = lp.lr_dot(A, B)
+    assert abs(got - ref) <= 1e-12 * np.sqrt(np.sum((A1.T @ A1) * (A2.T @ A2)) * np.sum((B1.T @ B1) * (B2.T @ B2)))
+
+
 def test_step_solve_vs_superlu():
     grid, K = _heat(31, 8)
     L, h, m = O.fd_operator(31)
