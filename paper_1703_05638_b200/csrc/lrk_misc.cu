@@ -116,11 +116,11 @@ __device__ __forceinline__ double upwind_nb(const StencilArgs& a, int i1, int i2
 // and every input is read from HBM once (16 B per output + the z halo, which
 // L2 serves).  One __syncthreads per plane: the slot refilled at step z held
 // plane z - 2, read during step z - 1.
-//   D = 3: TX = 32, TY = 16, 7-point (+ optional upwind), 2 rows per thread.
-//   D = 2: TX = 256, TY = 1, 3 x 3 box (5- or 9-point, + optional upwind).
+//   D = 3: TX = 32, TY = 16, 7-point (+ optional upwind), 2 rows per thread, MZ = 32.
+//   D = 2: TX = 256, TY = 1, 3 x 3 box (5- or 9-point, + optional upwind), MZ = 16.
 template <int D> struct MarchShape;
-template <> struct MarchShape<3> { static constexpr int TX = 32, TY = 16, MZ = 32; };
-template <> struct MarchShape<2> { static constexpr int TX = 256, TY = 1, MZ = 32; };
+template <> struct MarchShape<3> { static constexpr int TX = 32, TY = 16; };
+template <> struct MarchShape<2> { static constexpr int TX = 256, TY = 1; };
 constexpr int MARCH_NA = 3;                 // planes in flight beyond z + 1
 constexpr int MARCH_NS = MARCH_NA + 3;      // ring slots: z-1, z, z+1, NA in flight
 
@@ -134,9 +134,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int D, bool WIND>
+template <int D, bool WIND, int MZ>
 __global__ void __launch_bounds__(256, WIND ? 3 : 4) stencil_march_kernel(StencilArgs a, int nzb) {
-  constexpr int TX = MarchShape<D>::TX, TY = MarchShape<D>::TY, MZ = MarchShape<D>::MZ;
+  constexpr int TX = MarchShape<D>::TX, TY = MarchShape<D>::TY;
   constexpr int PW = TX + 2, PH = D == 3 ? TY + 2 : 1, PS = PW * PH;  // plane slot (doubles)
   constexpr int RPT = TY * TX / 256;                       // rows per thread
   constexpr int NS = MARCH_NS, NA = MARCH_NA;
@@ -218,16 +218,23 @@ __global__ void __launch_bounds__(256, WIND ? 3 : 4) stencil_march_kernel(Stenci
   cp_async_wait<0>();
 }
 
-template <int D>
-static void launch_march(const StencilArgs& a, cudaStream_t s) {
-  constexpr int TX = MarchShape<D>::TX, TY = MarchShape<D>::TY, MZ = MarchShape<D>::MZ;
+template <int D, int MZ>
+static void launch_march_mz(const StencilArgs& a, cudaStream_t s) {
+  constexpr int TX = MarchShape<D>::TX, TY = MarchShape<D>::TY;
   const int n = a.n;
   const int nzb = (n + MZ - 1) / MZ;
   dim3 grid((n + TX - 1) / TX, D == 3 ? (n + TY - 1) / TY : 1, nzb * a.ncols);
   if (a.wind_field)
-    stencil_march_kernel<D, true><<<grid, 256, 0, s>>>(a, nzb);
+    stencil_march_kernel<D, true, MZ><<<grid, 256, 0, s>>>(a, nzb);
   else
-    stencil_march_kernel<D, false><<<grid, 256, 0, s>>>(a, nzb);
+    stencil_march_kernel<D, false, MZ><<<grid, 256, 0, s>>>(a, nzb);
+}
+
+// planes per CTA (measured at C3 / C4: 2-D 8/16/32/64 -> 80/78/82/91 us,
+// 3-D 16/32/64 -> 717/710/709 us)
+template <int D>
+static void launch_march(const StencilArgs& a, cudaStream_t s) {
+  launch_march_mz<D, D == 2 ? 16 : 32>(a, s);
 }
 
 // Launch the marching kernel that fits the operator (2-D box; 3-D 7-point),

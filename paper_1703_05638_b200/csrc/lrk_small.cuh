@@ -355,6 +355,65 @@ __device__ __forceinline__ void update_rows_dmma(double* __restrict__ A, int64_t
   }
 }
 
+// Wide-core variant (n = na + nb <= 64, rn <= 64): the same in-place row-tile
+// update with 16 k-steps and 8 output column tiles; W is read through L1
+// (global per-CTA scratch, n x rn <= 32 KB) and amortised over TPI row tiles.
+template <int TPI>
+__device__ __forceinline__ void update_rows_dmma_wide(double* __restrict__ A, int64_t lda, int na,
+                                                      const double* __restrict__ B, int64_t ldb,
+                                                      int nb, const double* __restrict__ W,
+                                                      int ldw, int rn, int m) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int n = na + nb;
+  const int ntile = (m + 7) >> 3;
+  const int nk = (n + 3) >> 2, nj = (rn + 7) >> 3;
+  for (int tile0 = warp * TPI; tile0 < ntile; tile0 += NWARP * TPI) {
+    double av[TPI][16];
+#pragma unroll
+    for (int h = 0; h < TPI; ++h) {
+      const int row = (tile0 + h) * 8 + g;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int k = kk * 4 + t;
+        av[h][kk] = 0.0;
+        if (row < m && k < n) av[h][kk] = (k < na) ? A[row + (int64_t)k * lda] : B[row + (int64_t)(k - na) * ldb];
+      }
+    }
+    double acc[TPI][8][2];
+#pragma unroll
+    for (int h = 0; h < TPI; ++h)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[h][j][0] = acc[h][j][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      if (kk >= nk) break;
+      const int k = kk * 4 + t;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= nj) break;
+        const int col = j * 8 + g;
+        const double b = (k < n && col < rn) ? W[k + col * ldw] : 0.0;
+#pragma unroll
+        for (int h = 0; h < TPI; ++h) dmma884(acc[h][j][0], acc[h][j][1], av[h][kk], b);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < TPI; ++h) {
+      const int row = (tile0 + h) * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c0 = j * 8 + 2 * t;
+        if (row < m) {
+          if (c0 < rn) A[row + (int64_t)c0 * lda] = acc[h][j][0];
+          if (c0 + 1 < rn) A[row + (int64_t)(c0 + 1) * lda] = acc[h][j][1];
+        }
+      }
+    }
+  }
+}
+
 // CTA partial of A^T B (na <= 8*NI, nb <= 8) on the FP64 tensor pipe:
 // warp w takes a contiguous row chunk; m8n8k4 with the A-operand = rows k..k+3
 // of 8 columns of A (lane (g,t) reads A[k+t, 8i+g]: fully used 32-byte

@@ -681,8 +681,25 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     } else if (n <= 32) {
       update_rows_dmma<4, RES ? 2 : 4>(Ul, ldu, r, Ql, ldq, pc, Ucs, ldc, rn, m_loc);
       update_time_rows<32>(Vl, ldvl, r, Vcs, ldc, rn, t0, t1, a.adjoint, n_t, start, pc);
+    } else if (n <= 64) {
+      // wide core (n <= 64): U rows in place on the DMMA pipe (one pass over
+      // U; the former per-column loop re-read the row block rn times); the
+      // time rows out of place through the global alternate, then copied back
+      update_rows_dmma_wide<RES ? 1 : 2>(Ul, ldu, r, Ql, ldq, pc, Ucg, ldc, rn, m_loc);
+      const double* Vc = Vcg;
+      for (int c = 0; c < rn; ++c)
+        for (int64_t t = t0 + tid; t < t1; t += NT) {
+          int sel = a.adjoint ? (n_t - 1 - start) - (int)t : (int)t - start;
+          double acc = (sel >= 0 && sel < pc) ? Vc[(r + sel) + c * ldc] : 0.0;
+          for (int k = 0; k < r; ++k) acc += Vl[(t - t0) + (int64_t)k * ldvl] * Vc[k + c * ldc];
+          a.V1[t + (int64_t)c * a.ldv] = acc;
+        }
+      __syncthreads();
+      for (int c = 0; c < rn; ++c)
+        for (int64_t t = t0 + tid; t < t1; t += NT) Vl[(t - t0) + (int64_t)c * ldvl] = a.V1[t + (int64_t)c * a.ldv];
     } else {
-      // wide core: out of place through the global alternates, then copy back
+      // widest cores (n > 64, no rank cap): out of place through the global
+      // alternates, then copy back
       const double* Uc = Ucg;
       const double* Vc = Vcg;
       for (int c = 0; c < rn; ++c) {

@@ -718,11 +718,12 @@ def test_sweep_flush_widths_vs_oracle(p, n_side, n_t, adjoint, resident):
     assert np.linalg.norm(_dense(Y) - ref) <= 1e-11 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("adjoint", [False, True])
-def test_sweep_wide_core_vs_oracle(adjoint):
-    """Pane ranks above 28 (core order r + p > 32: the CTA-wide Jacobi path of
-    the sweep, as reached by C4 at rank 39) against the oracle."""
-    n_side, n_t = 20, 56
+@pytest.mark.parametrize("adjoint,n_side,n_t", [(False, 20, 56), (True, 20, 56),
+                                                (False, 400, 40), (True, 400, 40)])
+def test_sweep_wide_core_vs_oracle(adjoint, n_side, n_t):
+    """Pane ranks above 28 (core order r + p > 32: the CTA-wide Jacobi path and
+    the wide DMMA basis update of the sweep, as reached by C4 at rank 39)
+    against the oracle, with resident (SMEM) and global rows (n_x = 160,000)."""
     grid, K = _heat(n_side, n_t)
     rng = np.random.default_rng(95 + adjoint)
     R1 = rng.standard_normal((grid.n_x, 40))
