@@ -124,12 +124,6 @@ template <> struct MarchShape<2> { static constexpr int TX = 256, TY = 1; };
 constexpr int MARCH_NA = 3;                 // planes in flight beyond z + 1
 constexpr int MARCH_NS = MARCH_NA + 3;      // ring slots: z-1, z, z+1, NA in flight
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int sz = valid ? 8 : 0;  // 0: zero-fill, nothing read
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz)
-               : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -148,18 +142,37 @@ __global__ void __launch_bounds__(256, WIND ? 3 : 4) stencil_march_kernel(Stenci
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const double* x = a.X + (int64_t)c * a.ldx;
   const int z0 = zb * MZ, z1 = min(n, z0 + MZ);
+  // this thread's slot elements (the same for every plane): in-plane
+  // offset, in-domain flag and shared-memory address, computed once
+  constexpr int NE = (PS + 255) / 256;
+  int64_t eoff[NE];
+  bool eok[NE];
+  unsigned edst[NE];
+#pragma unroll
+  for (int m = 0; m < NE; ++m) {
+    const int e = tid + 256 * m;
+    const int ly = e / PW, lx = e - ly * PW;
+    const int gx = x0 + lx - 1, gy = y0 + ly - 1;
+    eok[m] = e < PS && gx >= 0 && gx < n && (D == 2 || (gy >= 0 && gy < n));
+    eoff[m] = eok[m] ? (D == 3 ? (int64_t)gy * n : 0) + gx : 0;
+    edst[m] = (unsigned)__cvta_generic_to_shared(ring + (e < PS ? e : 0));
+  }
   // load index q = 0, 1, ... is plane z0 - 1 + q, slot q % NS
   auto issue = [&](int q) {
     const int pz = z0 - 1 + q;
     if (pz <= z1) {
-      double* slot = ring + (q % NS) * PS;
+      const unsigned soff = (unsigned)((q % NS) * PS * sizeof(double));
       const bool zin = pz >= 0 && pz < n;
-      for (int e = tid; e < PS; e += 256) {
-        const int ly = e / PW, lx = e - ly * PW;
-        const int gx = x0 + lx - 1, gy = y0 + ly - 1;
-        const bool ok = zin && gx >= 0 && gx < n && (D == 2 || (gy >= 0 && gy < n));
-        const int64_t off = ok ? (int64_t)pz * pstride + (D == 3 ? (int64_t)gy * n : 0) + gx : 0;
-        cp_async8(slot + e, x + off, ok);
+      const double* xp = x + (zin ? (int64_t)pz * pstride : 0);
+#pragma unroll
+      for (int m = 0; m < NE; ++m) {
+        if (tid + 256 * m < PS) {
+          const bool ok = zin && eok[m];
+          const int sz = ok ? 8 : 0;  // 0: zero-fill, nothing read
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(edst[m] + soff),
+                       "l"(xp + eoff[m]), "r"(sz)
+                       : "memory");
+        }
       }
     }
     cp_async_commit();  // one group per load index, empty past the end
