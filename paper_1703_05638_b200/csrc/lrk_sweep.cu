@@ -329,6 +329,63 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
       int ks[Q];
 #pragma unroll
       for (int s = 0; s < Q; ++s) ks[s] = a.adjoint ? (n_t - 1 - (st + s)) : (st + s);
+      if constexpr (!RES && Q <= 8) {
+        // rows from HBM: GR rows per thread with all their loads issued
+        // before the recurrence (same per-row arithmetic and order)
+        constexpr int GR = 4;
+        const int gs = 32 * GW;
+        for (int i0 = gt; i0 < m_loc; i0 += GR * gs) {
+          double acc[GR][Q], tv[GR], rs[GR], y[GR];
+#pragma unroll
+          for (int h = 0; h < GR; ++h) {
+            const int i = i0 + h * gs;
+            const bool ok = i < m_loc;
+            tv[h] = ok ? th[i] : 0.0;
+            rs[h] = ok ? (rsc ? rsc[i] : 1.0) : 0.0;
+            y[h] = ok ? yp[i] : 0.0;
+#pragma unroll
+            for (int s = 0; s < Q; ++s) acc[h][s] = 0.0;
+          }
+          for (int j0 = 0; j0 < rb; j0 += 4) {
+            double bv[GR][4];
+#pragma unroll
+            for (int h = 0; h < GR; ++h)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = i0 + h * gs;
+                bv[h][u] = (i < m_loc && j0 + u < rb) ? a.B[r0 + i + (int64_t)(j0 + u) * a.ldb] : 0.0;
+              }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (j0 + u >= rb) break;
+              const double* w2 = a.W2 + (int64_t)(j0 + u) * a.ldw2;
+#pragma unroll
+              for (int s = 0; s < Q; ++s)
+                if (s < pcn) {
+                  const double wv = w2[ks[s]];
+#pragma unroll
+                  for (int h = 0; h < GR; ++h) acc[h][s] += bv[h][u] * wv;
+                }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < GR; ++h) {
+            const int i = i0 + h * gs;
+            if (i < m_loc) {
+              double yy = y[h];
+#pragma unroll
+              for (int s = 0; s < Q; ++s) {
+                if (s < pcn) {
+                  yy = tv[h] * yy + rs[h] * acc[h][s];
+                  if (fabs(yy) < a.ftz) yy = 0.0;
+                  Yl[i + (int64_t)s * ldy] = yy;
+                }
+              }
+              yp[i] = yy;
+            }
+          }
+        }
+      } else {
       for (int i = gt; i < m_loc; i += 32 * GW) {
         double acc[Q];
 #pragma unroll
@@ -353,6 +410,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
           }
         }
         yp[i] = y;
+      }
       }
     }
     grp_sync<GW, WOFF>();
