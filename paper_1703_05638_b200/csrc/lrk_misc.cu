@@ -709,10 +709,13 @@ static void launch_gram_staged(const double* A, int64_t lda, int na, const doubl
                                int nb, int64_t n, double* part, int ldo, int64_t pstride,
                                int nparts, cudaStream_t s) {
   const int smem = GST * 128 * GSS * (int)sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  // the opt-in shared-memory size is a per-device function attribute
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     cudaFuncSetAttribute(gram_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   gram_staged_kernel<<<nparts, NT, smem, s>>>(A, lda, na, B, ldb, nb, n, part, ldo, pstride);
 }
