@@ -809,13 +809,16 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
 
 template <int Q, bool RES>
 static cudaError_t launch_q(const SweepBatch& batch, cudaStream_t s) {
-  static int attr_bytes = 0;
+  // the opt-in shared-memory size is a per-device function attribute
+  static int attr_bytes[64] = {};
   const int smem = batch.g[0].smem_doubles * (int)sizeof(double);
-  if (smem > attr_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || smem > attr_bytes[dev]) {
     cudaError_t e = cudaFuncSetAttribute(sweep_kernel<Q, RES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_bytes = smem;
+    if (dev >= 0 && dev < 64) attr_bytes[dev] = smem;
   }
   void* params[] = {(void*)&batch};
   return cudaLaunchCooperativeKernel((const void*)sweep_kernel<Q, RES>,

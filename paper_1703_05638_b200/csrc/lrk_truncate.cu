@@ -369,13 +369,16 @@ __global__ void __launch_bounds__(NT, 1) truncate_kernel(const __grid_constant__
 }
 
 cudaError_t launch_truncate(const TruncArgs& args, cudaStream_t st) {
-  static bool attr_set = false;
+  // the opt-in shared-memory size is a per-device function attribute
+  static bool attr_set[64] = {};
   const size_t smem = TruncSmem::bytes;
-  if (!attr_set) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(truncate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   void* params[] = {(void*)&args};
   return cudaLaunchCooperativeKernel((const void*)truncate_kernel, dim3(args.ncta), dim3(NT), params,
