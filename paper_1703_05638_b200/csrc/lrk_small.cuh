@@ -15,7 +15,9 @@ namespace lrk {
 // reduction per column: sums[0] = ||x_j below diag||^2, sums[k] = x_j . x_k.
 // Reflectors overwrite X below the diagonal, tau[j] saved, R (q x q
 // row-major, zero padded) to Rout.  red: NWARP*Q, tmp: Q (shared).
-template <int Q>
+// RB > 1 (rows streaming from HBM/L2): RB rows per thread per iteration with
+// all their loads issued first; per-thread accumulation order unchanged.
+template <int Q, int RB = 1>
 __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, int m, int q,
                            double* __restrict__ tau, double* __restrict__ Rout,
                            double* __restrict__ red, double* __restrict__ tmp) {
@@ -26,12 +28,36 @@ __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, 
     double s[Q];
 #pragma unroll
     for (int k = 0; k < Q; ++k) s[k] = 0.0;
+    if constexpr (RB > 1) {
+      for (int i0 = j + 1 + tid; i0 < m; i0 += RB * NT) {
+        double xv[RB][Q];
+#pragma unroll
+        for (int h = 0; h < RB; ++h) {
+          const int i = i0 + h * NT;
+#pragma unroll
+          for (int k = 0; k < Q; ++k)
+            xv[h][k] = (i < m && k >= j && k < q) ? X[i + (int64_t)k * ldx] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < RB; ++h)
+          if (i0 + h * NT < m) {
+            double xj = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q; ++k)
+              if (k == j) xj = xv[h][k];
+#pragma unroll
+            for (int k = 0; k < Q; ++k)
+              if (k >= j && k < q) s[k] += xj * xv[h][k];
+          }
+      }
+    } else {
 #pragma unroll 4
     for (int i = j + 1 + tid; i < m; i += NT) {
       const double xj = X[i + (int64_t)j * ldx];
 #pragma unroll
       for (int k = 0; k < Q; ++k)
         if (k >= j && k < q) s[k] += xj * X[i + (int64_t)k * ldx];
+    }
     }
     // s[j] = ||x_j||^2 below the diagonal, s[k>j] = x_j . x_k (below the diagonal)
     block_sum<Q>(s, red, tmp);
@@ -57,6 +83,32 @@ __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, 
 #pragma unroll
     for (int k = 0; k < Q; ++k) f[k] = (k > j && k < q) ? t * (xr[k] + scale * s[k]) : 0.0;
     __syncthreads();  // row j read by everyone before it changes
+    if constexpr (RB > 1) {
+      for (int i0 = j + 1 + tid; i0 < m; i0 += RB * NT) {
+        double xv[RB][Q];
+#pragma unroll
+        for (int h = 0; h < RB; ++h) {
+          const int i = i0 + h * NT;
+#pragma unroll
+          for (int k = 0; k < Q; ++k)
+            xv[h][k] = (i < m && k >= j && k < q) ? X[i + (int64_t)k * ldx] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < RB; ++h) {
+          const int i = i0 + h * NT;
+          if (i < m) {
+            double vi = 0.0;
+#pragma unroll
+            for (int k = 0; k < Q; ++k)
+              if (k == j) vi = xv[h][k] * scale;
+            X[i + (int64_t)j * ldx] = vi;
+#pragma unroll
+            for (int k = 0; k < Q; ++k)
+              if (k > j && k < q) X[i + (int64_t)k * ldx] = xv[h][k] - f[k] * vi;
+          }
+        }
+      }
+    } else {
 #pragma unroll 4
     for (int i = j + 1 + tid; i < m; i += NT) {
       const double vi = X[i + (int64_t)j * ldx] * scale;
@@ -67,6 +119,7 @@ __device__ __forceinline__ void block_qr_t(double* __restrict__ X, int64_t ldx, 
 #pragma unroll
       for (int k = 0; k < Q; ++k)
         if (k > j && k < q) X[i + (int64_t)k * ldx] = x[k] - f[k] * vi;
+    }
     }
     if (tid == 0) {
       tau[j] = t;

@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     }
     LRK_TSTAMP(2);
     // ---------------- phase 3: local Householder QR of the remainder
-    block_qr_t<Q>(Yl, ldy, m_loc, pc, sTau, sR, sRed, sTmp);
+    block_qr_t<Q, (!RES && Q <= 4) ? 4 : 1>(Yl, ldy, m_loc, pc, sTau, sR, sRed, sTmp);
     for (int i = tid; i < pc * pc; i += NT) part3[i] = sR[i];
     LRK_TSTAMP(3);
     group_barrier(a.gbar, ncta_all, sysf);
