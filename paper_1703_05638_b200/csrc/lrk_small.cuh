@@ -320,6 +320,29 @@ __device__ __forceinline__ void rows_sub_t(double* __restrict__ X, int64_t ldx, 
     for (int q = 0; q < RPI; ++q)
 #pragma unroll
       for (int j = 0; j < Q; ++j) acc[q][j] = 0.0;
+    if constexpr (RPI >= 4 && Q <= 4) {
+      // rows from HBM: four columns of A for all RPI rows loaded before
+      // their FMAs (same per-row accumulation order)
+      for (int i0 = 0; i0 < na; i0 += 4) {
+        double av[4][RPI];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < RPI; ++q)
+            av[u][q] = (i0 + u < na && t + q * NT < nrows) ? A[t + q * NT + (int64_t)(i0 + u) * lda] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (i0 + u >= na) break;
+#pragma unroll
+          for (int j = 0; j < Q; ++j)
+            if (j < nx) {
+              const double c = Cm[(i0 + u) * nx + j];
+#pragma unroll
+              for (int q = 0; q < RPI; ++q) acc[q][j] += av[u][q] * c;
+            }
+        }
+      }
+    } else {
 #pragma unroll 8
     for (int i = 0; i < na; ++i) {
       double a[RPI];
@@ -332,6 +355,7 @@ __device__ __forceinline__ void rows_sub_t(double* __restrict__ X, int64_t ldx, 
 #pragma unroll
           for (int q = 0; q < RPI; ++q) acc[q][j] += a[q] * c;
         }
+    }
     }
 #pragma unroll
     for (int j = 0; j < Q; ++j)
