@@ -318,6 +318,12 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     const int gt = tid - 32 * WOFF;
     const int st = fi * p;
     const int pcn = (n_t - st) < p ? (n_t - st) : p;
+    // squared column norms accumulated by the batched generation (global rows;
+    // same rows per thread in the same order as the separate pass below)
+    double vgen[Q];
+#pragma unroll
+    for (int s = 0; s < Q; ++s) vgen[s] = 0.0;
+    bool have_vgen = false;
     if (a.yext) {
       const double* ye = a.yext + r0 + (int64_t)(st - a.flush0 * p) * a.ldyext;
       for (int i = gt; i < m_loc; i += 32 * GW) {
@@ -379,12 +385,14 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
                   yy = tv[h] * yy + rs[h] * acc[h][s];
                   if (fabs(yy) < a.ftz) yy = 0.0;
                   Yl[i + (int64_t)s * ldy] = yy;
+                  vgen[s] += yy * yy;
                 }
               }
               yp[i] = yy;
             }
           }
         }
+        have_vgen = true;
       } else {
       for (int i = gt; i < m_loc; i += 32 * GW) {
         double acc[Q];
@@ -428,12 +436,13 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(const __grid_constant__ Sw
     {
       double v[Q];
 #pragma unroll
-      for (int s = 0; s < Q; ++s) v[s] = 0.0;
-      for (int i = gt; i < m_loc; i += 32 * GW) {
+      for (int s = 0; s < Q; ++s) v[s] = vgen[s];
+      if (!have_vgen)
+        for (int i = gt; i < m_loc; i += 32 * GW) {
 #pragma unroll
-        for (int s = 0; s < Q; ++s)
-          if (s < pcn) { const double y = Yl[i + (int64_t)s * ldy]; v[s] += y * y; }
-      }
+          for (int s = 0; s < Q; ++s)
+            if (s < pcn) { const double y = Yl[i + (int64_t)s * ldy]; v[s] += y * y; }
+        }
 #pragma unroll
       for (int s = 0; s < Q; ++s) v[s] = warp_sum(v[s]);
       double* red = sRed;  // GW * Q <= NWARP * PMAX doubles (unused by the Jacobi warps)
