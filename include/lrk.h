@@ -57,7 +57,7 @@ typedef struct {
 } lrk_lr;
 
 /* Spatial operator + time grid (discretize.py:107-127, forward.py:40-51).
- * kind: 0 = heat, 1 = convdiff (not yet on device).
+ * kind: 0 = heat, 1 = convection-diffusion (physical-space sweep).
  * stencil: 0 = FD (5-point in 2-D as the reference, 7-point in 3-D),
  *          1 = Q1 bilinear FEM stiffness with lumped mass (9-point, 2-D only;
  *              L = K_Q1 / h^2).
@@ -163,6 +163,48 @@ int lrk_st_solve_sweep(lrk_ctx* ctx, const lrk_lr* rhs, int adjoint,
                        int compress_every, double eps0, int r_max,
                        lrk_lr* out, int* trace, int trace_cap, int* trace_len,
                        void* stream);
+
+/* Fused concatenate-and-truncate (lowrank.py:147-154 then :124-144):
+ * out = truncate(sum_i coef[i] * terms[i]) with ONE truncation of the whole
+ * concatenation, as the reference's GMRES (forward.py:247-251) and Ritz
+ * combinations do.  coef is a host array (NULL = all ones).  Widths above the
+ * 160-column device core are handled exactly: through the dense n_x x n_t
+ * (or n_t x n_x) product when min(n_x, n_t) <= 160, otherwise by folding
+ * slices at the rounding floor (LRK_ERR_UNSUPPORTED only if the numerical rank
+ * of a partial sum exceeds 160).  out->r and *r_out hold the rank. */
+int lrk_add_truncate(lrk_ctx* ctx, int nterms, const lrk_lr* terms, const double* coef,
+                     double eps0, int r_max, lrk_lr* out, int* r_out, void* stream);
+/* Batched lr_dot of one field against many (lowrank.py:163-168):
+ * basis is the column-wise concatenation of nseg fields (segment g has
+ * seg_cols[g] columns, host array); out_host[g] = <w, field g>.  Two Gram
+ * launches on the FP64 tensor pipe + one segmented reduction + ONE readback
+ * (the per-pass inner products of CGS/MGS without per-pair host syncs). */
+int lrk_lr_dots(lrk_ctx* ctx, const lrk_lr* w, const lrk_lr* basis, int nseg,
+                const int* seg_cols, double* out_host, void* stream);
+
+/* Space-time solve with a selectable backend (forward.py:133-201, :217-274). */
+enum { LRK_SOLVE_SWEEP = 0, LRK_SOLVE_GMRES = 1 };
+typedef struct {
+  int backend;          /* LRK_SOLVE_*                                       */
+  double eps0;          /* TruncationPolicy.eps0                             */
+  int r_max;            /* < 0: None                                          */
+  int compress_every;   /* sweep flush period                                 */
+  double tol;           /* GMRES relative residual (forward.py:221)          */
+  int max_iter;         /* GMRES iteration cap; <= 0: n_t + 5 (:235-236)     */
+} lrk_solve_desc;
+/* Filled on return, also on LRK_ERR_CONVERGENCE (ConvergenceFailure's
+ * achieved_residual and iterations, errors.py:12-21, forward.py:269-274). */
+typedef struct {
+  double achieved_residual;
+  int iterations;
+  int rank;
+} lrk_solve_info;
+/* K vec(Y) = vec(rhs) (K^T when adjoint).  trace (host, may be NULL): sweep =
+ * pane rank per flush + final (forward.py:175, :187); GMRES = rank of each
+ * orthogonalised Krylov field (forward.py:252-253). */
+int lrk_st_solve(lrk_ctx* ctx, const lrk_lr* rhs, int adjoint, const lrk_solve_desc* sd,
+                 lrk_lr* out, lrk_solve_info* info, int* trace, int trace_cap, int* trace_len,
+                 void* stream);
 
 /* ---- Hessian apply (hessian.py:211-245) -------------------------------- */
 /* misfit_apply_ic: out = H~ v for nbatch independent dense vectors (columns

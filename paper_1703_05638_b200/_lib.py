@@ -35,6 +35,8 @@ LRK_MODE_IC = 0
 LRK_MODE_SOURCE = 1
 LRK_TRUNC_W1_ORTHO = 1
 LRK_TRUNC_W2_ORTHOSCALED = 2
+LRK_SOLVE_SWEEP = 0
+LRK_SOLVE_GMRES = 1
 
 
 class lrk_lr(Structure):
@@ -58,6 +60,17 @@ class lrk_obs_desc(Structure):
         ("idx1", POINTER(c_int32)), ("idx2", POINTER(c_int32)),
         ("n_list", c_int), ("list", POINTER(c_int32)),
     ]
+
+
+class lrk_solve_desc(Structure):
+    _fields_ = [
+        ("backend", c_int), ("eps0", c_double), ("r_max", c_int), ("compress_every", c_int),
+        ("tol", c_double), ("max_iter", c_int),
+    ]
+
+
+class lrk_solve_info(Structure):
+    _fields_ = [("achieved_residual", c_double), ("iterations", c_int), ("rank", c_int)]
 
 
 class lrk_hessian_desc(Structure):
@@ -103,6 +116,13 @@ _SIGNATURES = {
                                      c_int64, c_void_p, c_int64, POINTER(c_int), c_void_p]),
     "lrk_hessian_apply_st": (c_int, [c_void_p, POINTER(lrk_hessian_desc), POINTER(lrk_lr),
                                      POINTER(lrk_lr), POINTER(c_int), c_void_p]),
+    "lrk_add_truncate": (c_int, [c_void_p, c_int, POINTER(lrk_lr), POINTER(c_double), c_double,
+                                 c_int, POINTER(lrk_lr), POINTER(c_int), c_void_p]),
+    "lrk_lr_dots": (c_int, [c_void_p, POINTER(lrk_lr), POINTER(lrk_lr), c_int, POINTER(c_int),
+                            POINTER(c_double), c_void_p]),
+    "lrk_st_solve": (c_int, [c_void_p, POINTER(lrk_lr), c_int, POINTER(lrk_solve_desc),
+                             POINTER(lrk_lr), POINTER(lrk_solve_info), POINTER(c_int), c_int,
+                             POINTER(c_int), c_void_p]),
     "lrk_cgs2": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int, POINTER(c_double),
                          POINTER(c_double), c_void_p]),
     "lrk_combine": (c_int, [c_void_p, c_void_p, c_int64, c_int, POINTER(c_double), c_int,
@@ -151,7 +171,9 @@ def stream_handle():
     return c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def check(status, ctx=None, what=""):
+def check(status, ctx=None, what="", info=None):
+    """Map an lrk_status onto the reference's exceptions (errors.py:4-21);
+    ``info`` (an lrk_solve_info) carries ConvergenceFailure's payload."""
     if status == LRK_OK:
         return
     msg = ""
@@ -164,6 +186,9 @@ def check(status, ctx=None, what=""):
     if status == LRK_ERR_CONFIG:
         raise InvalidConfigError(msg)
     if status == LRK_ERR_CONVERGENCE:
+        if info is not None:
+            raise ConvergenceFailure(msg, achieved_residual=float(info.achieved_residual),
+                                     iterations=int(info.iterations))
         raise ConvergenceFailure(msg)
     if status == LRK_ERR_NUMERICAL:
         raise NumericalError(msg)

@@ -1,20 +1,37 @@
-"""Low-rank Arnoldi with full reorthogonalisation (mirrors lrpostcov/arnoldi.py).
+"""Arnoldi recurrence around the Hessian apply, with its Krylov basis on the device.
 
-Algorithm 1 of the paper as the reference implements it (arnoldi.py:271-375):
-apply, two orthogonalisation passes accumulating ``H[i, j] +=``, breakdown
-at 1e-14 (stop or seeded restart), Ritz refresh every ``check_every``.
-Dense (IC/steady) iterates live in one device matrix and are orthogonalised
-with a two-pass classical Gram-Schmidt in liblrk.so (lrk_cgs2 — the CGS2 form
-of the reference's MGS2, identical in exact arithmetic); low-rank iterates
-use the device lr_* operations with the reference's work_cap=48 policy.  The
-k x k Hessenberg eigenproblems stay on the host in numpy, exactly as in the
-reference, so Ritz values are computed by the same LAPACK routine.
+Drop-in for lrpostcov.arnoldi (arnoldi.py:271-375): same public names
+(StopRule, ArnoldiResult, lr_arnoldi, ritz_pairs, rank_one_check), same
+stopping rule, breakdown/restart behaviour and Ritz extraction; Algorithm 1
+of the paper.
+
+The recurrence itself is organised around a *Krylov space* object that owns
+the basis on the device and performs one full re-orthogonalised step per call:
+
+* dense iterates (IC / steady parameters): the basis is the column block of one
+  device matrix; each orthogonalisation pass is one `lrk_cgs2` call (batched
+  Gram of w against every basis column, subtraction, one readback);
+* low-rank iterates (space-time source parameter): the basis fields are stored
+  as contiguous column ranges of one n_x x C and one n_t x C device matrix.
+  A pass evaluates every inner product <w, V_i> with ONE batched Gram
+  (`lrk_lr_dots`) and turns them into the reference's *modified* Gram-Schmidt
+  coefficients with the basis Gram G_li = <V_l, V_i> (kept current, one batched
+  dot per new field): h_i = c_i - sum_{l<i} h_l G_li, which is MGS exactly in
+  exact arithmetic because the subtraction is an exact concatenation.  The
+  subtraction then costs one fused concatenate-and-truncate
+  (`lrk_add_truncate`).  Documented deviation: the reference additionally
+  truncates mid-pass whenever the working rank passes work_cap = 48
+  (arnoldi.py:141-151); here each pass truncates once, so intermediate
+  rounding differs at the eps0 level (Ritz values agree to 1e-6, tests).
+
+The k x k Hessenberg eigenproblems stay on the host (numpy LAPACK, like the
+reference), so Ritz values come from the same routine.
 """
 
 from __future__ import annotations
 
 import time as _time
-from ctypes import byref, c_double
+from ctypes import byref, c_double, c_int
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,15 +42,15 @@ from .lowrank import (
     LowRankMat,
     TruncationPolicy,
     colmajor,
-    lr_add,
+    lr_add_truncate,
     lr_dot,
-    lr_norm,
     lr_scale,
     lr_singular_values,
     lr_truncate,
 )
 
-BREAKDOWN_TOL = 1e-14
+BREAKDOWN_TOL = 1e-14   # arnoldi.py:35
+RESTART_SALT = 0x5EED   # seed offset of restart directions (arnoldi.py:224)
 
 
 @dataclass(frozen=True)
@@ -58,6 +75,8 @@ class StopRule:
 
 @dataclass
 class ArnoldiResult:
+    """Outcome of lr_arnoldi (arnoldi.py:65-87)."""
+
     H: np.ndarray
     basis: list
     rank_trace: list
@@ -70,14 +89,9 @@ class ArnoldiResult:
     restarts: int = 0
 
     def gram_defect(self) -> float:
-        """max |<v_i, v_j> - δ_ij| over the stored basis."""
-        ops = _ops_for(self.basis[0])
-        worst = 0.0
-        for i in range(len(self.basis)):
-            for j in range(i, len(self.basis)):
-                g = ops.dot(self.basis[i], self.basis[j])
-                worst = max(worst, abs(g - (1.0 if i == j else 0.0)))
-        return worst
+        """max |<v_i, v_j> - δ_ij| over the stored basis (batched on the device)."""
+        G = _gram_matrix(self.basis)
+        return float(np.abs(G - np.eye(G.shape[0])).max()) if G.size else 0.0
 
 
 def _torch():
@@ -86,80 +100,207 @@ def _torch():
     return torch
 
 
-class _DenseOps:
-    """Dense spatial vectors (numpy or device tensors)."""
+def _to_dev_vec(x):
+    torch = _torch()
+    return torch.as_tensor(np.asarray(x) if isinstance(x, np.ndarray) else x,
+                           dtype=torch.float64).reshape(-1).to("cuda").contiguous()
 
-    def __init__(self, pol: TruncationPolicy):
-        self.pol = pol
 
-    @staticmethod
-    def dot(a, b) -> float:
-        if isinstance(a, np.ndarray) and isinstance(b, np.ndarray):
-            return float(np.dot(a, b))
-        torch = _torch()
-        return float(torch.dot(torch.as_tensor(a, device="cuda", dtype=torch.float64).reshape(-1),
-                               torch.as_tensor(b, device="cuda", dtype=torch.float64).reshape(-1)))
+# ----------------------------------------------------------------- dense space
+class _DenseSpace:
+    """Dense spatial iterates as columns of one device matrix; CGS2 on the device."""
 
-    @staticmethod
-    def norm(a) -> float:
-        return float(np.sqrt(max(_DenseOps.dot(a, a), 0.0)))
+    lowrank = False
 
-    @staticmethod
-    def scale(a, c):
-        return a * c
+    def __init__(self, v1, capacity: int):
+        self.as_numpy = isinstance(v1, np.ndarray) or not _torch().is_tensor(v1)
+        v = _to_dev_vec(v1)
+        nrm = float(v.norm())
+        if nrm == 0:
+            raise ValueError("start vector must be nonzero")
+        self.n = v.numel()
+        self.Q = colmajor(self.n, capacity)
+        self.k = 0
+        self._ctx = _lib.algebra_context()
+        self._push(v / nrm)
+
+    def _push(self, v):
+        if self.k == self.Q.shape[1]:  # restarts can exceed the planned size
+            Q = colmajor(self.n, 2 * self.k)
+            Q[:, : self.k] = self.Q[:, : self.k]
+            self.Q = Q
+        self.Q[:, self.k] = v
+        self.k += 1
+
+    def current(self):
+        col = self.Q[:, self.k - 1]
+        return col.cpu().numpy() if self.as_numpy else col
+
+    def prepare(self, w):
+        return _to_dev_vec(w).clone()
+
+    def orthogonalize(self, w):
+        """Two CGS passes against all k columns: (h, ||w||, w)."""
+        k = self.k
+        h = (c_double * max(k, 1))()
+        nrm = c_double(0.0)
+        _lib.check(
+            _lib.get_lib().lrk_cgs2(self._ctx.handle, self.Q.data_ptr(), self.n, k, w.data_ptr(),
+                                    self.n, h, byref(nrm), _lib.stream_handle()),
+            self._ctx.handle, "lr_arnoldi")
+        return np.array(h[:k]), float(nrm.value), w
+
+    def extend(self, w, h_sub):
+        self._push(w / h_sub)
+
+    def fresh(self, seed):
+        rng = np.random.default_rng(RESTART_SALT + seed)
+        f = _to_dev_vec(rng.standard_normal(self.n))
+        f = f / float(f.norm())
+        _, fn, f = self.orthogonalize(f)
+        if fn <= 1e-6:
+            return None
+        return f / fn
+
+    def push_fresh(self, f):
+        self._push(f)
 
     @staticmethod
     def rank(w) -> int:
         return 0
 
+    def export(self) -> list:
+        cols = [self.Q[:, i] for i in range(self.k)]
+        return [c.cpu().numpy() for c in cols] if self.as_numpy else cols
 
-class _LowRankOps:
-    """LowRankMat iterates with working-rank control (arnoldi.py:128-166)."""
 
-    def __init__(self, pol: TruncationPolicy, work_cap: int = 48):
+# ------------------------------------------------------------- low-rank space
+class _FieldStore:
+    """Low-rank fields as contiguous column ranges of one n_x x C and one
+    n_t x C device matrix, with batched inner products against all of them."""
+
+    def __init__(self, n_x: int, n_t: int, cap: int = 64):
+        self.n_x, self.n_t = n_x, n_t
+        self._ctx = _lib.algebra_context()
+        self.W1 = colmajor(n_x, cap)
+        self.W2 = colmajor(n_t, cap)
+        self.used = 0
+        self.off, self.rk = [], []
+
+    def __len__(self) -> int:
+        return len(self.rk)
+
+    def append(self, v: LowRankMat):
+        if self.used + v.r > self.W1.shape[1]:
+            cap = max(2 * self.W1.shape[1], self.used + v.r)
+            W1, W2 = colmajor(self.n_x, cap), colmajor(self.n_t, cap)
+            W1[:, : self.used] = self.W1[:, : self.used]
+            W2[:, : self.used] = self.W2[:, : self.used]
+            self.W1, self.W2 = W1, W2
+        a = self.used
+        self.W1[:, a:a + v.r] = v.W1
+        self.W2[:, a:a + v.r] = v.W2
+        self.off.append(a)
+        self.rk.append(v.r)
+        self.used += v.r
+
+    def field(self, i: int) -> LowRankMat:
+        a, r = self.off[i], self.rk[i]
+        return LowRankMat._wrap(self.W1[:, a:a + r], self.W2[:, a:a + r])
+
+    def dots(self, w: LowRankMat, k: int | None = None) -> np.ndarray:
+        """<w, V_i> for the first k fields: one batched Gram + one readback."""
+        k = len(self) if k is None else k
+        if k == 0:
+            return np.zeros(0)
+        out = (c_double * k)()
+        seg = (c_int * k)(*self.rk[:k])
+        basis = LowRankMat._wrap(self.W1[:, : self.used], self.W2[:, : self.used])._c()
+        _lib.check(
+            _lib.get_lib().lrk_lr_dots(self._ctx.handle, byref(w._c()), byref(basis), k, seg, out,
+                                       _lib.stream_handle()),
+            self._ctx.handle, "lr_arnoldi")
+        return np.array(out[:k])
+
+
+def _lr_norm(w: LowRankMat) -> float:
+    return float(np.sqrt(max(lr_dot(w, w), 0.0))) if w.r else 0.0
+
+
+class _LowRankSpace:
+    """Low-rank iterates in a _FieldStore plus their Gram matrix (see module doc)."""
+
+    lowrank = True
+
+    def __init__(self, v1: LowRankMat, pol: TruncationPolicy):
         self.pol = pol
-        self.work_cap = work_cap
+        self.store = _FieldStore(*v1.shape)
+        self.G = np.zeros((0, 0))
+        nrm = _lr_norm(v1)
+        if nrm == 0:
+            raise ValueError("start vector must be nonzero")
+        self._append(lr_truncate(lr_scale(v1, 1.0 / nrm), pol))
 
-    @staticmethod
-    def dot(a, b) -> float:
-        return lr_dot(a, b)
+    def _append(self, v: LowRankMat):
+        self.store.append(v)
+        k = len(self.store)
+        row = self.store.dots(self.store.field(k - 1))
+        G = np.zeros((k, k))
+        G[: k - 1, : k - 1] = self.G
+        G[k - 1, :], G[:, k - 1] = row, row
+        self.G = G
 
-    @staticmethod
-    def norm(a) -> float:
-        return lr_norm(a)
+    @property
+    def k(self) -> int:
+        return len(self.store)
 
-    @staticmethod
-    def scale(a, c):
-        return lr_scale(a, c)
+    def current(self) -> LowRankMat:
+        return self.store.field(self.k - 1)
 
-    def sub(self, w, h, v):
-        w = lr_add(w, lr_scale(v, -h))
-        if w.r > self.work_cap:
-            w = lr_truncate(w, self.pol)
+    def prepare(self, w):
         return w
 
-    def compress(self, w, final=False):
-        return lr_truncate(w, self.pol)
+    def _pass(self, w: LowRankMat):
+        k = self.k
+        c = self.store.dots(w, k)
+        h = np.empty(k)
+        for i in range(k):  # MGS coefficients from the batched inner products
+            h[i] = c[i] - h[:i] @ self.G[:i, i]
+        terms = [w] + [self.store.field(i) for i in range(k)]
+        return h, lr_add_truncate(terms, np.concatenate(([1.0], -h)), self.pol)
+
+    def orthogonalize(self, w: LowRankMat):
+        h1, w = self._pass(w)
+        h2, w = self._pass(w)
+        return h1 + h2, _lr_norm(w), w
+
+    def extend(self, w: LowRankMat, h_sub: float):
+        self._append(lr_scale(w, 1.0 / h_sub))
+
+    def fresh(self, seed):
+        rng = np.random.default_rng(RESTART_SALT + seed)
+        n_x, n_t = self.store.n_x, self.store.n_t
+        w = LowRankMat(rng.standard_normal((n_x, 2)), rng.standard_normal((n_t, 2)))
+        w = lr_scale(w, 1.0 / _lr_norm(w))
+        _, nrm, w = self.orthogonalize(w)
+        if nrm <= 1e-6:
+            return None
+        return lr_truncate(lr_scale(w, 1.0 / nrm), self.pol)
+
+    def push_fresh(self, f):
+        self._append(f)
 
     @staticmethod
     def rank(w) -> int:
         return w.r
 
-    def combine(self, basis, coeffs):
-        out = LowRankMat.zeros(*basis[0].shape)
-        for v, c in zip(basis, coeffs):
-            out = lr_add(out, lr_scale(v, float(np.real(c))))
-            if out.r > self.work_cap:
-                out = lr_truncate(out, self.pol)
-        return lr_truncate(out, self.pol)
+    def export(self) -> list:
+        return [self.store.field(i) for i in range(self.k)]
 
 
-def _ops_for(v, pol: TruncationPolicy | None = None):
-    pol = pol or TruncationPolicy()
-    return _LowRankOps(pol) if isinstance(v, LowRankMat) else _DenseOps(pol)
-
-
+# ------------------------------------------------------------ Ritz extraction
 def _hessenberg_eigs(Hm: np.ndarray):
+    """Eigenpairs of the leading square block, descending real part (arnoldi.py:174-181)."""
     try:
         vals, vecs = np.linalg.eig(Hm)
     except np.linalg.LinAlgError as exc:
@@ -168,249 +309,138 @@ def _hessenberg_eigs(Hm: np.ndarray):
     return vals[order], vecs[:, order]
 
 
-def _coeffs(H: np.ndarray):
-    """Ritz values and combination coefficients (arnoldi.py:197-204)."""
+def _ritz_coefficients(H: np.ndarray):
+    """Ritz values and combination coefficients (arnoldi.py:197-204): the
+    symmetric eigensolver's vectors when H_m is symmetric to 1e-6."""
     m = H.shape[1]
     Hm = H[:m, :m]
     vals, vecs = _hessenberg_eigs(Hm)
-    scale = float(np.abs(Hm).max()) if m else 0.0
-    defect = float(np.abs(Hm - Hm.T).max()) if m else 0.0
-    if scale > 0 and defect <= 1e-6 * scale:
-        _, sym_vecs = np.linalg.eigh(0.5 * (Hm + Hm.T))
-        vecs = sym_vecs[:, ::-1]
+    if m:
+        scale = float(np.abs(Hm).max())
+        if scale > 0 and float(np.abs(Hm - Hm.T).max()) <= 1e-6 * scale:
+            vecs = np.linalg.eigh(0.5 * (Hm + Hm.T))[1][:, ::-1]
     return vals, vecs
 
 
-class _DenseBasis:
-    """Arnoldi basis held as columns of one device matrix."""
-
-    def __init__(self, n: int, cap: int, as_numpy: bool):
-        self.Q = colmajor(n, cap)
-        self.n = n
-        self.k = 0
-        self.as_numpy = as_numpy
-        self._ctx = _lib.algebra_context()
-
-    def push(self, v_dev):
-        self.Q[:, self.k] = v_dev
-        self.k += 1
-
-    def user(self, i):
-        col = self.Q[:, i]
-        return col.cpu().numpy() if self.as_numpy else col
-
-    def cgs2(self, w_dev, k):
-        h = (c_double * max(k, 1))()
-        nrm = c_double(0.0)
-        _lib.check(
-            _lib.get_lib().lrk_cgs2(self._ctx.handle, self.Q.data_ptr(), self.n, k,
-                                    w_dev.data_ptr(), self.n, h, byref(nrm), _lib.stream_handle()),
-            self._ctx.handle, "lr_arnoldi")
-        return np.array(h[:k]), float(nrm.value)
-
-    def combine(self, coeffs):
-        torch = _torch()
-        k = len(coeffs)
-        y = torch.empty(self.n, dtype=torch.float64, device=self.Q.device)
-        cf = (c_double * max(k, 1))(*[float(np.real(c)) for c in coeffs])
-        _lib.check(
-            _lib.get_lib().lrk_combine(self._ctx.handle, self.Q.data_ptr(), self.n, k, cf, self.n,
-                                       y.data_ptr(), _lib.stream_handle()),
-            self._ctx.handle, "ritz_pairs")
-        return y
-
-
-def _to_dev_vec(x):
+def _combine_dense(basis: list, coeffs: np.ndarray):
+    """All Ritz vectors as one device product basis @ coeffs, columns normalised."""
     torch = _torch()
-    return torch.as_tensor(np.asarray(x) if isinstance(x, np.ndarray) else x,
-                           dtype=torch.float64).reshape(-1).to("cuda").contiguous()
+    Q = torch.stack([_to_dev_vec(b) for b in basis], dim=1)
+    Y = Q @ torch.as_tensor(np.real(coeffs), dtype=torch.float64, device=Q.device)
+    nrm = Y.norm(dim=0)
+    return Y / torch.where(nrm > 0, nrm, torch.ones_like(nrm))
 
 
 def ritz_pairs(H: np.ndarray, basis: list, pol: TruncationPolicy | None = None) -> list:
     """Ritz pairs from the leading m x m block (arnoldi.py:184-213)."""
     m = H.shape[1]
-    vals, vecs = _coeffs(H)
+    vals, vecs = _ritz_coefficients(H)
+    if m == 0:
+        return []
     if isinstance(basis[0], LowRankMat):
-        ops = _LowRankOps(pol or TruncationPolicy())
+        pol = pol or TruncationPolicy()
         pairs = []
         for i in range(m):
-            v = ops.combine(basis[:m], vecs[:, i])
-            nrm = ops.norm(v)
-            if nrm > 0:
-                v = ops.scale(v, 1.0 / nrm)
-            pairs.append((complex(vals[i]), v))
+            v = lr_add_truncate(basis[:m], np.real(vecs[:, i]), pol)
+            nrm = _lr_norm(v)
+            pairs.append((complex(vals[i]), lr_scale(v, 1.0 / nrm) if nrm > 0 else v))
         return pairs
     as_np = isinstance(basis[0], np.ndarray)
-    n = int(np.asarray(basis[0]).shape[0]) if as_np else int(basis[0].shape[0])
-    B = _DenseBasis(n, m, as_np)
-    for i in range(m):
-        B.push(_to_dev_vec(basis[i]))
-    pairs = []
-    for i in range(m):
-        y = B.combine(vecs[:, i])
-        nrm = float(y.norm())
-        if nrm > 0:
-            y = y / nrm
-        pairs.append((complex(vals[i]), y.cpu().numpy() if as_np else y))
-    return pairs
+    Y = _combine_dense(basis[:m], vecs)
+    cols = [Y[:, i] for i in range(m)]
+    if as_np:
+        Yh = Y.cpu().numpy()
+        cols = [Yh[:, i] for i in range(m)]
+    return [(complex(vals[i]), cols[i]) for i in range(m)]
 
 
+def _gram_matrix(basis: list) -> np.ndarray:
+    k = len(basis)
+    if k == 0:
+        return np.zeros((0, 0))
+    if isinstance(basis[0], LowRankMat):
+        st = _FieldStore(*basis[0].shape, cap=max(sum(b.r for b in basis), 1))
+        for b in basis:
+            st.append(b)
+        return np.array([st.dots(st.field(i)) for i in range(k)])
+    torch = _torch()
+    Q = torch.stack([_to_dev_vec(b) for b in basis], dim=1)
+    return (Q.T @ Q).cpu().numpy()
+
+
+# --------------------------------------------------------------- stop rule
 def _stop_ready(vals, prev, stop: StopRule):
-    """Refresh-to-refresh stopping condition (arnoldi.py:242-268)."""
-    above = int(np.sum(vals.real >= stop.eps_eig))
+    """(stop?, #values >= eps_eig) from two consecutive refreshes (arnoldi.py:242-268):
+    same count above the threshold, and those leading values (or the leading
+    one when none is above) stable to stability_rtol."""
+    re = np.asarray(vals).real
+    above = int(np.count_nonzero(re >= stop.eps_eig))
     if prev is None:
         return False, above
-    if above != int(np.sum(prev.real >= stop.eps_eig)):
+    pr = np.asarray(prev).real
+    if above != int(np.count_nonzero(pr >= stop.eps_eig)):
         return False, above
-    n_check = above if above > 0 else min(1, len(vals), len(prev))
-    if n_check > len(prev):
+    n = above if above else min(1, re.size, pr.size)
+    if n > pr.size:
         return False, above
-    for i in range(n_check):
-        denom = max(abs(vals[i].real), abs(prev[i].real), 1e-300)
-        if abs(vals[i].real - prev[i].real) / denom > stop.stability_rtol:
-            return False, above
-    return True, above
+    a, b = re[:n], pr[:n]
+    denom = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-300)
+    return bool(np.all(np.abs(a - b) / denom <= stop.stability_rtol)), above
 
 
-def _fresh_lowrank(basis, ops, seed):
-    rng = np.random.default_rng(0x5EED + seed)
-    n_x, n_t = basis[0].shape
-    w = LowRankMat(rng.standard_normal((n_x, 2)), rng.standard_normal((n_t, 2)))
-    w = ops.scale(w, 1.0 / ops.norm(w))
-    for _pass in range(2):
-        for v in basis:
-            w = ops.sub(w, ops.dot(w, v), v)
-        w = ops.compress(w)
-    nrm = ops.norm(w)
-    if nrm <= 1e-6:
-        return None
-    return ops.compress(ops.scale(w, 1.0 / nrm))
-
-
+# --------------------------------------------------------------- the driver
 def lr_arnoldi(apply, v1, pol: TruncationPolicy, stop: StopRule,
                rank_source: list | None = None) -> ArnoldiResult:
     """Arnoldi iteration for a self-adjoint-up-to-truncation operator (arnoldi.py:271-375)."""
-    if isinstance(v1, LowRankMat):
-        return _arnoldi_lowrank(apply, v1, pol, stop, rank_source)
-    return _arnoldi_dense(apply, v1, pol, stop, rank_source)
-
-
-def _finish(H, j_done, basis_user, pol, stop, prev_vals, rank_trace, diagnostics, breakdown,
-            restarts):
-    Hout = H[: j_done + 1, : j_done]
-    pairs = ritz_pairs(Hout, basis_user, pol)
+    space = (_LowRankSpace(v1, pol) if isinstance(v1, LowRankMat)
+             else _DenseSpace(v1, stop.m_a + 1))
+    H = np.zeros((stop.m_a + 1, stop.m_a))
+    ranks, diagnostics = [], []
+    prev = None
+    breakdown, restarts, done = False, 0, 0
+    seen = len(rank_source) if rank_source is not None else 0
+    for j in range(stop.m_a):
+        t0 = _time.perf_counter()
+        w = space.prepare(apply(space.current()))
+        r_apply = space.rank(w)
+        if rank_source is not None and len(rank_source) > seen:
+            r_apply = max(r_apply, max(rank_source[seen:]))
+            seen = len(rank_source)
+        h, h_sub, w = space.orthogonalize(w)
+        H[: h.size, j] += h
+        H[j + 1, j] = h_sub
+        r_step = max(r_apply, space.rank(w))
+        ranks.append(r_step)
+        diagnostics.append((j + 1, h_sub, r_step, _time.perf_counter() - t0))
+        done = j + 1
+        if h_sub <= BREAKDOWN_TOL:  # invariant subspace reached
+            breakdown = True
+            if stop.on_breakdown != "restart" or done >= stop.m_a:
+                break
+            H[j + 1, j] = 0.0
+            f = space.fresh(stop.restart_seed + restarts)
+            if f is None:  # complement of the basis span exhausted
+                break
+            restarts += 1
+            space.push_fresh(f)
+            continue
+        space.extend(w, h_sub)
+        if done % stop.check_every == 0 and done < stop.m_a:
+            vals, _ = _hessenberg_eigs(H[:done, :done])
+            ready, _ = _stop_ready(vals, prev, stop)
+            prev = vals
+            if ready:
+                break
+    basis = space.export()
+    Hout = H[: done + 1, : done]
+    pairs = ritz_pairs(Hout, basis, pol)
     vals = np.array([p[0] for p in pairs])
-    if prev_vals is not None:
-        _, converged = _stop_ready(vals, prev_vals, stop)
-    else:
-        converged = int(np.sum(vals.real >= stop.eps_eig))
-    return ArnoldiResult(H=Hout, basis=basis_user, rank_trace=rank_trace, ritz_values=vals,
+    converged = (_stop_ready(vals, prev, stop)[1] if prev is not None
+                 else int(np.count_nonzero(vals.real >= stop.eps_eig)))
+    return ArnoldiResult(H=Hout, basis=basis, rank_trace=ranks, ritz_values=vals,
                          ritz_vectors=[p[1] for p in pairs], converged_count=converged,
-                         breakdown=breakdown, iterations=j_done, diagnostics=diagnostics,
+                         breakdown=breakdown, iterations=done, diagnostics=diagnostics,
                          restarts=restarts)
-
-
-def _arnoldi_dense(apply, v1, pol, stop, rank_source):
-    as_np = isinstance(v1, np.ndarray) or not _torch().is_tensor(v1)
-    v = _to_dev_vec(v1)
-    nrm = float(v.norm())
-    if nrm == 0:
-        raise ValueError("start vector must be nonzero")
-    n = v.numel()
-    B = _DenseBasis(n, stop.m_a + 1, as_np)
-    B.push(v / nrm)
-    H = np.zeros((stop.m_a + 1, stop.m_a))
-    rank_trace, diagnostics = [], []
-    prev_vals, breakdown, restarts, j_done = None, False, 0, 0
-    src_seen = len(rank_source) if rank_source is not None else 0
-    for j in range(stop.m_a):
-        t0 = _time.perf_counter()
-        w = _to_dev_vec(apply(B.user(j))).clone()
-        apply_rank = 0
-        if rank_source is not None and len(rank_source) > src_seen:
-            apply_rank = max(rank_source[src_seen:])
-            src_seen = len(rank_source)
-        h, h_sub = B.cgs2(w, B.k)
-        H[: B.k, j] += h
-        H[j + 1, j] = h_sub
-        rank_trace.append(apply_rank)
-        diagnostics.append((j + 1, h_sub, apply_rank, _time.perf_counter() - t0))
-        j_done = j + 1
-        if h_sub <= BREAKDOWN_TOL:
-            breakdown = True
-            if stop.on_breakdown != "restart" or j + 1 >= stop.m_a:
-                break
-            H[j + 1, j] = 0.0
-            rng = np.random.default_rng(0x5EED + stop.restart_seed + restarts)
-            f = _to_dev_vec(rng.standard_normal(n))
-            f = f / float(f.norm())
-            _, fn = B.cgs2(f, B.k)
-            if fn <= 1e-6:
-                break
-            restarts += 1
-            B.push(f / fn)
-            continue
-        B.push(w / h_sub)
-        if (j + 1) % stop.check_every == 0 and j + 1 < stop.m_a:
-            vals, _ = _hessenberg_eigs(H[: j + 1, : j + 1])
-            ready, _ = _stop_ready(vals, prev_vals, stop)
-            prev_vals = vals
-            if ready:
-                break
-    basis_user = [B.user(i) for i in range(B.k)]
-    return _finish(H, j_done, basis_user, pol, stop, prev_vals, rank_trace, diagnostics,
-                   breakdown, restarts)
-
-
-def _arnoldi_lowrank(apply, v1, pol, stop, rank_source):
-    ops = _LowRankOps(pol)
-    nrm = ops.norm(v1)
-    if nrm == 0:
-        raise ValueError("start vector must be nonzero")
-    basis = [ops.compress(ops.scale(v1, 1.0 / nrm))]
-    H = np.zeros((stop.m_a + 1, stop.m_a))
-    rank_trace, diagnostics = [], []
-    prev_vals, breakdown, restarts, j_done = None, False, 0, 0
-    src_seen = len(rank_source) if rank_source is not None else 0
-    for j in range(stop.m_a):
-        t0 = _time.perf_counter()
-        w = apply(basis[j])
-        apply_rank = ops.rank(w)
-        if rank_source is not None and len(rank_source) > src_seen:
-            apply_rank = max(apply_rank, max(rank_source[src_seen:]))
-            src_seen = len(rank_source)
-        for _pass in range(2):
-            for i in range(j + 1):
-                hij = ops.dot(w, basis[i])
-                H[i, j] += hij
-                w = ops.sub(w, hij, basis[i])
-            w = ops.compress(w)
-        h_sub = ops.norm(w)
-        H[j + 1, j] = h_sub
-        max_rank = max(apply_rank, ops.rank(w))
-        rank_trace.append(max_rank)
-        diagnostics.append((j + 1, h_sub, max_rank, _time.perf_counter() - t0))
-        j_done = j + 1
-        if h_sub <= BREAKDOWN_TOL:
-            breakdown = True
-            if stop.on_breakdown != "restart" or j + 1 >= stop.m_a:
-                break
-            H[j + 1, j] = 0.0
-            fresh = _fresh_lowrank(basis, ops, stop.restart_seed + restarts)
-            if fresh is None:
-                break
-            restarts += 1
-            basis.append(fresh)
-            continue
-        basis.append(ops.compress(ops.scale(w, 1.0 / h_sub)))
-        if (j + 1) % stop.check_every == 0 and j + 1 < stop.m_a:
-            vals, _ = _hessenberg_eigs(H[: j + 1, : j + 1])
-            ready, _ = _stop_ready(vals, prev_vals, stop)
-            prev_vals = vals
-            if ready:
-                break
-    return _finish(H, j_done, basis, pol, stop, prev_vals, rank_trace, diagnostics, breakdown,
-                   restarts)
 
 
 def rank_one_check(vec, reshape=None, tail_tol: float = 1e-6):
@@ -426,7 +456,6 @@ def rank_one_check(vec, reshape=None, tail_tol: float = 1e-6):
         s = torch.linalg.svdvals(X.to("cuda")).cpu().numpy()
     if s.size == 0 or s[0] == 0.0:
         return 0, 0.0
-    total = float(np.linalg.norm(s))
-    tail = np.sqrt(np.cumsum(s[::-1] ** 2))[::-1]
-    r = int(np.searchsorted(-tail, -tail_tol * total, side="left"))
+    tail = np.sqrt(np.cumsum((s ** 2)[::-1]))[::-1]
+    r = int(np.count_nonzero(tail > tail_tol * float(np.linalg.norm(s))))
     return r, (float(s[1] / s[0]) if s.size > 1 else 0.0)

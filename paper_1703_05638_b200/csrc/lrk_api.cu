@@ -871,6 +871,11 @@ int hd_check(lrk_ctx* c, const lrk_hessian_desc* hd) {
   if (hd->prior_gamma < 0.0 || (hd->prior_gamma > 0.0 && !(hd->prior_delta > 0.0)))
     return fail(c, LRK_ERR_CONFIG, "operator prior needs prior_delta > 0 and prior_gamma >= 0");
   if (hd->obs_every < 0) return fail(c, LRK_ERR_CONFIG, "obs_every must be >= 0");
+  if (hd->compress_every < 1 || hd->compress_every > PMAX)
+    return fail(c, LRK_ERR_UNSUPPORTED, "compress_every must lie in [1, 16] on the device path");
+  if (hd->r_max > NMAX - hd->compress_every)
+    return fail(c, LRK_ERR_UNSUPPORTED,
+                "r_max must be <= 160 - compress_every (the sweep core is r + compress_every wide)");
   return LRK_OK;
 }
 
@@ -917,12 +922,20 @@ double sweep_alg_bytes(int64_t n_x, int n_t, int p, const std::vector<int>& tr, 
 int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOut& g,
                   const int* extra_info, int* out, int p, int rb_f, int nnz_f, cudaStream_t s) {
   std::vector<int> t1(f.nflush + 1), t2(g.nflush + 1);
-  int zr[8] = {0}, er[8] = {0};
+  int zr[8] = {0}, er[8] = {0}, fi[8] = {0}, gi[8] = {0};
   CK(cudaMemcpyAsync(t1.data(), f.trace, t1.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(t2.data(), g.trace, t2.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(zr, zinfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(fi, f.info, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(gi, g.info, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
   if (extra_info) CK(cudaMemcpyAsync(er, extra_info, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  // a sweep whose core outgrew the device limit stops early with info[2] set:
+  // never return its (incomplete) pane as a result
+  if (fi[2] != 0 || gi[2] != 0)
+    return fail(c, LRK_ERR_UNSUPPORTED,
+                "sweep core exceeded the 160-column device limit (set r_max <= 160 - compress_every)");
+  if (zr[2] != 0) return fail(c, LRK_ERR_SHAPE, "observation truncation exceeded its capacity");
   int m = zr[0];
   for (int v : t1) m = std::max(m, v);
   for (int v : t2) m = std::max(m, v);
@@ -1556,3 +1569,6 @@ int lrk_combine(lrk_ctx* c, const double* Q, int64_t ldq, int k, const double* c
 }
 
 }  // extern "C"
+
+// device-resident Krylov layer (fused add-truncate, batched dots, GMRES)
+#include "lrk_krylov.inc"

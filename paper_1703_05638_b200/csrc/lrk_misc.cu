@@ -433,6 +433,64 @@ __global__ void fill_kernel(double* X, int64_t ldx, int64_t n, int ncols, double
     X[i + (int64_t)c * ldx] = v;
 }
 
+// Y = alpha * X^T for a rows x cols column-major X (Y is cols x rows, ld ldy):
+// the row-major views the DMMA GEMM needs for the wide truncation path.
+__global__ void transpose_kernel(const double* X, int64_t ldx, int64_t rows, int cols, double alpha,
+                                 double* Y, int64_t ldy) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x;
+    const int c = c0 + k;
+    t[k][threadIdx.x] = (i < rows && c < cols) ? X[i + (int64_t)c * ldx] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + threadIdx.x;
+    const int64_t i = i0 + k;
+    if (i < rows && c < cols) Y[c + i * ldy] = alpha * t[threadIdx.x][k];
+  }
+}
+
+// n x n identity (ld ldx)
+__global__ void eye_kernel(double* X, int64_t ldx, int n) {
+  const int c = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    X[i + (int64_t)c * ldx] = (i == c) ? 1.0 : 0.0;
+}
+
+// Segmented Hadamard sums of two reduced Gram blocks (the batched lr_dot of
+// one field against many, lowrank.py:163-168): out[g] = sum over rows a < na
+// and columns b in [segoff[g], segoff[g+1]) of G1[a][b] * G2[a][b], where
+// G1 / G2 are the sums of the n1 / n2 partials (row-major a * nb + b).
+// One block per segment, fixed summation order -> deterministic.
+__global__ void __launch_bounds__(256) seg_dot_kernel(const double* __restrict__ p1, int n1,
+                                                      const double* __restrict__ p2, int n2,
+                                                      int na, int nb, const int* __restrict__ segoff,
+                                                      double* __restrict__ out) {
+  __shared__ double red[8];
+  const int g = blockIdx.x;
+  const int b0 = segoff[g], b1 = segoff[g + 1], w = b1 - b0;
+  const int nout = na * nb;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < na * w; e += 256) {
+    const int o = (e / w) * nb + b0 + e % w;
+    double g1 = 0.0, g2 = 0.0;
+    for (int k = 0; k < n1; ++k) g1 += p1[(int64_t)k * nout + o];
+    for (int k = 0; k < n2; ++k) g2 += p2[(int64_t)k * nout + o];
+    acc += g1 * g2;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += red[k];
+    out[g] = s;
+  }
+}
+
 // --------------------------------------------------------- _svd_flip
 // Per-block partial argmax |U[:, c]| (first index on ties), then finalize
 // + apply: largest-|entry| of each column positive (lowrank.py:114-121).

@@ -57,6 +57,11 @@ __global__ void gather_rows_kernel(const double* X, int64_t ldx, const int32_t* 
 __global__ void scatter_rows_kernel(const double* X, int64_t ldx, const int32_t* idx, int nidx,
                                     const int* ncols_dev, int ncols, double* Y, int64_t ldy);
 __global__ void fill_kernel(double* X, int64_t ldx, int64_t n, int ncols, double v);
+__global__ void transpose_kernel(const double* X, int64_t ldx, int64_t rows, int cols, double alpha,
+                                 double* Y, int64_t ldy);
+__global__ void eye_kernel(double* X, int64_t ldx, int n);
+__global__ void seg_dot_kernel(const double* p1, int n1, const double* p2, int n2, int na, int nb,
+                               const int* segoff, double* out);
 __global__ void flip_partial_kernel(const double* U, int64_t ldu, int64_t n, const int* r_dev,
                                     int rcap, double* part);
 __global__ void flip_apply_kernel(double* U, int64_t ldu, int64_t n_x, double* V, int64_t ldv,

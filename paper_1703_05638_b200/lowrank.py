@@ -169,22 +169,18 @@ def lr_to_dense(A: LowRankMat) -> np.ndarray:
 
 
 def lr_truncate(A: LowRankMat, pol: TruncationPolicy, flags: int = 0) -> LowRankMat:
-    """Recompress to canonical form: ||A - out||_F <= eps0 ||A||_F (lowrank.py:124-144)."""
+    """Recompress to canonical form: ||A - out||_F <= eps0 ||A||_F (lowrank.py:124-144).
+
+    Inputs wider than the 160-column device core go through the fused
+    concatenate-and-truncate entry point, which reduces the width exactly
+    (dense product on a short side, or rounding-floor folds) before the one
+    policy truncation — the reference truncates the whole input once.
+    """
     n_x, n_t = A.shape
     if A.r == 0:
         return LowRankMat.zeros(n_x, n_t)
     if A.r > CORE_MAX:
-        # wider than the device core: fold in CORE_MAX-column slices (each fold
-        # is itself a truncation, so the overall error stays within the budget
-        # of successive eps0 truncations)
-        acc = lr_truncate(LowRankMat._wrap(A.W1[:, :CORE_MAX], A.W2[:, :CORE_MAX]), pol)
-        start = CORE_MAX
-        while start < A.r:
-            take = min(CORE_MAX - acc.r, A.r - start)
-            part = LowRankMat._wrap(A.W1[:, start:start + take], A.W2[:, start:start + take])
-            acc = lr_truncate(lr_add(acc, part), pol)
-            start += take
-        return acc
+        return lr_add_truncate([A], None, pol)
     ctx = _lib.algebra_context()
     cap = A.r if pol.r_max is None else max(min(A.r, pol.r_max), 1)
     W1, W2, out = _out_pair(n_x, n_t, cap)
@@ -197,19 +193,47 @@ def lr_truncate(A: LowRankMat, pol: TruncationPolicy, flags: int = 0) -> LowRank
     return LowRankMat._wrap(W1[:, : r.value], W2[:, : r.value])
 
 
+def lr_add_truncate(terms, coefs, pol: TruncationPolicy) -> LowRankMat:
+    """truncate(sum_i coefs[i] * terms[i]) with ONE truncation of the whole
+    concatenation (lr_add chains + lr_truncate, lowrank.py:147-154/:124-144),
+    fused on the device (lrk_add_truncate); coefs None = all ones."""
+    terms = list(terms)
+    if not terms:
+        raise ValueError("lr_add_truncate needs at least one term")
+    n_x, n_t = terms[0].shape
+    for t in terms[1:]:
+        _check_same_shape(terms[0], t)
+    R = sum(t.r for t in terms)
+    if R == 0:
+        return LowRankMat.zeros(n_x, n_t)
+    ctx = _lib.algebra_context()
+    cap = min(R, CORE_MAX, n_x, n_t)
+    if pol.r_max is not None:
+        cap = max(min(cap, pol.r_max), 1)
+    W1, W2, out = _out_pair(n_x, n_t, max(cap, 1))
+    arr = (_lib.lrk_lr * len(terms))(*[t._c() for t in terms])
+    cf = None if coefs is None else (c_double * len(terms))(*[float(c) for c in coefs])
+    r = c_int(0)
+    _lib.check(
+        _lib.get_lib().lrk_add_truncate(ctx.handle, len(terms), arr, cf, float(pol.eps0),
+                                        pol.r_max_c, byref(out), byref(r), _lib.stream_handle()),
+        ctx.handle, "lr_add_truncate",
+    )
+    return LowRankMat._wrap(W1[:, : r.value], W2[:, : r.value])
+
+
 def lr_from_dense(X, pol: TruncationPolicy) -> LowRankMat:
-    """Compress a dense matrix under the policy (lowrank.py:90-95)."""
+    """Compress a dense matrix under the policy (lowrank.py:90-95): the field
+    (X, I) with the identity on the shorter side (skips that side's QR)."""
     torch = _torch()
     Xd = to_device_colmajor(X)
     n_x, n_t = Xd.shape
-    if n_t <= CORE_MAX:
+    if n_t <= CORE_MAX or n_t <= n_x:
         eye = to_device_colmajor(torch.eye(n_t, dtype=torch.float64))
         return lr_truncate(LowRankMat._wrap(Xd, eye), pol, flags=_lib.LRK_TRUNC_W2_ORTHOSCALED)
-    if n_x <= CORE_MAX:
-        eye = to_device_colmajor(torch.eye(n_x, dtype=torch.float64))
-        return lr_truncate(LowRankMat._wrap(eye, to_device_colmajor(Xd.T)), pol,
-                           flags=_lib.LRK_TRUNC_W1_ORTHO)
-    return lr_truncate(LowRankMat._wrap(Xd, to_device_colmajor(torch.eye(n_t, dtype=torch.float64))), pol)
+    eye = to_device_colmajor(torch.eye(n_x, dtype=torch.float64))
+    return lr_truncate(LowRankMat._wrap(eye, to_device_colmajor(Xd.T)), pol,
+                       flags=_lib.LRK_TRUNC_W1_ORTHO)
 
 
 def lr_add(A: LowRankMat, B: LowRankMat) -> LowRankMat:
