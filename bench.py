@@ -1,32 +1,41 @@
 #!/usr/bin/env python
-"""Benchmark: low-rank space-time Hessian matvecs/s on the C2 workload.
+"""Benchmark: low-rank space-time Hessian matvecs/s (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], the metric's config): 2-D heat equation on
-[0,1]^2, 256x256 interior grid (n_x = 65,536), n_t = 512, T = 1, implicit
-Euler, fp64; initial-condition parameter; 32x32 uniform point-sensor subgrid
-observed at every step; noise sigma = 0.01 (pointwise weight 1/sigma^2,
-SURVEY Appendix D1); prior (delta I + gamma L)^-2 with delta = 1, gamma = 0.05
-(square root applied on both sides); truncation eps0 =
-1e-8, rank cap 32; seed 1.  Operator: Q1 bilinear FEM stiffness with lumped
-mass (9-point stencil), exactly the config's discretisation.
+Default workload = C4 (BASELINE.json configs[3]), the largest configuration
+that fits one GPU: 3-D heat equation on [0,1]^3, 7-point FD 128^3 (n_x =
+2,097,152), n_t = 2048, T = 1, implicit Euler, fp64; initial-condition
+parameter; 32^3 point sensors (stride 4) observed every 4th step; noise sigma
+0.005 (pointwise weight 1/sigma^2); prior
+(delta I + gamma L)^-2 with delta 1, gamma 0.02 (square root on both sides,
+Appendix D4); truncation eps0 1e-8, rank cap 64; seed 3.  `--config C2`
+runs configs[1] (Q1 256^2, n_t 512, 32x32 sensors every step, sigma 0.01,
+gamma 0.05, r_max 32, seed 1) as a secondary line.
 
-One step = one prior-preconditioned misfit Hessian apply (forward sweep, obs,
-adjoint sweep; hessian.py:211-226) on a seeded N(0,1) unit probe already
-resident in HBM.  L2 is flushed (512 MiB write) before every timed step.
-Multi-GPU: every rank applies H~ to its own probes (independent units, no
-data-path collective) -> weak scaling; time = max over ranks.
+One step = one prior-preconditioned misfit Hessian apply (forward sweep,
+observation, adjoint sweep; hessian.py:211-226) on a seeded N(0,1) unit probe
+already resident in HBM; inputs are far larger than L2 and L2 is flushed
+(512 MiB write) before every timed step anyway.  `e2e` = the same applies
+through the public API (HessianContext.apply) from pinned HOST memory, the
+host->device copy and the device->host read of the result inside the
+perf_counter-timed region.
 
---impl reference times the reference algorithm on the host CPU (oracle/
-restatement, SuperLU + LAPACK, validated against the reference in
-tests/test_oracle_golden.py), all host cores as independent processes, each
-step a bounded prefix sample of the same apply (see _cpu_sample).
+CPU arms (the reference's algorithm on the host cores, oracle/ restatement,
+pinned to the reference in tests/test_oracle_golden.py): every host core runs
+one worker process with BLAS pinned to one thread (environment set before the
+workers start), the problem is built once per worker outside the timed
+region, and each timed unit advances every worker's own sweep by a bounded
+number of time steps; the rate is extrapolated to the 2 n_t steps of an apply.
+C2 uses the reference's own SuperLU step solves.  At C4 the reference cannot
+be set up (scipy splu of the 128^3 step matrix raises MemoryError),
+so its sweep runs with CG step solves to 1e-12 instead: "extrapolated,
+substitute solver".
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -38,30 +47,44 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_SIDE, N_T, SENSORS, SIGMA, EPS0, R_MAX, SEED, P_FLUSH = 256, 512, 32, 0.01, 1e-8, 32, 1, 4
-PRIOR_DELTA, PRIOR_GAMMA = 1.0, 0.05
-STENCIL = "q1"
-CPU_SAMPLE_STEPS = 32   # time steps per sweep in one CPU sample (of 512)
 L2_FLUSH_BYTES = 512 << 20
+METRIC = "low-rank space-time Hessian matvecs/s"
 
-WORKLOAD = ("C2: 2D heat 256x256 (n_x=65536), n_t=512, Q1 FEM (lumped mass, 9-point), IC "
-            "parameter, 32x32 point sensors every step, sigma=0.01 (w=1/sigma^2), prior "
-            "(I+0.05L)^-2, eps0=1e-8, r_max=32, compress_every=4, seed 1")
+CONFIGS = {
+    "C4": dict(n_side=128, dim=3, stencil="fd", n_t=2048, sensors=32, every=4, sigma=0.005,
+               delta=1.0, gamma=0.02, eps0=1e-8, r_max=64, seed=3, p=4,
+               cpu_solver="cg", cpu_steps_sample=4, cpu_steps_ref=1,
+               workload=("C4: 3D heat 128^3 (n_x=2097152), 7-point FD, n_t=2048, IC parameter, "
+                         "32^3 point sensors (stride 4) every 4th step, sigma=0.005 "
+                         "(w=1/sigma^2), prior (I+0.02L)^-2, eps0=1e-8, r_max=64, "
+                         "compress_every=4, seed 3")),
+    "C2": dict(n_side=256, dim=2, stencil="q1", n_t=512, sensors=32, every=1, sigma=0.01,
+               delta=1.0, gamma=0.05, eps0=1e-8, r_max=32, seed=1, p=4,
+               cpu_solver="splu", cpu_steps_sample=64, cpu_steps_ref=32,
+               workload=("C2: 2D heat 256x256 (n_x=65536), n_t=512, Q1 FEM (lumped mass, "
+                         "9-point), IC parameter, 32x32 point sensors every step, sigma=0.01 "
+                         "(w=1/sigma^2), prior (I+0.05L)^-2, eps0=1e-8, r_max=32, "
+                         "compress_every=4, seed 1")),
+}
 
 
-def problem_scalars():
-    h = 1.0 / (N_SIDE + 1)
-    tau = 1.0 / N_T
-    beta_noise = 1.0 / (SIGMA ** 2 * tau * h * h)  # w = beta_noise*tau*h^2 = 1/sigma^2
-    beta_prior = 1.0 / (h * h)  # unused by the apply; gamma_prior = 1 scales nothing
-    return h, tau, beta_noise, beta_prior
+def scalars(cfg):
+    h = 1.0 / (cfg["n_side"] + 1)
+    tau = 1.0 / cfg["n_t"]
+    m = h ** cfg["dim"]
+    beta_noise = 1.0 / (cfg["sigma"] ** 2 * tau * m)  # w = beta_noise tau M = 1/sigma^2
+    return h, tau, m, beta_noise
 
 
-def sensor_mask():
-    stride = N_SIDE // SENSORS
-    idx = stride // 2 + stride * np.arange(SENSORS)
-    mask = np.zeros(N_SIDE * N_SIDE, bool)
-    mask[(idx[:, None] * N_SIDE + idx[None, :]).ravel()] = True
+def sensor_mask(cfg):
+    n, s = cfg["n_side"], cfg["sensors"]
+    stride = n // s
+    idx = stride // 2 + stride * np.arange(s)
+    mask = np.zeros(n ** cfg["dim"], bool)
+    if cfg["dim"] == 3:
+        mask[(idx[:, None, None] * n * n + idx[None, :, None] * n + idx[None, None, :]).ravel()] = True
+    else:
+        mask[(idx[:, None] * n + idx[None, :]).ravel()] = True
     return mask
 
 
@@ -72,47 +95,100 @@ def probes(n, count, seed):
 
 
 # ------------------------------------------------------------------ CPU arm
-def _cpu_sample(args):
-    """One bounded sample of the reference apply: the C2 operator (same n_x,
-    tau = 1/512, sensors, weights) swept over CPU_SAMPLE_STEPS of the 512 time
-    steps in each direction.  Returns seconds; the matvec rate is extrapolated
-    linearly in n_t (cost per step is ~constant once the rank settles)."""
-    seed, reps = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+def _cpu_worker(conn, cfg, seed):
+    """One host core: builds the reference apply's operator and first sweep
+    once, then advances it by the requested number of time steps per command
+    (oracle.SweepStepper: forward.py:133-188 with its flushes)."""
     from oracle import lrk_oracle as O
 
-    h, tau, bn, bp = problem_scalars()
-    P = O.Problem(N_SIDE, CPU_SAMPLE_STEPS, sensor_mask(), bn, 1.0, EPS0, R_MAX,
-                  T=CPU_SAMPLE_STEPS * tau, stencil=STENCIL, prior=(PRIOR_DELTA, PRIOR_GAMMA))
-    v = probes(N_SIDE * N_SIDE, 1, seed)[:, 0]
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        O.hessian_ic(P, v)
-    return (time.perf_counter() - t0) / reps
+    h, tau, m, bn = scalars(cfg)
+    L, _, _ = O.config_operator(cfg["n_side"], cfg["dim"], cfg["stencil"])
+    n_t = cfg["n_t"]
+    if cfg["cpu_solver"] == "cg":
+        solver = O.CGStepSolver(L, m, tau, n_t)
+    else:
+        solver = O.StepSolver(L, m, tau, n_t)
+    v = probes(L.shape[0], 1, seed)[:, 0]
+    e0 = np.zeros((n_t, 1))
+    e0[0, 0] = 1.0
 
+    def fresh():
+        return O.SweepStepper(solver, (m * v)[:, None], e0, cfg["eps0"], cfg["r_max"], False,
+                              cfg["p"])
 
-def cpu_arm(steps: int, warmup: int, reps: int = 1):
-    import multiprocessing as mp
-
-    cores = len(os.sched_getaffinity(0))
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores, initializer=_limit_threads) as pool:
-        for _ in range(warmup):
-            pool.map(_cpu_sample, [(SEED + i, 1) for i in range(cores)])
+    st = fresh()
+    conn.send(("ready", len(os.sched_getaffinity(0))))
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
         t0 = time.perf_counter()
-        per = []
-        for _ in range(steps):
-            per += pool.map(_cpu_sample, [(SEED + i, reps) for i in range(cores)])
-        wall = time.perf_counter() - t0
-    frac = CPU_SAMPLE_STEPS / N_T
-    # aggregate: cores x steps x reps samples, each frac of a matvec
-    value = cores * steps * reps * frac / wall
-    return value, cores, float(np.median(per)), wall
+        for _ in range(int(msg)):
+            if st.done:
+                st = fresh()
+            st.step()
+        conn.send(time.perf_counter() - t0)
+    conn.close()
 
 
-def _limit_threads():
-    os.environ["OMP_NUM_THREADS"] = "1"
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+class CpuArm:
+    """All host cores as independent reference workers (one BLAS thread each)."""
+
+    def __init__(self, cfg, seed0):
+        import multiprocessing as mp
+
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = "1"  # inherited by the spawned workers before numpy loads
+        self.cores = len(os.sched_getaffinity(0))
+        ctx = mp.get_context("spawn")
+        self.conns, self.procs = [], []
+        for i in range(self.cores):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_cpu_worker, args=(b, cfg, seed0 + i), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        for c in self.conns:  # problem setup finished everywhere (untimed)
+            c.recv()
+        self.cfg = cfg
+
+    def run(self, steps_per_worker):
+        """Advance every worker by k time steps; (wall seconds, per-worker seconds)."""
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(steps_per_worker)
+        per = [c.recv() for c in self.conns]
+        return time.perf_counter() - t0, per
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send(None)
+            except Exception:
+                pass
+        for p in self.procs:
+            p.join(timeout=10)
+
+    def rate(self, wall, k, units=1):
+        """matvec/s: each worker did k of the 2 n_t sweep steps of one apply."""
+        return self.cores * units * k / (2.0 * self.cfg["n_t"]) / wall
+
+
+def cpu_baseline(cfg, seed0):
+    arm = CpuArm(cfg, seed0)
+    try:
+        k = cfg["cpu_steps_sample"]
+        wall, per = arm.run(k)
+        value = arm.rate(wall, k)
+    finally:
+        arm.close()
+    solver = "CG 1e-12 step solves (substitute: splu does not fit at this size)" \
+        if cfg["cpu_solver"] == "cg" else "SuperLU step solves (the reference's own)"
+    return {"value": value, "unit": "matvec/s", "cores": arm.cores, "kind": "port",
+            "sample": (f"{arm.cores} processes x {k} of the {2 * cfg['n_t']} sweep steps of one "
+                       f"apply each (reference sweep + flushes, {solver}; extrapolated linearly "
+                       f"to the full apply); median worker {statistics.median(per):.1f}s, "
+                       f"wall {wall:.1f}s")}
 
 
 # ------------------------------------------------------------------ helpers
@@ -214,6 +290,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 200"}
 
 
+
 def measured_hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -222,19 +299,46 @@ def measured_hbm_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the sweep kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+def build_hash():
+    """Hash of the CUDA sources of liblrk.so, to match ncu captures to builds."""
+    d = os.path.join(ROOT, "paper_1703_05638_b200", "csrc")
+    hsh = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".h", ".inc")):
+            with open(os.path.join(d, f), "rb") as fh:
+                hsh.update(fh.read())
+    return hsh.hexdigest()[:16]
+
+
+def ncu_traffic(config_name):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture of THIS build (profiles/ncu_sweep_<cfg>.json, written by
+    tools/ncu_summary.py); None when the capture is from another build."""
+    path = os.path.join(ROOT, "profiles", f"ncu_sweep_{config_name.lower()}.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("dram_bytes_per_launch"), d.get("source")
     except Exception:
-        return None, None
+        return None, "no capture"
+    if d.get("build") != build_hash():
+        return None, f"capture {os.path.basename(path)} is from build {d.get('build')}"
+    return d.get("dram_bytes_per_launch"), os.path.basename(path)
 
 
 # ------------------------------------------------------------------ GPU arm
-def gpu_arm(args, rank, world, local_rank):
+def make_context(cfg, lp):
+    h, tau, m, bn = scalars(cfg)
+    grid = lp.build_grid(cfg["n_side"], cfg["dim"])
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, cfg["stencil"]), lp.build_time_grid(cfg["n_t"]))
+    cov = lp.CovarianceSpec(beta_noise=bn, beta_prior=1.0, gamma_prior=1.0,
+                            prior_delta=cfg["delta"], prior_gamma=cfg["gamma"])
+    layout = lp.SensorLayout((), sensor_mask(cfg), time_every=cfg["every"])
+    return lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                             pol=lp.TruncationPolicy(cfg["eps0"], cfg["r_max"]),
+                             compress_every=cfg["p"]), grid
+
+
+def gpu_arm(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
@@ -243,16 +347,10 @@ def gpu_arm(args, rank, world, local_rank):
     from ctypes import byref, c_double, c_int64
 
     torch.cuda.set_device(local_rank)
-    h, tau, bn, bp = problem_scalars()
-    grid = lp.build_grid(N_SIDE)
-    K = lp.SpaceTimeOperator(lp.assemble_heat(grid, STENCIL), lp.build_time_grid(N_T))
-    cov = lp.CovarianceSpec(beta_noise=bn, beta_prior=bp, gamma_prior=1.0,
-                            prior_delta=PRIOR_DELTA, prior_gamma=PRIOR_GAMMA)
-    ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.SensorLayout((), sensor_mask()),
-                            cov=cov, pol=lp.TruncationPolicy(EPS0, R_MAX), compress_every=P_FLUSH)
+    ctx, grid = make_context(cfg, lp)
     nprobe = args.steps + args.warmup
-    V = probes(grid.n_x, nprobe, SEED * 1000 + rank)
-    Vd = torch.as_tensor(V, device="cuda").T.contiguous()  # resident in HBM
+    V = probes(grid.n_x, nprobe, cfg["seed"] * 1000 + rank)
+    Vd = torch.as_tensor(V, device="cuda").T.contiguous()  # resident in HBM, one row per probe
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     lib = _lib.get_lib()
     h_dev = ctx._dev.handle
@@ -283,82 +381,97 @@ def gpu_arm(args, rank, world, local_rank):
             ranks.append(ctx.rank_trace[-1])
         torch.cuda.synchronize()
     barrier()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
+    total_ms = float(sum(a.elapsed_time(b) for a, b in evs))
     launches = ctx._dev.launches() - launches0
     sw_ms, sw_n, sw_bytes = c_double(0), c_int64(0), c_double(0)
     lib.lrk_profile_read(h_dev, byref(sw_ms), byref(sw_n), byref(sw_bytes), 1)
     lib.lrk_profile_enable(h_dev, 0)
 
-    # ---------------- end-to-end through the public API with host buffers
+    # ---------------- end to end through the public API with host buffers
     vh = torch.empty(grid.n_x, dtype=torch.float64).pin_memory()
     oh = torch.empty(grid.n_x, dtype=torch.float64).pin_memory()
-    e2e_ev = []
+    srcs = [torch.from_numpy(np.ascontiguousarray(V[:, args.warmup + i])) for i in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
     t_e2e = time.perf_counter()
     for i in range(args.steps):
-        vh.copy_(torch.from_numpy(V[:, args.warmup + i]))
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        vh.copy_(srcs[i])
         out = ctx.apply(vh.to("cuda", non_blocking=True))
         oh.copy_(out, non_blocking=True)
-        b.record()
-        e2e_ev.append((a, b))
-    torch.cuda.synchronize()
-    t_e2e = time.perf_counter() - t_e2e
+        torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t_e2e
     barrier()
-    e2e_ms = float(sum(a.elapsed_time(b) for a, b in e2e_ev))
 
-    # max over ranks
-    stats = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device="cuda")
+    stats = torch.tensor([total_ms, e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    total_ms, e2e_ms = float(stats[0]), float(stats[1])
     return {
-        "total_ms": total_ms, "e2e_ms": e2e_ms, "launches": launches, "ranks": ranks,
-        "sweep_ms": sw_ms.value, "sweep_n": sw_n.value, "sweep_bytes": sw_bytes.value,
-        "clocks": clk.summary(), "n_x": grid.n_x, "e2e_wall_s": t_e2e,
+        "total_ms": float(stats[0]), "e2e_s": float(stats[1]), "launches": launches,
+        "ranks": ranks, "sweep_ms": sw_ms.value, "sweep_n": sw_n.value,
+        "sweep_bytes": sw_bytes.value, "clocks": clk.summary(), "n_x": grid.n_x,
     }
+
+
+def reference_arm(args, cfg, base):
+    """--impl reference: the reference algorithm on all host cores; each step
+    advances every worker's sweep by cpu_steps_ref time steps."""
+    arm = CpuArm(cfg, cfg["seed"] * 1000)
+    k = cfg["cpu_steps_ref"]
+    try:
+        for _ in range(args.warmup):
+            arm.run(k)
+        walls, pers = [], []
+        for _ in range(args.steps):
+            w, per = arm.run(k)
+            walls.append(w)
+            pers += per
+    finally:
+        arm.close()
+    wall = float(sum(walls))
+    value = arm.rate(wall, k, units=args.steps)
+    solver = "CG 1e-12 step solves (substitute: the reference's splu does not fit at C4)" \
+        if cfg["cpu_solver"] == "cg" else "SuperLU step solves (the reference's own)"
+    sample = (f"per step: {arm.cores} processes x {k} of the {2 * cfg['n_t']} sweep steps of one "
+              f"apply ({solver}); extrapolated linearly to the full apply; median worker "
+              f"{statistics.median(pers):.2f}s")
+    line = dict(base)
+    line.update({"value": value, "ms_per_step": 1e3 * wall / args.steps,
+                 "impl": "reference",
+                 "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": arm.cores,
+                                  "kind": "port", "sample": sample},
+                 "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    return line
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = {"workload": WORKLOAD, "n_x": N_SIDE * N_SIDE, "n_t": N_T, "rank_cap": R_MAX,
-           "eps0": EPS0, "parallelism": f"independent probes x{args.gpus} (replicas)",
-           "l2": "flushed before every timed step (512 MiB write)",
-           "solver_backend": "sweep (forward.py:133-188), DST-I eigenbasis"}
+    config = {"workload": cfg["workload"], "n_x": cfg["n_side"] ** cfg["dim"], "n_t": cfg["n_t"],
+              "rank_cap": cfg["r_max"], "eps0": cfg["eps0"],
+              "parallelism": f"independent probes x{args.gpus} (replicas)",
+              "l2": "inputs > L2; L2 also flushed before every timed step (512 MiB write)",
+              "solver_backend": "sweep (forward.py:133-188), DST-I eigenbasis"}
+    base = {"metric": METRIC, "unit": "matvec/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded N(0,1) unit probes)",
+            "config": config}
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        value, cores, med, wall = cpu_arm(args.steps, args.warmup)
-        sample = (f"per step: {cores} processes x 1 apply on the C2 operator over "
-                  f"{CPU_SAMPLE_STEPS}/{N_T} time steps per sweep (extrapolated linearly in n_t); "
-                  f"median sample {med:.2f}s")
-        line = {"metric": "low-rank space-time Hessian matvecs/s", "value": value,
-                "unit": "matvec/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded N(0,1) unit probes)", "config": cfg,
-                "impl": "reference",
-                "cpu_baseline": {"value": value, "unit": "matvec/s", "cores": cores,
-                                 "kind": "port", "sample": sample},
-                "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        if rank == 0:
+            print(json.dumps(reference_arm(args, cfg, base)))
         return
 
     import torch
@@ -366,40 +479,34 @@ def main():
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = gpu_arm(args, rank, world, local_rank)
+    res = gpu_arm(args, cfg, rank, world, local_rank)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        value, cores, med, wall = cpu_arm(1, 0)
-        cpu = {"value": value, "unit": "matvec/s", "cores": cores, "kind": "port",
-               "sample": f"{cores} processes x 1 reference apply over {CPU_SAMPLE_STEPS}/{N_T} "
-                         f"steps per sweep of the C2 operator (extrapolated in n_t); "
-                         f"median sample {med:.2f}s"}
+        cpu = cpu_baseline(cfg, 7000)
     if rank == 0:
         peak, peak_kind = measured_hbm_peak()
         per_launch_ms = res["sweep_ms"] / max(res["sweep_n"], 1)
         per_launch_bytes = res["sweep_bytes"] / max(res["sweep_n"], 1)
         achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
-        traffic, _src = ncu_traffic()
+        traffic, tsrc = ncu_traffic(args.config)
         n = args.gpus
-        value = n * args.steps / (res["total_ms"] * 1e-3)
-        line = {
-            "metric": "low-rank space-time Hessian matvecs/s", "value": value, "unit": "matvec/s",
-            "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded N(0,1) unit probes; no dataset)", "config": cfg,
+        line = dict(base)
+        line.update({
+            "value": n * args.steps / (res["total_ms"] * 1e-3),
+            "ms_per_step": res["total_ms"] / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
                          "kernel": "lrk::sweep_kernel", "peak_kind": peak_kind,
                          "alg_bytes_per_launch": per_launch_bytes,
-                         "ms_per_launch": per_launch_ms},
+                         "ms_per_launch": per_launch_ms, "build": build_hash()},
             "cpu_baseline": cpu,
-            "e2e": {"value": n * args.steps / (res["e2e_ms"] * 1e-3), "unit": "matvec/s",
-                    "h2d_bytes_per_step": 8 * res["n_x"], "d2h_bytes_per_step": 8 * res["n_x"]},
+            "e2e": {"value": n * args.steps / res["e2e_s"], "unit": "matvec/s",
+                    "h2d_bytes_per_step": 8 * res["n_x"], "d2h_bytes_per_step": 8 * res["n_x"],
+                    "timing": "perf_counter wall, pinned host in/out, sync per step"},
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
             "max_rank_per_apply": res["ranks"],
-        }
+        })
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

@@ -147,6 +147,78 @@ class StepSolver:
         return self.lu.solve(B, trans="T" if adjoint else "N")
 
 
+class CGStepSolver:
+    """CPU SUBSTITUTE for StepSolver where SuperLU cannot be set up: the 3-D
+    C4/C5 step matrices exhaust memory in splu (MemoryError at 128³
+    after > 41 min).  S = M(I + tau L) is SPD for the heat operator, so each
+    solve is a CG solve to relative residual 1e-12 (SURVEY §8(d) "extrapolated,
+    substitute solver").  Same interface as StepSolver (forward.py:61-68)."""
+
+    def __init__(self, L, m_scale: float, tau: float, n_t: int, rtol: float = 1e-12):
+        n_x = L.shape[0]
+        self.L = L
+        self.m = m_scale
+        self.tau = tau
+        self.n_x, self.n_t = n_x, n_t
+        self.S = sp.csr_matrix(m_scale * (sp.identity(n_x) + tau * L))
+        self.rtol = rtol
+        self.iterations = 0
+
+    def _one(self, b):
+        it = [0]
+
+        def cb(_):
+            it[0] += 1
+        x, info = spla.cg(self.S, b, rtol=self.rtol, atol=0.0, maxiter=10000, callback=cb)
+        if info != 0:
+            raise RuntimeError(f"CG step solve did not converge (info {info})")
+        self.iterations += it[0]
+        return x
+
+    def solve(self, B, adjoint=False):  # S symmetric: S^{-T} = S^{-1}
+        B = np.asarray(B, dtype=float)
+        if B.ndim == 1:
+            return self._one(B)
+        return np.column_stack([self._one(B[:, j]) for j in range(B.shape[1])])
+
+
+class SweepStepper:
+    """The sweep of forward.py:133-188 (same arithmetic as ``sweep`` below),
+    resumable one time step at a time — the CPU baseline times bounded
+    prefixes of an apply with it (bench.py)."""
+
+    def __init__(self, solver, rW1, rW2, eps0, r_max=None, adjoint=False, p=4):
+        self.solver, self.eps0, self.r_max, self.adjoint, self.p = solver, eps0, r_max, adjoint, p
+        self.rW2 = np.asarray(rW2, float)
+        self.B = solver.solve(np.asarray(rW1, float), adjoint)
+        n_t = solver.n_t
+        self.order = list(range(n_t - 1, -1, -1) if adjoint else range(n_t))
+        self.pane = (np.zeros((solver.n_x, 0)), np.zeros((n_t, 0)))
+        self.cols, self.idx, self.trace = [], [], []
+        self.y = np.zeros(solver.n_x)
+        self.count = 0
+
+    @property
+    def done(self) -> bool:
+        return self.count >= len(self.order)
+
+    def step(self):
+        s = self.solver
+        k = self.order[self.count]
+        self.y = s.solve(s.m * self.y, self.adjoint) + self.B @ self.rW2[k]
+        self.cols.append(self.y)
+        self.idx.append(k)
+        self.count += 1
+        if self.count % self.p == 0 or self.done:
+            E = np.zeros((s.n_t, len(self.idx)))
+            E[self.idx, np.arange(len(self.idx))] = 1.0
+            self.pane = truncate(*concat(self.pane, (np.column_stack(self.cols), E)),
+                                 self.eps0, self.r_max)
+            self.trace.append(self.pane[0].shape[1])
+            self.cols.clear()
+            self.idx.clear()
+
+
 # ------------------------------------------------------------ factor algebra
 def rank_cut(s, eps0: float, r_max=None) -> int:
     """Smallest r with tail ||s[r:]|| <= eps0 ||s||, after the noise floor (lowrank.py:98-111)."""

@@ -19,10 +19,9 @@ the basis on the device and performs one full re-orthogonalised step per call:
   dot per new field): h_i = c_i - sum_{l<i} h_l G_li, which is MGS exactly in
   exact arithmetic because the subtraction is an exact concatenation.  The
   subtraction then costs one fused concatenate-and-truncate
-  (`lrk_add_truncate`).  Documented deviation: the reference additionally
-  truncates mid-pass whenever the working rank passes work_cap = 48
-  (arnoldi.py:141-151); here each pass truncates once, so intermediate
-  rounding differs at the eps0 level (Ritz values agree to 1e-6, tests).
+  (`lrk_add_truncate`) per segment between the reference's work_cap = 48
+  truncations (arnoldi.py:141-151), which are kept: a new batched Gram is
+  taken after each such truncation, so the iterates follow the reference's.
 
 The k x k Hessenberg eigenproblems stay on the host (numpy LAPACK, like the
 reference), so Ritz values come from the same routine.
@@ -50,6 +49,7 @@ from .lowrank import (
 )
 
 BREAKDOWN_TOL = 1e-14   # arnoldi.py:35
+WORK_CAP = 48           # working-rank cap of low-rank iterates (arnoldi.py:131)
 RESTART_SALT = 0x5EED   # seed offset of restart directions (arnoldi.py:224)
 
 
@@ -208,19 +208,21 @@ class _FieldStore:
         a, r = self.off[i], self.rk[i]
         return LowRankMat._wrap(self.W1[:, a:a + r], self.W2[:, a:a + r])
 
-    def dots(self, w: LowRankMat, k: int | None = None) -> np.ndarray:
-        """<w, V_i> for the first k fields: one batched Gram + one readback."""
+    def dots(self, w: LowRankMat, k: int | None = None, lo: int = 0) -> np.ndarray:
+        """<w, V_i> for fields lo <= i < k: one batched Gram + one readback."""
         k = len(self) if k is None else k
-        if k == 0:
+        if k <= lo:
             return np.zeros(0)
-        out = (c_double * k)()
-        seg = (c_int * k)(*self.rk[:k])
-        basis = LowRankMat._wrap(self.W1[:, : self.used], self.W2[:, : self.used])._c()
+        nseg = k - lo
+        out = (c_double * nseg)()
+        seg = (c_int * nseg)(*self.rk[lo:k])
+        a = self.off[lo]
+        basis = LowRankMat._wrap(self.W1[:, a: self.used], self.W2[:, a: self.used])._c()
         _lib.check(
-            _lib.get_lib().lrk_lr_dots(self._ctx.handle, byref(w._c()), byref(basis), k, seg, out,
-                                       _lib.stream_handle()),
+            _lib.get_lib().lrk_lr_dots(self._ctx.handle, byref(w._c()), byref(basis), nseg, seg,
+                                       out, _lib.stream_handle()),
             self._ctx.handle, "lr_arnoldi")
-        return np.array(out[:k])
+        return np.array(out[:nseg])
 
 
 def _lr_norm(w: LowRankMat) -> float:
@@ -261,13 +263,33 @@ class _LowRankSpace:
         return w
 
     def _pass(self, w: LowRankMat):
+        """One MGS pass of arnoldi.py:322-327 with its working-rank control
+        (_LowRankOps.sub, arnoldi.py:141-151): the subtractions are exact
+        concatenations, truncated whenever the working rank passes work_cap,
+        and once more at the end of the pass (compress).  Between two
+        truncations w is fixed up to the concatenated terms, so every MGS
+        coefficient of the segment follows from ONE batched Gram against the
+        segment's fields and the basis Gram: h_j = <w, V_j> - sum h_l <V_l, V_j>."""
         k = self.k
-        c = self.store.dots(w, k)
-        h = np.empty(k)
-        for i in range(k):  # MGS coefficients from the batched inner products
-            h[i] = c[i] - h[:i] @ self.G[:i, i]
-        terms = [w] + [self.store.field(i) for i in range(k)]
-        return h, lr_add_truncate(terms, np.concatenate(([1.0], -h)), self.pol)
+        h = np.zeros(k)
+        i = 0
+        while i < k:
+            c = self.store.dots(w, k, lo=i)
+            terms, coefs, width, j = [w], [1.0], w.r, i
+            while j < k:
+                h[j] = c[j - i] - h[i:j] @ self.G[i:j, j]
+                if h[j] != 0.0:  # lr_scale by 0 is the zero field (lowrank.py:157-160)
+                    terms.append(self.store.field(j))
+                    coefs.append(-h[j])
+                    width += self.store.rk[j]
+                j += 1
+                if width > WORK_CAP:
+                    break
+            w = lr_add_truncate(terms, coefs, self.pol)
+            i = j
+        if k == 0:
+            w = lr_truncate(w, self.pol)
+        return h, w
 
     def orthogonalize(self, w: LowRankMat):
         h1, w = self._pass(w)
@@ -326,9 +348,31 @@ def _combine_dense(basis: list, coeffs: np.ndarray):
     """All Ritz vectors as one device product basis @ coeffs, columns normalised."""
     torch = _torch()
     Q = torch.stack([_to_dev_vec(b) for b in basis], dim=1)
-    Y = Q @ torch.as_tensor(np.real(coeffs), dtype=torch.float64, device=Q.device)
+    Y = Q @ torch.as_tensor(np.ascontiguousarray(np.real(coeffs)), dtype=torch.float64,
+                             device=Q.device)
     nrm = Y.norm(dim=0)
     return Y / torch.where(nrm > 0, nrm, torch.ones_like(nrm))
+
+
+def _combine_lowrank(basis: list, coeffs, pol: TruncationPolicy) -> LowRankMat:
+    """sum_i c_i V_i with the reference's working-rank control (arnoldi.py:158-166):
+    fused concatenate-and-truncate whenever the running width passes work_cap,
+    and a final truncation."""
+    out, i, k = None, 0, len(basis)
+    while i < k:
+        terms = [] if out is None else [out]
+        cf = [] if out is None else [1.0]
+        width = 0 if out is None else out.r
+        while i < k:
+            if float(coeffs[i]) != 0.0:
+                terms.append(basis[i])
+                cf.append(float(coeffs[i]))
+                width += basis[i].r
+            i += 1
+            if width > WORK_CAP:
+                break
+        out = lr_add_truncate(terms, cf, pol) if terms else LowRankMat.zeros(*basis[0].shape)
+    return out if out is not None else LowRankMat.zeros(*basis[0].shape)
 
 
 def ritz_pairs(H: np.ndarray, basis: list, pol: TruncationPolicy | None = None) -> list:
@@ -341,7 +385,7 @@ def ritz_pairs(H: np.ndarray, basis: list, pol: TruncationPolicy | None = None) 
         pol = pol or TruncationPolicy()
         pairs = []
         for i in range(m):
-            v = lr_add_truncate(basis[:m], np.real(vecs[:, i]), pol)
+            v = _combine_lowrank(basis[:m], np.real(vecs[:, i]), pol)
             nrm = _lr_norm(v)
             pairs.append((complex(vals[i]), lr_scale(v, 1.0 / nrm) if nrm > 0 else v))
         return pairs

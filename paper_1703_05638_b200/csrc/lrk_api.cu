@@ -350,6 +350,42 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
     batch.ngroups = G;
   }
   const int slot = adjoint ? 1 : 0;
+  // Large n_x (rows not resident in shared memory): the streaming-flush form
+  // (lrk_sflush.cu) — one kernel per row pass instead of the persistent
+  // kernel's global-row phases.  LRK_SFLUSH=0 forces the persistent kernel,
+  // LRK_SFLUSH=1 forces the streaming form (tests).
+  {
+    const char* sfe = std::getenv("LRK_SFLUSH");
+    const int force = sfe ? std::atoi(sfe) : -1;
+    const bool fits = p <= SF_P && ucap <= SF_CAP && rb <= SF_CAP && (nx % 2) == 0 && G == 1 &&
+                      !std::getenv("LRK_DUMP_CORES") && !std::getenv("LRK_DEBUG");
+    const bool want = force == 1 || (force != 0 && !a.resident);
+    if (fits && want) {
+      WS(SFState, sfst, tag + "sfst", 1);
+      WS(unsigned, tick, "sf_tick", 8);
+      const int Gs = c->num_sms;
+      WS(double, sfpart, "sf_part", (int64_t)(8 * Gs) * sf_part_stride());
+      CK(cudaMemsetAsync(sfst, 0, sizeof(SFState), s));
+      CK(cudaMemsetAsync(yprev, 0, nx * sizeof(double), s));
+      SFArgs sa{};
+      sa.n_x = nx; sa.n_t = nt; sa.p = p; sa.cap = ucap; sa.adjoint = adjoint; sa.r_max = r_max;
+      sa.nflush = nflush; sa.eps0 = eps0; sa.ftz = a.ftz;
+      sa.U = U0; sa.ldu = nx; sa.V = V0; sa.ldv = nt;
+      sa.Yg[0] = ybuf; sa.Yg[1] = qbuf; sa.ldy = nx;
+      sa.yprev = yprev; sa.theta = c->dTheta; sa.rowscale = c->dThetaM;
+      sa.B = B; sa.ldb = ldb; sa.rb = rb; sa.rb_dev = rb_dev; sa.W2 = W2; sa.ldw2 = ldw2;
+      sa.part = sfpart; sa.ticket = tick; sa.st = sfst;
+      sa.trace = trace; sa.info = info; sa.sigma = sig;
+      sa.G = Gs; sa.Ggen = 8 * c->num_sms;
+      sa.dbg_print = std::getenv("LRK_SF_DEBUG") ? std::atoi(std::getenv("LRK_SF_DEBUG")) : 0;
+      if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
+      CK(launch_sweep_stream(sa, nflush, s, &c->launches));
+      if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
+      o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
+      o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
+      return LRK_OK;
+    }
+  }
   const char* dump = std::getenv("LRK_DUMP_CORES");  // diagnostics (tools/jacobi_bench)
   const int64_t dsz = (int64_t)nflush * (1 + 32 * 33);
   WS(double, cd, tag + "cdump", dump ? dsz : 1);

@@ -58,9 +58,13 @@ def _check_apply(ctx, v, fx):
     assert err <= 1e-9, err
 
 
-def test_c2_apply_at_bench_config_vs_reference():
-    """The EXACT bench workload (C2: Q1 256², n_t 512, 32×32 sensors, prior,
-    r_max 32): one apply against the reference, identical per-flush ranks."""
+@pytest.mark.parametrize("form", ["auto", "persistent", "streaming"])
+def test_c2_apply_at_bench_config_vs_reference(monkeypatch, form):
+    """The EXACT C2 workload (Q1 256², n_t 512, 32×32 sensors, prior, r_max
+    32): one apply against the reference, identical per-flush ranks — with
+    either sweep form (persistent resident-row kernel / streaming flush)."""
+    if form != "auto":
+        monkeypatch.setenv("LRK_SFLUSH", "0" if form == "persistent" else "1")
     ctx, grid, _ = _c2()
     fx = _fx("c2_apply")
     v = np.random.default_rng(1).standard_normal(grid.n_x)
@@ -102,17 +106,22 @@ def test_c1_source_mode_lowrank_arnoldi_vs_reference():
     assert res.iterations == int(fx["iters"][0])
     lead = fx["ritz"] >= 1e-1
     np.testing.assert_allclose(res.ritz_values.real[: lead.sum()], fx["ritz"][lead], rtol=1e-6)
-    assert np.all(np.abs(np.array(res.rank_trace) - fx["ranks"]) <= 1)
+    assert np.all(np.abs(np.array(res.rank_trace) - fx["ranks"]) <= 1), \
+        (res.rank_trace, fx["ranks"].tolist())
     top = res.ritz_vectors[0]
     sv = lp.lr_singular_values(top)
     k = min(len(sv), len(fx["top_sv"]), 4)
     np.testing.assert_allclose(sv[:k], fx["top_sv"][:k], rtol=1e-5, atol=1e-9)
 
 
-def test_c4_path_3d_point_sensors_global_rows_vs_reference():
-    """The C4 path at n_x >= 1e5 (3-D 7-point heat 48³ = 110,592 dofs, global
-    CTA rows in the sweep): 12³ point sensors every 4th step, σ 0.005, prior
-    (I + 0.02 L)⁻¹, r_max 64 — one apply against the reference."""
+@pytest.mark.parametrize("form", ["auto", "persistent"])
+def test_c4_path_3d_point_sensors_global_rows_vs_reference(monkeypatch, form):
+    """The C4 path at n_x >= 1e5 (3-D 7-point heat 48³ = 110,592 dofs, rows
+    not resident: the streaming-flush sweep by default, the persistent kernel's
+    global-row phases with LRK_SFLUSH=0): 12³ point sensors every 4th step,
+    σ 0.005, prior (I + 0.02 L)⁻¹, r_max 64 — one apply against the reference."""
+    if form == "persistent":
+        monkeypatch.setenv("LRK_SFLUSH", "0")
     ctx, grid, _ = _ctx(48, 3, "fd", 32, 12, 4, 0.005, 1.0, 0.02, 64)
     fx = _fx("c4_sweep3d")
     v = np.random.default_rng(3).standard_normal(grid.n_x)
@@ -232,3 +241,33 @@ def test_batched_lr_dots_match_pairwise():
     ref = np.array([O.dot((w.W1.cpu().numpy(), w.W2.cpu().numpy()),
                           (f.W1.cpu().numpy(), f.W2.cpu().numpy())) for f in fields])
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", ["hic_d", "cfg_q1b"])
+def test_streaming_flush_small_fixtures_vs_reference(golden, monkeypatch, name):
+    """The streaming-flush sweep forced on the reference's small rank-capped
+    fixtures (ragged last chunk, tiny grids): same outputs and max ranks."""
+    monkeypatch.setenv("LRK_SFLUSH", "1")
+    if name == "hic_d":
+        n_side, n_t, bn, bp, gp, rmax = golden["hic_d_meta"]
+        grid = lp.build_grid(int(n_side))
+        K = lp.SpaceTimeOperator(lp.assemble_heat(grid), lp.build_time_grid(int(n_t)))
+        cov = lp.CovarianceSpec(bn, bp, gp)
+        layout = lp.SensorLayout((), golden["hic_d_mask"])
+        ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                                pol=lp.TruncationPolicy(1e-8, int(rmax)))
+    else:
+        meta = golden["cfg_q1b_meta"]
+        n_side, n_t, delta, gp, bn, rmax = int(meta[0]), int(meta[3]), meta[5], meta[6], meta[7], int(meta[8])
+        grid = lp.build_grid(n_side)
+        K = lp.SpaceTimeOperator(lp.assemble_heat(grid, "q1"), lp.build_time_grid(n_t))
+        cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=delta, prior_gamma=gp)
+        ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.SensorLayout((), golden["cfg_q1b_mask"]),
+                                cov=cov, pol=lp.TruncationPolicy(1e-8, rmax))
+    V, Oref = golden[f"{name}_V"], golden[f"{name}_O"]
+    refr = golden[f"{name}_ranks"]
+    for j in range(V.shape[1]):
+        out = ctx.apply(V[:, j])
+        assert np.linalg.norm(out - Oref[:, j]) <= 1e-9 * np.linalg.norm(Oref[:, j])
+        if refr.size == V.shape[1]:
+            assert ctx.rank_trace[-1] == refr[j]
