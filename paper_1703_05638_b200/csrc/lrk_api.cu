@@ -37,6 +37,7 @@ struct lrk_ctx {
   bool has_op = false;
   lrk_operator_desc op{};
   int64_t n_x = 0;
+  int64_t ldp = 0;            // padded leading dimension of n_x-row workspace (see padld)
   int n = 0;
   double* dS = nullptr;       // n x n DST-I (symmetric, orthogonal)
   double* dSsq = nullptr;     // n x n elementwise square of the DST-I (operator diagonals)
@@ -132,6 +133,15 @@ inline int grid1(int64_t n, int per = 256, int cap = 4096) {
   if (g < 1) g = 1;
   if (g > cap) g = cap;
   return (int)g;
+}
+
+// Leading dimension for n_x-row, multi-column workspace: column starts are
+// staggered (+2.25 KB) so that the columns of a large power-of-two n_x do not
+// all map onto the same DRAM channels (C4: n_x = 2^21, a 16 MiB column stride).
+int64_t padld(int64_t n) {
+  static const int64_t extra = std::getenv("LRK_LDPAD") ? std::atoll(std::getenv("LRK_LDPAD")) : 288;
+  if (n < 4096) return n;
+  return ((n + 31) / 32) * 32 + extra;
 }
 
 int pick_ncta(lrk_ctx* c, int64_t rows) {
@@ -278,15 +288,16 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   const int ucap = (r_max >= 0 && r_max < NMAX) ? std::max(r_max, 1) : NMAX;
   const int ncta = pick_ncta(c, nx);
   const int nflush = (nt + p - 1) / p;
-  WS(double, U0, tag + "U0", nx * (int64_t)ucap);
-  WS(double, U1, tag + "U1", nx * (int64_t)ucap);
+  const int64_t ld = padld(nx);
+  WS(double, U0, tag + "U0", ld * (int64_t)ucap);
+  WS(double, U1, tag + "U1", ld * (int64_t)ucap);
   WS(double, V0, tag + "V0", (int64_t)nt * ucap);
   WS(double, V1, tag + "V1", (int64_t)nt * ucap);
   WS(double, sig, tag + "sig", NMAX);
   WS(int, info, tag + "info", 8);
   WS(int, trace, tag + "trace", nflush + 1);
-  WS(double, ybuf, "sw_ybuf", nx * (int64_t)p);
-  WS(double, qbuf, "sw_qbuf", nx * (int64_t)p);
+  WS(double, ybuf, "sw_ybuf", ld * (int64_t)p);
+  WS(double, qbuf, "sw_qbuf", ld * (int64_t)p);
   WS(double, yprev, "sw_yprev", nx);
   // emulated n_x shards (lrk_set_emulated_shards): G groups of one launch
   // acting as G GPUs of a sharded sweep, ncta/G CTAs each
@@ -307,9 +318,9 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   a.theta = c->dTheta; a.rowscale = c->dThetaM;
   a.B = B; a.ldb = ldb; a.rb = rb; a.rb_dev = rb_dev;
   a.W2 = W2; a.ldw2 = ldw2;
-  a.U0 = U0; a.U1 = U1; a.ldu = nx; a.V0 = V0; a.V1 = V1; a.ldv = nt; a.ucap = ucap;
+  a.U0 = U0; a.U1 = U1; a.ldu = ld; a.V0 = V0; a.V1 = V1; a.ldv = nt; a.ucap = ucap;
   a.sigma = sig; a.info = info; a.trace = trace;
-  a.ybuf = ybuf; a.ldy = nx; a.qbuf = qbuf; a.ldq = nx; a.yprev = yprev;
+  a.ybuf = ybuf; a.ldy = ld; a.qbuf = qbuf; a.ldq = ld; a.yprev = yprev;
   a.part = part; a.pstride = pst; a.scratch = scratch; a.scratch_stride = sst;
   a.bar = bar; a.ncta = ncta;
   a.yext = nullptr; a.ldyext = 0;
@@ -370,19 +381,21 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
       SFArgs sa{};
       sa.n_x = nx; sa.n_t = nt; sa.p = p; sa.cap = ucap; sa.adjoint = adjoint; sa.r_max = r_max;
       sa.nflush = nflush; sa.eps0 = eps0; sa.ftz = a.ftz;
-      sa.U = U0; sa.ldu = nx; sa.V = V0; sa.ldv = nt;
-      sa.Yg[0] = ybuf; sa.Yg[1] = qbuf; sa.ldy = nx;
+      sa.U = U0; sa.ldu = ld; sa.V = V0; sa.ldv = nt;
+      sa.Yg[0] = ybuf; sa.Yg[1] = qbuf; sa.ldy = ld;
       sa.yprev = yprev; sa.theta = c->dTheta; sa.rowscale = c->dThetaM;
       sa.B = B; sa.ldb = ldb; sa.rb = rb; sa.rb_dev = rb_dev; sa.W2 = W2; sa.ldw2 = ldw2;
       sa.part = sfpart; sa.ticket = tick; sa.st = sfst;
       sa.trace = trace; sa.info = info; sa.sigma = sig;
       sa.G = Gs; sa.Ggen = 8 * c->num_sms;
       sa.dbg_print = std::getenv("LRK_SF_DEBUG") ? std::atoi(std::getenv("LRK_SF_DEBUG")) : 0;
+      sa.smem_update = (int)sf_smem_update();
+      sa.smem_subtract = (int)sf_smem_subtract();
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
       CK(launch_sweep_stream(sa, nflush, s, &c->launches));
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
       o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
-      o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
+      o.ucap = ucap; o.nflush = nflush; o.ldu = ld; o.ldv = nt;
       return LRK_OK;
     }
   }
@@ -408,7 +421,7 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
     }
   }
   o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
-  o.ucap = ucap; o.nflush = nflush; o.ldu = nx; o.ldv = nt;
+  o.ucap = ucap; o.nflush = nflush; o.ldu = ld; o.ldv = nt;
   return LRK_OK;
 }
 
@@ -832,7 +845,7 @@ int check_op(lrk_ctx* c) {
 // Observation + weight + truncation of the forward pane (apply_obs_weight,
 // hessian.py:138-156).  Output: spectral Zhat (n_x x cap), Z2 (n_t x cap), zinfo.
 int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, int r_max,
-               double** Zhat, double** Z2, int** zinfo, int* zcap, cudaStream_t s) {
+               double** Zhat, int64_t* ldz_out, double** Z2, int** zinfo, int* zcap, cudaStream_t s) {
   const int64_t nx = c->n_x;
   const int nt = c->op.n_t;
   const int cap = y.ucap;
@@ -847,12 +860,13 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, 
   }
   // a time mask breaks the orthonormality of the time factor
   const int w2flag = every > 1 ? 0 : LRK_TRUNC_W2_ORTHOSCALED;
-  WS(double, Zh, "ob_Zhat", nx * (int64_t)cap);
+  const int64_t ldz = padld(nx);
+  WS(double, Zh, "ob_Zhat", ldz * (int64_t)cap);
   WS(double, Zt, "ob_Z2", (int64_t)nt * cap);
   TruncOut to;
   if (c->obs_kind == LRK_OBS_FULL) {
     TRY(run_truncate(c, "ob_", nx, nt, y.U, y.ldu, W2s, nt, cap, y.info,
-                     LRK_TRUNC_W1_ORTHO | w2flag, eps0, r_max, Zh, nx, Zt, nt,
+                     LRK_TRUNC_W1_ORTHO | w2flag, eps0, r_max, Zh, ldz, Zt, nt,
                      cap, nullptr, nullptr, 1, to, s));
   } else {
     const int no = c->n_obs;
@@ -874,13 +888,13 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, 
     TRY(run_truncate(c, "ob_", no, nt, Uo, no, W2s, nt, cap, y.info, w2flag,
                      eps0, r_max, Zo, no, Zt, nt, cap, nullptr, nullptr, 1, to, s));
     if (phys_basis(c)) {
-      fill_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(Zh, nx, nx, cap, 0.0);
+      fill_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(Zh, ldz, nx, cap, 0.0);
       CKL();
       scatter_rows_kernel<<<dim3(grid1(no, 256, 256), cap), 256, 0, s>>>(Zo, no, c->dList, no,
-                                                                          to.info, cap, Zh, nx);
+                                                                          to.info, cap, Zh, ldz);
       CKL();
     } else if (c->obs_kind == LRK_OBS_SUBGRID) {
-      TRY(subgrid_scatter(c, Zo, no, Zh, nx, cap, to.info, s));
+      TRY(subgrid_scatter(c, Zo, no, Zh, ldz, cap, to.info, s));
     } else {
       WS(double, Zp, "ob_Zphys", nx * (int64_t)cap);
       fill_kernel<<<dim3(grid1(nx, 256, 1024), cap), 256, 0, s>>>(Zp, nx, nx, cap, 0.0);
@@ -888,10 +902,11 @@ int obs_weight(lrk_ctx* c, const SweepOut& y, double w, int every, double eps0, 
       scatter_rows_kernel<<<dim3(grid1(no, 256, 256), cap), 256, 0, s>>>(Zo, no, c->dList, no,
                                                                           to.info, cap, Zp, nx);
       CKL();
-      TRY(dst2(c, Zp, nx, Zh, nx, cap, to.info, 1.0, s));
+      TRY(dst2(c, Zp, nx, Zh, ldz, cap, to.info, 1.0, s));
     }
   }
   *Zhat = Zh;
+  *ldz_out = ldz;
   *Z2 = Zt;
   *zinfo = to.info;
   *zcap = cap;
@@ -1475,11 +1490,12 @@ int lrk_hessian_apply_ic(lrk_ctx* c, const lrk_hessian_desc* hd, int nbatch, con
     TRY(run_sweep(c, "f_", Bv, nx, 1, nullptr, c->dE0, nt, 0, hd->compress_every, hd->eps0,
                   hd->r_max, fw, s));
     double *Zh, *Z2;
+    int64_t ldz = nx;
     int* zinfo;
     int zcap;
-    TRY(obs_weight(c, fw, hd->obs_weight, hd->obs_every, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo,
+    TRY(obs_weight(c, fw, hd->obs_weight, hd->obs_every, hd->eps0, hd->r_max, &Zh, &ldz, &Z2, &zinfo,
                    &zcap, s));
-    TRY(run_sweep(c, "b_", Zh, nx, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
+    TRY(run_sweep(c, "b_", Zh, ldz, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
                   bw, s));
     // extract: sqrt(g) M Q.column(0)  (forward.py:111-112)
     column_eval_kernel<<<grid1(nx, 256, 1024), 256, 0, s>>>(bw.U, bw.ldu, nx, bw.sigma, bw.V,
@@ -1514,11 +1530,12 @@ int lrk_hessian_apply_st(lrk_ctx* c, const lrk_hessian_desc* hd, const lrk_lr* v
   TRY(run_sweep(c, "f_", Bh, nx, v->r, nullptr, v->W2, v->ld2, 0, hd->compress_every, hd->eps0,
                 hd->r_max, fw, s));
   double *Zh, *Z2;
+  int64_t ldz = nx;
   int* zinfo;
   int zcap;
-  TRY(obs_weight(c, fw, hd->obs_weight, hd->obs_every, hd->eps0, hd->r_max, &Zh, &Z2, &zinfo,
+  TRY(obs_weight(c, fw, hd->obs_weight, hd->obs_every, hd->eps0, hd->r_max, &Zh, &ldz, &Z2, &zinfo,
                  &zcap, s));
-  TRY(run_sweep(c, "b_", Zh, nx, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
+  TRY(run_sweep(c, "b_", Zh, ldz, zcap, zinfo, Z2, nt, 1, hd->compress_every, hd->eps0, hd->r_max,
                 bw, s));
   // out = truncate(sqrt(g) tau M Q)  (hessian.py:242)
   const int cap = bw.ucap;

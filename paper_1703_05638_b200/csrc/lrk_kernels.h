@@ -133,7 +133,10 @@ struct SFArgs {
   int G;                 // CTAs of the staged row passes
   int Ggen;              // CTAs of the light grid-stride passes
   int dbg_print;         // LRK_SF_DEBUG: flushes to report (diagnostics)
+  int smem_update, smem_subtract;  // dynamic shared memory of the staged passes (bytes)
 };
+size_t sf_smem_update();
+size_t sf_smem_subtract();
 int64_t sf_part_stride();
 cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, int64_t* launches);
 

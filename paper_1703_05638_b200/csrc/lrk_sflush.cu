@@ -26,7 +26,8 @@
 //                      and the update matrices W' for the next launch.
 //
 // Each kernel streams its CTA's contiguous rows in 64-row chunks through a
-// cp.async ring (16-byte copies, four stages in flight), runs the row x small
+// TMA bulk-copy ring (cp.async.bulk + mbarriers, depth sized from the actual
+// pane rank so ~150 KB are in flight per SM), runs the row x small
 // products on the FP64 tensor pipe (DMMA m8n8k4) from shared memory, writes a
 // CTA partial and the LAST CTA to finish (atomic ticket) reduces the partials
 // in CTA order — deterministic, no grid barrier, no cooperative launch.  Per
@@ -44,43 +45,91 @@ namespace lrk {
 
 namespace {
 
-constexpr int ST = 256;           // threads per CTA
-constexpr int TR = 64;            // rows per staged chunk
-constexpr int LDX = 68;           // shared leading dimension (== 4 mod 16: conflict-free fragments)
-constexpr int NSTAGE = 4;         // cp.async ring depth
+constexpr int ST = 256;           // threads per CTA of the light passes
+constexpr int NW = 16;            // warps of the staged row passes
+constexpr int SPT = 32 * NW;
+constexpr int LDW = 68;           // shared leading dimension of the update matrix (== 4 mod 16)
 constexpr int PSTR = SF_N * SF_P + SF_P + 8;  // per-CTA partial stride (doubles)
 
+// ---- warp-private cp.async rings.  Every staged pass works on 8-row tiles
+// and each warp only ever touches its own tiles (the update tile, its share
+// of the projections and Grams), so a warp streams its rows through its own
+// shared-memory ring: 16-byte cp.async per lane, cp.async.wait_group, no CTA
+// barrier and no cross-warp handshake in the main loop.  The ring depth is
+// chosen from the ACTUAL column count (the pane rank is only known on the
+// device): deep rings at low rank, >= 2 tiles at rank 64.
 __device__ __forceinline__ void cp16(void* smem, const void* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz)
+               : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// Stage rows [i0, i0 + TR) of `ncols` columns into shared memory (column c at
-// dst + c * LDX); column c comes from src(c) (a global column pointer, 16-byte
-// aligned, n_x even).  Rows >= nrows are zero-filled.
-template <typename ColFn>
-__device__ __forceinline__ void stage_cols(double* dst, int ncols, ColFn src, int64_t i0,
-                                           int64_t nrows) {
-  constexpr int PER = TR / 2;  // 16-byte pieces per column
-  for (int idx = threadIdx.x; idx < ncols * PER; idx += ST) {
-    const int c = idx / PER, k = idx - c * PER;
-    const int64_t row = i0 + 2 * k;
-    const bool ok = row < nrows;
-    const double* g = src(c) + (ok ? row : 0);
-    cp16(dst + c * LDX + 2 * k, g, ok);
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_wait_dyn(int n) {
+  switch (n) {
+    case 0: cp_wait<0>(); break;
+    case 1: cp_wait<1>(); break;
+    case 2: cp_wait<2>(); break;
+    case 3: cp_wait<3>(); break;
+    case 4: cp_wait<4>(); break;
+    case 5: cp_wait<5>(); break;
+    case 6: cp_wait<6>(); break;
+    case 7: cp_wait<7>(); break;
+    case 8: cp_wait<8>(); break;
+    case 9: cp_wait<9>(); break;
+    case 10: cp_wait<10>(); break;
+    case 11: cp_wait<11>(); break;
+    case 12: cp_wait<12>(); break;
+    case 13: cp_wait<13>(); break;
+    default: cp_wait<14>(); break;
   }
 }
+constexpr int LDT = 8;        // rows per tile = leading dimension of a staged column
+constexpr int MAXDEPTH = 15;  // (cp_wait_dyn covers depth - 1 <= 14)
 
-// Rows of this CTA: whole chunks [c0, c1) of the 64-row chunk grid.
-__device__ __forceinline__ void cta_chunks(int64_t n_x, int& c0, int& c1) {
-  const int nch = (int)((n_x + TR - 1) / TR);
-  const int per = (nch + gridDim.x - 1) / gridDim.x;
-  c0 = min(nch, (int)blockIdx.x * per);
-  c1 = min(nch, c0 + per);
+struct WRing {
+  double* base;  // this warp's region
+  int slot;      // doubles per tile (ncols * LDT)
+  int depth;
+};
+
+__device__ __forceinline__ WRing wring(double* region, int per_warp, int ncols) {
+  WRing R;
+  R.base = region + (int64_t)(threadIdx.x >> 5) * per_warp;
+  R.slot = (ncols > 0 ? ncols : 1) * LDT;
+  R.depth = per_warp / R.slot;
+  R.depth = R.depth < 2 ? 2 : (R.depth > MAXDEPTH ? MAXDEPTH : R.depth);
+  return R;
+}
+
+// Copy tile `tile` (rows tile*8 .. +8) of ncols columns into slot `sl`; every
+// lane commits one group (possibly empty) so the group counts stay aligned.
+template <typename ColFn>
+__device__ __forceinline__ void wring_issue(const WRing& R, int sl, int64_t tile, bool valid, int ncols,
+                                            ColFn src, int64_t n_x) {
+  if (valid) {
+    const int lane = threadIdx.x & 31;
+    double* dst = R.base + (int64_t)sl * R.slot;
+    const int64_t r0 = tile * LDT;
+    for (int q = lane; q < ncols * 4; q += 32) {
+      const int c = q >> 2, j = q & 3;
+      const int64_t row = r0 + 2 * j;
+      const bool ok = row < n_x;
+      cp16(dst + c * LDT + 2 * j, src(c) + (ok ? row : 0), ok);
+    }
+  }
+  cp_commit();
+}
+
+// Tiles of this CTA: a contiguous range [t0, t1) of the 8-row tile grid;
+// warp w takes tiles t0 + w, t0 + w + NW, ...
+__device__ __forceinline__ void cta_tiles(int64_t n_x, int64_t& t0, int64_t& t1) {
+  const int64_t nt = (n_x + LDT - 1) / LDT;
+  const int64_t per = (nt + gridDim.x - 1) / gridDim.x;
+  t0 = min(nt, (int64_t)blockIdx.x * per);
+  t1 = min(nt, t0 + per);
 }
 
 // Block-wide sum of K per-thread values into out (shared), fixed order.
@@ -95,7 +144,7 @@ __device__ __forceinline__ void cta_sum(double (&v)[K], double* red, double* out
   __syncthreads();
   if (threadIdx.x < K) {
     double s = 0.0;
-    for (int ww = 0; ww < ST / 32; ++ww) s += red[ww * K + threadIdx.x];
+    for (int ww = 0; ww < (int)(blockDim.x / 32); ++ww) s += red[ww * K + threadIdx.x];
     out[threadIdx.x] = s;
   }
   __syncthreads();
@@ -118,12 +167,21 @@ __device__ __forceinline__ bool last_cta(unsigned* ticket, int* flag) {
   return *flag != 0;
 }
 
-// out[e] = sum over CTAs (in order) of part[c * PSTR + e], e < len
+// out[e] = sum over CTAs of part[c * PSTR + e], e < len: one warp per entry,
+// lanes stride over the CTAs (independent loads in flight), then a fixed
+// shuffle tree — deterministic.
 __device__ __forceinline__ void reduce_parts(const double* part, int len, double* out) {
-  for (int e = threadIdx.x; e < len; e += ST) {
-    double s = 0.0;
-    for (int c = 0; c < (int)gridDim.x; ++c) s += __ldcg(part + (int64_t)c * PSTR + e);
-    out[e] = s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = w; e < len; e += nw) {
+    double s0 = 0.0, s1 = 0.0;
+    int c = lane;
+    for (; c + 32 < (int)gridDim.x; c += 64) {
+      s0 += __ldcg(part + (int64_t)c * PSTR + e);
+      s1 += __ldcg(part + (int64_t)(c + 32) * PSTR + e);
+    }
+    if (c < (int)gridDim.x) s0 += __ldcg(part + (int64_t)c * PSTR + e);
+    const double v = warp_sum(s0 + s1);
+    if (lane == 0) out[e] = v;
   }
   __syncthreads();
 }
@@ -244,10 +302,55 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
 
 }  // namespace
 
+// Tail of the second CGS pass (thread 0): the shifted Cholesky factor of
+// G0 = y2^T y2 (Fukaya et al. shifted CholeskyQR3, first step); a remainder at
+// the block's rounding floor 16 eps ||Y|| is dropped whole.  Out of line: keeps
+// the streaming kernel's register count low.
+static __device__ __noinline__ void sf_shifted_chol(const SFArgs& a, SFState* st, const double* tot,
+                                                    int pc) {
+  double G[16] = {};
+  for (int u = 0; u < pc; ++u)
+    for (int v = 0; v < pc; ++v) G[u * 4 + v] = tot[u * pc + v];
+  double tr = 0.0, ysq = 0.0;
+  for (int s = 0; s < pc; ++s) { tr += G[s * 5]; ysq += st->yn[s]; }
+  const double delta = 16.0 * DEPS * sqrt(ysq);
+  st->drop_all = !(sqrt(tr) > delta);
+  double Rm[16], Zm[16];
+  if (st->drop_all) {
+    for (int i = 0; i < 16; ++i) { Rm[i] = 0.0; Zm[i] = 0.0; }
+  } else {
+    const double shift = 11.0 * ((double)a.n_x * pc + pc * (pc + 1)) * DEPS * tr;
+    for (int s = 0; s < pc; ++s) G[s * 5] += shift;
+    pivoted_chol4(G, pc, 0.0, Rm, Zm);
+  }
+  for (int i = 0; i < 16; ++i) { st->Rc[i] = Rm[i]; st->Rinv[i] = Zm[i]; }
+}
+
+// CholeskyQR pass tail (thread 0): R <- chol(G) R, Rinv <- Rinv chol(G)^{-1};
+// pivots below (1e-10)^2 of the leading one are rounding residue of a
+// numerically rank-deficient remainder and are dropped (see header).
+static __device__ __noinline__ void sf_chol_update(SFState* st, const double* tot, int pc) {
+  double G[16] = {};
+  int q = 0;
+  for (int u = 0; u < SF_P; ++u)
+    for (int v = u; v < SF_P; ++v) {
+      G[u * 4 + v] = G[v * 4 + u] = tot[q];
+      ++q;
+    }
+  double R1[16], Z1[16], Rc[16], Ri[16], Rn[16], Zn[16];
+  pivoted_chol4(G, pc, 1e-20, R1, Z1);
+  for (int i = 0; i < 16; ++i) { Rc[i] = st->Rc[i]; Ri[i] = st->Rinv[i]; }
+  mat4_mul(R1, Rc, Rn, pc);
+  mat4_mul(Ri, Z1, Zn, pc);
+  for (int i = 0; i < 16; ++i) { st->Rc[i] = Rn[i]; st->Rinv[i] = Zn[i]; }
+}
+
 // --------------------------------------------------------------- update + project
 // Pending update (st->pending): U'[:, :rn] = [U[:, :r], y2] Wp, V' likewise;
-// then (unless final) M = [U', ...] handled as P1 = Wp^T ([U, y2]^T Y).
-__global__ void __launch_bounds__(ST, 1) sf_update_project(const SFArgs a, int f, int final_only) {
+// then (unless final) P1 = U'^T Y evaluated as Wp^T ([U, y2]^T Y).
+// Warp w owns rows 8w..8w+7 of every 128-row chunk: the update tile and its
+// share of the projection need no CTA barrier inside a chunk.
+__global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int f, int final_only) {
   extern __shared__ double smem[];
   SFState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -261,17 +364,16 @@ __global__ void __launch_bounds__(ST, 1) sf_update_project(const SFArgs a, int f
   const int pc = final_only ? 0 : min(a.p, a.n_t - start);
   const double* Ycur = a.Yg[f & 1];
   const double* Y2 = a.Yg[(f + 1) & 1];       // the previous flush's remainder
-  double* W = smem;                           // SF_N x LDX (Wp, col-major by output column)
-  double* stage = W + SF_N * LDX;
-  const int xcols = SF_CAP + SF_P;            // X region columns per stage
-  const int scols = xcols + SF_P;             // + Y columns
-  int* flag = reinterpret_cast<int*>(stage + NSTAGE * scols * LDX);
+  double* W = smem;                           // Wp (n x rn), column c at W + c * LDW
+  double* stage = W + SF_N * LDW;             // V update scratch, then the warp rings
+  const int avail = a.smem_update / (int)sizeof(double) - SF_N * LDW - 16;
+  int* flag = reinterpret_cast<int*>(stage + avail);
   double* red = stage;                        // reused after the main loop
 
   if (pend) {
-    for (int idx = tid; idx < n * rn; idx += ST) {
+    for (int idx = tid; idx < n * rn; idx += SPT) {
       const int k = idx % n, c = idx / n;
-      W[c * LDX + k] = st->Wp[k + c * SF_LDW];
+      W[c * LDW + k] = st->Wp[k + c * SF_LDW];
     }
     // time rows of this CTA: V' = [V, E] Vc   (in place, via shared memory)
     const int64_t tper = ((int64_t)a.n_t + gridDim.x - 1) / gridDim.x;
@@ -280,12 +382,12 @@ __global__ void __launch_bounds__(ST, 1) sf_update_project(const SFArgs a, int f
     const int nrow = (int)(t1 - t0);
     double* Vs = stage;  // nrow x r
     double* Vc = stage + nrow * SF_CAP + 8;
-    for (int idx = tid; idx < n * rn; idx += ST) Vc[idx] = st->Vc[(idx % n) + (idx / n) * SF_LDW];
-    for (int idx = tid; idx < nrow * r; idx += ST)
+    for (int idx = tid; idx < n * rn; idx += SPT) Vc[idx] = st->Vc[(idx % n) + (idx / n) * SF_LDW];
+    for (int idx = tid; idx < nrow * r; idx += SPT)
       Vs[idx] = a.V[(t0 + idx % nrow) + (int64_t)(idx / nrow) * a.ldv];
     __syncthreads();
     const int sp = st->startp;
-    for (int idx = tid; idx < nrow * rn; idx += ST) {
+    for (int idx = tid; idx < nrow * rn; idx += SPT) {
       const int tl = idx % nrow, c = idx / nrow;
       const int64_t tt = t0 + tl;
       const int sel = a.adjoint ? (a.n_t - 1 - sp) - (int)tt : (int)tt - sp;
@@ -293,51 +395,55 @@ __global__ void __launch_bounds__(ST, 1) sf_update_project(const SFArgs a, int f
       for (int k = 0; k < r; ++k) acc += Vs[tl + k * nrow] * Vc[k + c * n];
       a.V[tt + (int64_t)c * a.ldv] = acc;
     }
-    __syncthreads();
   }
 
-  int c0, c1;
-  cta_chunks(a.n_x, c0, c1);
-  const int nk = (n + 3) >> 2, nj = (rn + 7) >> 3;
+  int64_t ct0, ct1;
+  cta_tiles(a.n_x, ct0, ct1);
+  const int nk = (n + 3) >> 2, nj = (rn + 7) >> 3, nm = (n + 7) >> 3;
   const double* U = a.U;
-  auto issue = [&](int ch) {
-    if (ch < c1) {
-      double* s = stage + ((ch - c0) % NSTAGE) * scols * LDX;
-      const int64_t i0 = (int64_t)ch * TR;
-      stage_cols(s, n, [&](int c) { return c < r ? U + (int64_t)c * a.ldu : Y2 + (int64_t)(c - r) * a.ldy; },
-                 i0, a.n_x);
-      if (pc > 0) stage_cols(s + xcols * LDX, pc, [&](int c) { return Ycur + (int64_t)c * a.ldy; }, i0, a.n_x);
-    }
-    cp_commit();
+  const int ncol = n + pc;  // tile: X = [U, y2] columns, then Y
+  __syncthreads();          // W and the V-update scratch are settled
+  const WRing R = wring(stage, (avail / NW) & ~1, ncol);
+  auto src = [&](int c) -> const double* {
+    return c < r ? U + (int64_t)c * a.ldu
+                 : (c < n ? Y2 + (int64_t)(c - r) * a.ldy : Ycur + (int64_t)(c - n) * a.ldy);
   };
-  // projection accumulators: M rows (X columns) 8*warp + g (and 64 + g on warp 0)
-  double m0[2] = {0.0, 0.0}, m1[2] = {0.0, 0.0};
+  // projection M = X^T Y over this warp's rows: tile jt = X columns 8jt..8jt+7
+  double m[9][2];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) m[j][0] = m[j][1] = 0.0;
   double ysq = 0.0;
   const bool do_upd = pend && rn > 0 && n > 0;
-  for (int s = 0; s < NSTAGE - 1; ++s) issue(c0 + s);
-  for (int ch = c0; ch < c1; ++ch) {
-    cp_wait<NSTAGE - 2>();
-    __syncthreads();
-    issue(ch + NSTAGE - 1);
-    const double* X = stage + ((ch - c0) % NSTAGE) * scols * LDX;
-    const double* Yt = X + xcols * LDX;
-    const int64_t i0 = (int64_t)ch * TR;
+  const int64_t first = ct0 + warp;
+  for (int q = 0; q < R.depth - 1; ++q) {
+    const int64_t tq = first + (int64_t)q * NW;
+    wring_issue(R, q, tq, tq < ct1, ncol, src, a.n_x);
+  }
+  int cur = 0, nxt = R.depth - 1;
+  for (int64_t tile = first; tile < ct1; tile += NW) {
+    {
+      const int64_t tq = tile + (int64_t)(R.depth - 1) * NW;
+      wring_issue(R, nxt, tq, tq < ct1, ncol, src, a.n_x);
+    }
+    cp_wait_dyn(R.depth - 1);
+    __syncwarp();
+    const double* X = R.base + (int64_t)cur * R.slot;
+    const double* Yt = X + n * LDT;
     if (do_upd) {
-      // U' rows of tile `warp`: acc[j] = X[8w.., :] W[:, 8j..]
       double acc[8][2];
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
       for (int kk = 0; kk < nk; ++kk) {
         const int k = 4 * kk + t;
-        const double av = (k < n) ? X[k * LDX + 8 * warp + g] : 0.0;
+        const double av = (k < n) ? X[k * LDT + g] : 0.0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (j >= nj) break;
-          const double bv = (k < n && 8 * j + g < rn) ? W[(8 * j + g) * LDX + k] : 0.0;
+          const double bv = (k < n && 8 * j + g < rn) ? W[(8 * j + g) * LDW + k] : 0.0;
           dmma884(acc[j][0], acc[j][1], av, bv);
         }
       }
-      const int64_t row = i0 + 8 * warp + g;
+      const int64_t row = tile * LDT + g;
       if (row < a.n_x) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -349,63 +455,72 @@ __global__ void __launch_bounds__(ST, 1) sf_update_project(const SFArgs a, int f
       }
     }
     if (pc > 0) {
-      // M += X^T Y  (rows = X columns, k = chunk rows)
-      if (8 * warp < n) {
-#pragma unroll 4
-        for (int kk = 0; kk < TR / 4; ++kk) {
-          const double av = X[(8 * warp + g) * LDX + 4 * kk + t];
-          const double bv = (g < pc) ? Yt[g * LDX + 4 * kk + t] : 0.0;
-          dmma884(m0[0], m0[1], av, bv);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int rho = 4 * kk + t;
+        const double bv = (g < pc) ? Yt[g * LDT + rho] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+          if (j >= nm) break;
+          const double av = (8 * j + g < n) ? X[(8 * j + g) * LDT + rho] : 0.0;
+          dmma884(m[j][0], m[j][1], av, bv);
         }
       }
-      if (warp == 0 && n > 64) {
-#pragma unroll 4
-        for (int kk = 0; kk < TR / 4; ++kk) {
-          const double av = (64 + g < n) ? X[(64 + g) * LDX + 4 * kk + t] : 0.0;
-          const double bv = (g < pc) ? Yt[g * LDX + 4 * kk + t] : 0.0;
-          dmma884(m1[0], m1[1], av, bv);
-        }
-      }
-      if (tid < TR * pc) {
-        const double y = Yt[(tid / TR) * LDX + (tid % TR)];
+      if ((lane >> 3) < pc) {
+        const double y = Yt[(lane >> 3) * LDT + (lane & 7)];
         ysq += y * y;
       }
     }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    cur = cur + 1 == R.depth ? 0 : cur + 1;
+    nxt = nxt + 1 == R.depth ? 0 : nxt + 1;
   }
   cp_wait<0>();
   __syncthreads();
-  // ---- CTA partial: M (n x pc, row-major), then |Y_s|^2
+  // ---- CTA partial: M (n x pc, row-major), then |Y_s|^2; warps meet in
+  // shared memory and are summed in warp order
   double* part = a.part + (int64_t)blockIdx.x * PSTR;
+  const int plen = n * pc + pc;
   if (pc > 0) {
-    const int row = 8 * warp + g;
+    double* wp = stage;  // NW x plen
+    for (int idx = tid; idx < NW * plen; idx += SPT) wp[idx] = 0.0;
+    __syncthreads();
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = 2 * t + h;
-      if (row < n && c < pc) part[row * pc + c] = m0[h];
-      if (warp == 0 && 64 + g < n && c < pc) part[(64 + g) * pc + c] = m1[h];
+    for (int j = 0; j < 9; ++j) {
+      if (j >= nm) break;
+      const int row = 8 * j + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 2 * t + h;
+        if (row < n && c < pc) wp[warp * plen + row * pc + c] = m[j][h];
+      }
     }
-    // ysq: thread tid covers column tid / TR
-    double v[SF_P];
-#pragma unroll
-    for (int s = 0; s < SF_P; ++s) v[s] = (tid < TR * pc && tid / TR == s) ? ysq : 0.0;
-    double* outv = red + 8 * SF_P;
-    cta_sum<SF_P>(v, red, outv);
-    if (tid < pc) part[n * pc + tid] = outv[tid];
+    double yw = ysq;
+    yw += __shfl_xor_sync(0xffffffffu, yw, 1);
+    yw += __shfl_xor_sync(0xffffffffu, yw, 2);
+    yw += __shfl_xor_sync(0xffffffffu, yw, 4);
+    if ((lane & 7) == 0 && (lane >> 3) < pc) wp[warp * plen + n * pc + (lane >> 3)] = yw;
+    __syncthreads();
+    for (int e = tid; e < plen; e += SPT) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w) acc += wp[w * plen + e];
+      part[e] = acc;
+    }
   }
   if (!last_cta(a.ticket + 0, flag)) return;
   // ---- last CTA: P1 = Wp^T M (or M), pane bookkeeping
-  double* tot = red + 64;
-  reduce_parts(a.part, n * pc + pc, tot);
+  double* tot = red + NW * (SF_N * SF_P + SF_P) + 64;
+  reduce_parts(a.part, plen * (pc > 0), tot);
   if (pc > 0) {
-    for (int idx = tid; idx < rn * pc; idx += ST) {
-      const int i = idx / pc, s = idx % pc;
+    for (int idx = tid; idx < rn * pc; idx += SPT) {
+      const int i = idx / pc, s2 = idx % pc;
       double acc = 0.0;
       if (pend) {
-        for (int k = 0; k < n; ++k) acc += W[i * LDX + k] * tot[k * pc + s];
+        for (int k = 0; k < n; ++k) acc += W[i * LDW + k] * tot[k * pc + s2];
       } else {
-        acc = tot[i * pc + s];
+        acc = tot[i * pc + s2];
       }
-      st->C[i * SF_P + s] = acc;
+      st->C[i * SF_P + s2] = acc;
     }
     if (tid < pc) st->yn[tid] = tot[n * pc + tid];
   }
@@ -420,7 +535,7 @@ __global__ void __launch_bounds__(ST, 1) sf_update_project(const SFArgs a, int f
     }
   }
   if (final_only)
-    for (int k = tid; k < rn; k += ST) a.sigma[k] = st->sig[k];
+    for (int k = tid; k < rn; k += SPT) a.sigma[k] = st->sig[k];
 }
 
 // ------------------------------------------------------------ generation
@@ -473,7 +588,9 @@ __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
 // ------------------------------------------------------- CGS subtractions
 // mode 0: y1 = Y - U C1 (in place), P2 = U^T y1          -> C += P2
 // mode 1: y2 = y1 - U P2 (in place), G0 = y2^T y2        -> shifted Cholesky
-__global__ void __launch_bounds__(ST, 1) sf_subtract(const SFArgs a, int f, int mode) {
+// Warp w owns rows 8w..8w+7 of every chunk (subtraction tile and its share of
+// the projection / Gram): one CTA barrier per chunk, for the slot refill.
+__global__ void __launch_bounds__(SPT, 1) sf_subtract(const SFArgs a, int f, int mode) {
   extern __shared__ double smem[];
   SFState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -483,39 +600,43 @@ __global__ void __launch_bounds__(ST, 1) sf_subtract(const SFArgs a, int f, int 
   double* Ybuf = a.Yg[f & 1];
   double* Cs = smem;                           // r x SF_P (row-major)
   double* stage = Cs + SF_CAP * SF_P + 8;
-  const int scols = SF_CAP + SF_P;
-  int* flag = reinterpret_cast<int*>(stage + NSTAGE * scols * LDX);
+  const int avail = a.smem_subtract / (int)sizeof(double) - SF_CAP * SF_P - 8 - 16;
+  int* flag = reinterpret_cast<int*>(stage + avail);
   double* red = stage;
   const double* Csrc = mode == 0 ? st->C : st->P2;
-  for (int idx = tid; idx < r * SF_P; idx += ST) Cs[idx] = Csrc[idx];
-  __syncthreads();
-  int c0, c1;
-  cta_chunks(a.n_x, c0, c1);
-  const int nk = (r + 3) >> 2;
-  auto issue = [&](int ch) {
-    if (ch < c1) {
-      double* s = stage + ((ch - c0) % NSTAGE) * scols * LDX;
-      const int64_t i0 = (int64_t)ch * TR;
-      stage_cols(s, r, [&](int c) { return a.U + (int64_t)c * a.ldu; }, i0, a.n_x);
-      stage_cols(s + SF_CAP * LDX, pc, [&](int c) { return Ybuf + (int64_t)c * a.ldy; }, i0, a.n_x);
-    }
-    cp_commit();
+  for (int idx = tid; idx < r * SF_P; idx += SPT) Cs[idx] = Csrc[idx];
+  int64_t ct0, ct1;
+  cta_tiles(a.n_x, ct0, ct1);
+  const int nk = (r + 3) >> 2, nm = (r + 7) >> 3;
+  const int ncol = r + pc;  // tile: U columns, then Y
+  __syncthreads();          // Cs is settled
+  const WRing R = wring(stage, (avail / NW) & ~1, ncol);
+  auto src = [&](int c) -> const double* {
+    return c < r ? a.U + (int64_t)c * a.ldu : Ybuf + (int64_t)(c - r) * a.ldy;
   };
-  double p2[2] = {0.0, 0.0};   // mode 0: P2 rows 8*warp + g (U columns)
-  double gacc[10] = {};        // mode 1: upper triangle of y2^T y2 (thread = row)
-  for (int s = 0; s < NSTAGE - 1; ++s) issue(c0 + s);
-  for (int ch = c0; ch < c1; ++ch) {
-    cp_wait<NSTAGE - 2>();
-    __syncthreads();
-    issue(ch + NSTAGE - 1);
-    double* X = stage + ((ch - c0) % NSTAGE) * scols * LDX;
-    double* Yt = X + SF_CAP * LDX;
-    const int64_t i0 = (int64_t)ch * TR;
-    // D = U_tile C  (rows 8*warp.., cols 0..pc)
+  double p2[8][2];  // mode 0: P2 tile j = U columns 8j.. ; mode 1: p2[0] = Gram
+#pragma unroll
+  for (int j = 0; j < 8; ++j) p2[j][0] = p2[j][1] = 0.0;
+  const int64_t first = ct0 + warp;
+  for (int q = 0; q < R.depth - 1; ++q) {
+    const int64_t tq = first + (int64_t)q * NW;
+    wring_issue(R, q, tq, tq < ct1, ncol, src, a.n_x);
+  }
+  int cur = 0, nxt = R.depth - 1;
+  for (int64_t tile = first; tile < ct1; tile += NW) {
+    {
+      const int64_t tq = tile + (int64_t)(R.depth - 1) * NW;
+      wring_issue(R, nxt, tq, tq < ct1, ncol, src, a.n_x);
+    }
+    cp_wait_dyn(R.depth - 1);
+    __syncwarp();
+    double* X = R.base + (int64_t)cur * R.slot;
+    double* Yt = X + r * LDT;
+    // D = U_rows C  (this tile's 8 rows, columns 0..pc)
     double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
     for (int kk = 0; kk < nk; ++kk) {
       const int k = 4 * kk + t;
-      const double av = (k < r) ? X[k * LDX + 8 * warp + g] : 0.0;
+      const double av = (k < r) ? X[k * LDT + g] : 0.0;
       const double bv = (k < r && g < pc) ? Cs[k * SF_P + g] : 0.0;
       if (kk & 1) dmma884(e0, e1, av, bv);
       else dmma884(d0, d1, av, bv);
@@ -523,97 +644,87 @@ __global__ void __launch_bounds__(ST, 1) sf_subtract(const SFArgs a, int f, int 
     d0 += e0;
     d1 += e1;
     {
-      const int row = 8 * warp + g;
-      const int64_t grow = i0 + row;
+      const int64_t grow = tile * LDT + g;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = 2 * t + h;
         if (c < pc) {
-          const double y = Yt[c * LDX + row] - (h ? d1 : d0);
-          Yt[c * LDX + row] = y;
+          const double y = Yt[c * LDT + g] - (h ? d1 : d0);
+          Yt[c * LDT + g] = y;
           if (grow < a.n_x) Ybuf[grow + (int64_t)c * a.ldy] = y;
         }
       }
     }
-    __syncthreads();
-    if (mode == 0) {
-      if (8 * warp < r) {
-#pragma unroll 4
-        for (int kk = 0; kk < TR / 4; ++kk) {
-          const double av = X[(8 * warp + g) * LDX + 4 * kk + t];
-          const double bv = (g < pc) ? Yt[g * LDX + 4 * kk + t] : 0.0;
-          dmma884(p2[0], p2[1], av, bv);
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int rho = 4 * kk + t;
+      const double yv = (g < pc) ? Yt[g * LDT + rho] : 0.0;
+      if (mode == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j >= nm) break;
+          const double av = (8 * j + g < r) ? X[(8 * j + g) * LDT + rho] : 0.0;
+          dmma884(p2[j][0], p2[j][1], av, yv);
         }
+      } else {
+        dmma884(p2[0][0], p2[0][1], yv, yv);  // G[g][2t..] += y2[rho][g] y2[rho][2t..]
       }
-    } else if (tid < TR) {
-      double y[SF_P];
-#pragma unroll
-      for (int s = 0; s < SF_P; ++s) y[s] = s < pc ? Yt[s * LDX + tid] : 0.0;
-      int q = 0;
-#pragma unroll
-      for (int u = 0; u < SF_P; ++u)
-#pragma unroll
-        for (int v = u; v < SF_P; ++v) gacc[q++] += y[u] * y[v];
     }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    cur = cur + 1 == R.depth ? 0 : cur + 1;
+    nxt = nxt + 1 == R.depth ? 0 : nxt + 1;
   }
   cp_wait<0>();
   __syncthreads();
+  // ---- CTA partial (warp partials summed in warp order)
   double* part = a.part + (int64_t)blockIdx.x * PSTR;
-  int plen;
+  const int plen = mode == 0 ? r * pc : pc * pc;
+  double* wp = stage;
+  for (int idx = tid; idx < NW * plen; idx += SPT) wp[idx] = 0.0;
+  __syncthreads();
   if (mode == 0) {
-    const int row = 8 * warp + g;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= nm) break;
+      const int row = 8 * j + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 2 * t + h;
+        if (row < r && c < pc) wp[warp * plen + row * pc + c] = p2[j][h];
+      }
+    }
+  } else {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = 2 * t + h;
-      if (row < r && c < pc) part[row * pc + c] = p2[h];
+      if (g < pc && c < pc) wp[warp * plen + g * pc + c] = p2[0][h];
     }
-    plen = r * pc;
-  } else {
-    double* outv = red + 8 * 10;
-    cta_sum<10>(gacc, red, outv);
-    if (tid < 10) part[tid] = outv[tid];
-    plen = 10;
+  }
+  __syncthreads();
+  for (int e = tid; e < plen; e += SPT) {
+    double acc = 0.0;
+    for (int w = 0; w < NW; ++w) acc += wp[w * plen + e];
+    part[e] = acc;
   }
   if (!last_cta(a.ticket + 1 + mode, flag)) return;
-  double* tot = red + 256;
+  double* tot = red + NW * SF_CAP * SF_P + 64;
   reduce_parts(a.part, plen, tot);
   if (mode == 0) {
-    for (int idx = tid; idx < r * pc; idx += ST) {
-      const int i = idx / pc, s = idx % pc;
-      st->P2[i * SF_P + s] = tot[idx];
-      st->C[i * SF_P + s] += tot[idx];
+    for (int idx = tid; idx < r * pc; idx += SPT) {
+      const int i = idx / pc, s2 = idx % pc;
+      st->P2[i * SF_P + s2] = tot[idx];
+      st->C[i * SF_P + s2] += tot[idx];
     }
     return;
   }
-  if (tid != 0) return;
-  // shifted Cholesky of G0 (Fukaya et al. shifted CholeskyQR3, first step);
-  // a remainder at the block's rounding floor 16 eps ||Y|| is dropped whole
-  double G[16] = {};
-  int q = 0;
-  for (int u = 0; u < SF_P; ++u)
-    for (int v = u; v < SF_P; ++v) {
-      G[u * 4 + v] = G[v * 4 + u] = tot[q];
-      ++q;
-    }
-  double tr = 0.0, ysq = 0.0;
-  for (int s = 0; s < pc; ++s) { tr += G[s * 5]; ysq += st->yn[s]; }
-  const double delta = 16.0 * DEPS * sqrt(ysq);
-  st->drop_all = !(sqrt(tr) > delta);
-  double R[16], Z[16];
-  if (st->drop_all) {
-    for (int i = 0; i < 16; ++i) { R[i] = 0.0; Z[i] = 0.0; }
-  } else {
-    const double shift = 11.0 * ((double)a.n_x * pc + pc * (pc + 1)) * DEPS * tr;
-    for (int s = 0; s < pc; ++s) G[s * 5] += shift;
-    pivoted_chol4(G, pc, 0.0, R, Z);
-  }
-  for (int i = 0; i < 16; ++i) { st->Rc[i] = R[i]; st->Rinv[i] = Z[i]; }
+  if (tid == 0) sf_shifted_chol(a, st, tot, pc);
 }
 
 // ----------------------------------------------------------- CholeskyQR passes
 // G = Q^T Q with Q = y2 Rinv; R <- chol(G) R, Rinv <- Rinv chol(G)^{-1}
 // (pivoted, drop-tolerant).  Light streaming kernel (4 columns, L2-resident).
-__global__ void __launch_bounds__(ST) sf_cholqr(const SFArgs a, int f, int pass) {
+__global__ void __launch_bounds__(ST, 4) sf_cholqr(const SFArgs a, int f, int pass) {
   SFState* st = a.st;
   __shared__ int flag;
   __shared__ double red[8 * 10 + 16];
@@ -627,22 +738,31 @@ __global__ void __launch_bounds__(ST) sf_cholqr(const SFArgs a, int f, int pass)
 #pragma unroll
     for (int i = 0; i < 16; ++i) Ri[i] = st->Rinv[i];
     const double* Y = a.Yg[f & 1];
-    for (int64_t i = (int64_t)blockIdx.x * ST + tid; i < a.n_x; i += (int64_t)gridDim.x * ST) {
-      double y[SF_P], qv[SF_P];
+    const int64_t stride = (int64_t)gridDim.x * ST;
+    for (int64_t i0 = (int64_t)blockIdx.x * ST + tid; i0 < a.n_x; i0 += 2 * stride) {
+      double y[2][SF_P];
 #pragma unroll
-      for (int s = 0; s < SF_P; ++s) y[s] = s < pc ? Y[i + (int64_t)s * a.ldy] : 0.0;
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = i0 + h * stride;
 #pragma unroll
-      for (int c = 0; c < SF_P; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int s = 0; s < SF_P; ++s) acc += y[s] * Ri[s * 4 + c];
-        qv[c] = acc;
+        for (int s = 0; s < SF_P; ++s) y[h][s] = (s < pc && i < a.n_x) ? Y[i + (int64_t)s * a.ldy] : 0.0;
       }
-      int q = 0;
 #pragma unroll
-      for (int u = 0; u < SF_P; ++u)
+      for (int h = 0; h < 2; ++h) {
+        double qv[SF_P];
 #pragma unroll
-        for (int v = u; v < SF_P; ++v) gacc[q++] += qv[u] * qv[v];
+        for (int c = 0; c < SF_P; ++c) {
+          double acc = 0.0;
+#pragma unroll
+          for (int s = 0; s < SF_P; ++s) acc += y[h][s] * Ri[s * 4 + c];
+          qv[c] = acc;
+        }
+        int q = 0;
+#pragma unroll
+        for (int u = 0; u < SF_P; ++u)
+#pragma unroll
+          for (int v = u; v < SF_P; ++v) gacc[q++] += qv[u] * qv[v];
+      }
     }
   }
   double* outv = red + 8 * 10;
@@ -651,24 +771,7 @@ __global__ void __launch_bounds__(ST) sf_cholqr(const SFArgs a, int f, int pass)
   if (tid < 10) part[tid] = outv[tid];
   if (!last_cta(a.ticket + 3 + pass, &flag)) return;
   reduce_parts(a.part, 10, tot);
-  if (tid == 0 && !skip) {
-    double G[16] = {};
-    int q = 0;
-    for (int u = 0; u < SF_P; ++u)
-      for (int v = u; v < SF_P; ++v) {
-        G[u * 4 + v] = G[v * 4 + u] = tot[q];
-        ++q;
-      }
-    double R1[16], Z1[16], Rc[16], Ri[16];
-    // pivots below (1e-10)^2 of the leading one are rounding residue of a
-    // numerically rank-deficient remainder: dropped (see header)
-    pivoted_chol4(G, pc, 1e-20, R1, Z1);
-    for (int i = 0; i < 16; ++i) { Rc[i] = st->Rc[i]; Ri[i] = st->Rinv[i]; }
-    double Rn[16], Zn[16];
-    mat4_mul(R1, Rc, Rn, pc);
-    mat4_mul(Ri, Z1, Zn, pc);
-    for (int i = 0; i < 16; ++i) { st->Rc[i] = Rn[i]; st->Rinv[i] = Zn[i]; }
-  }
+  if (tid == 0 && !skip) sf_chol_update(st, tot, pc);
 }
 
 // The flush's small algebra (one CTA): rank-revealing fix-up of R, core
@@ -785,12 +888,8 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
 }
 
 // ------------------------------------------------------------------ host side
-size_t sf_smem_update() {
-  return ((size_t)SF_N * LDX + (size_t)NSTAGE * (SF_CAP + 2 * SF_P) * LDX) * sizeof(double) + 64;
-}
-size_t sf_smem_subtract() {
-  return ((size_t)SF_CAP * SF_P + 8 + (size_t)NSTAGE * (SF_CAP + SF_P) * LDX) * sizeof(double) + 64;
-}
+size_t sf_smem_update() { return 200 * 1024; }
+size_t sf_smem_subtract() { return 200 * 1024; }
 size_t sf_smem_finish() {
   return (size_t)(16 + 16 + SF_N + 4 + 512 + 4 * (SF_N * SF_N + 8) + 2 * SF_N + 16) * sizeof(double);
 }
@@ -821,7 +920,7 @@ cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, int
   if (e != cudaSuccess) return e;
   const int G = a.G;
   const int Gg = a.Ggen;
-  const size_t su = sf_smem_update(), ss = sf_smem_subtract(), sfin = sf_smem_finish();
+  const size_t su = a.smem_update, ss = a.smem_subtract, sfin = sf_smem_finish();
   int64_t nl = 0;
   const int dbg = a.dbg_print;
   auto show = [&](const char* what, int f) {
@@ -836,12 +935,12 @@ cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, int
   sf_generate<<<Gg, ST, 0, s>>>(a, 0);
   ++nl;
   for (int f = 0; f < nflush; ++f) {
-    sf_update_project<<<G, ST, su, s>>>(a, f, 0);
+    sf_update_project<<<G, SPT, su, s>>>(a, f, 0);
     show("update", f);
     if (f + 1 < nflush) { sf_generate<<<Gg, ST, 0, s>>>(a, f + 1); ++nl; }
-    sf_subtract<<<G, ST, ss, s>>>(a, f, 0);
+    sf_subtract<<<G, SPT, ss, s>>>(a, f, 0);
     show("sub1", f);
-    sf_subtract<<<G, ST, ss, s>>>(a, f, 1);
+    sf_subtract<<<G, SPT, ss, s>>>(a, f, 1);
     show("sub2", f);
     sf_cholqr<<<Gg, ST, 0, s>>>(a, f, 0);
     sf_cholqr<<<Gg, ST, 0, s>>>(a, f, 1);
@@ -850,7 +949,7 @@ cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, int
     show("finish", f);
     nl += 6;
   }
-  sf_update_project<<<G, ST, su, s>>>(a, nflush, 1);
+  sf_update_project<<<G, SPT, su, s>>>(a, nflush, 1);
   ++nl;
   if (launches) *launches += nl;
   return cudaGetLastError();

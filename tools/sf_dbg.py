@@ -11,7 +11,7 @@ rhs = lp.LowRankMat(rng.standard_normal((grid.n_x, 1)), np.eye(n_t)[:, :1])
 pol = lp.TruncationPolicy(1e-8, 64)
 for form in ("0", "1"):
     os.environ["LRK_SFLUSH"] = form
-    os.environ["LRK_SF_DEBUG"] = "0"
+    os.environ["LRK_SF_DEBUG"] = os.environ.get("DBG", "0") if form == "1" else "0"
     tr = []
     Y = lp.st_solve_sweep(K, rhs, pol, trace=tr)
     print(form, tr, np.linalg.svd(lp.lr_to_dense(Y), compute_uv=False)[:6], flush=True)
