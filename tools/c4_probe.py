@@ -16,7 +16,8 @@ layout = lp.make_sensor_subgrid(grid, n_side // 4, time_every=4)
 ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov, pol=lp.TruncationPolicy(1e-8, 64))
 v = torch.as_tensor(np.random.default_rng(3).standard_normal(grid.n_x), device="cuda")
 v /= v.norm()
-for i in range(3):
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+for i in range(reps):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     out = ctx.apply(v)
     torch.cuda.synchronize(); t1 = time.perf_counter()
