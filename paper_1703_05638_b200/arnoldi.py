@@ -487,6 +487,36 @@ def lr_arnoldi(apply, v1, pol: TruncationPolicy, stop: StopRule,
                          restarts=restarts)
 
 
+def start_vector(n_x: int, n_t: int | None = None, mode: str = "ic", start: str = "ones",
+                 seed: int = 0, device=None):
+    """Seeded Arnoldi start (cli.py:247-266): all-ones by default, otherwise
+    numpy's PCG64 `default_rng(seed).standard_normal`, generated on the host
+    (so the bits are the reference's) and normalised.  IC / steady modes give a
+    unit n_x vector; source mode a rank-1 field whose two factors have unit
+    norm (W1 drawn before W2, as the reference).  `device=None` returns host
+    numpy (what the reference returns); a torch device returns device data."""
+    if start not in ("ones", "random"):
+        raise ValueError(f"start must be 'ones' or 'random', got {start!r}")
+    if mode == "source":
+        if n_t is None:
+            raise ValueError("source mode needs n_t")
+        if start == "ones":
+            w1 = np.ones((n_x, 1)) / np.sqrt(n_x)
+            w2 = np.ones((n_t, 1)) / np.sqrt(n_t)
+        else:
+            rng = np.random.default_rng(seed)
+            w1 = rng.standard_normal((n_x, 1))
+            w2 = rng.standard_normal((n_t, 1))
+            w1 /= np.linalg.norm(w1)
+            w2 /= np.linalg.norm(w2)
+        return LowRankMat(w1, w2)
+    v = np.ones(n_x) if start == "ones" else np.random.default_rng(seed).standard_normal(n_x)
+    v = v / np.linalg.norm(v)
+    if device is None:
+        return v
+    return _torch().as_tensor(v, dtype=_torch().float64).to(device)
+
+
 def rank_one_check(vec, reshape=None, tail_tol: float = 1e-6):
     """Numerical separation rank of a vector (arnoldi.py:378-399); diagnostic."""
     if isinstance(vec, LowRankMat):

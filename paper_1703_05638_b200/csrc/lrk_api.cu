@@ -59,12 +59,16 @@ struct lrk_ctx {
   // instrumentation
   bool prof = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  lrk::SFAux aux{};           // second stream of the streaming-flush sweep
   double prof_ms = 0.0, prof_bytes = 0.0;
   int64_t prof_n = 0;
   std::vector<int> last_fwd, last_bwd;
   int last_obs = 0;
   ~lrk_ctx() {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
+    if (aux.ready) cudaEventDestroy(aux.ready);
+    if (aux.done) cudaEventDestroy(aux.done);
+    if (aux.stream) cudaStreamDestroy(aux.stream);
     for (auto& kv : ws) cudaFree(kv.second.p);
     cudaFree(dS); cudaFree(dTheta); cudaFree(dThetaM); cudaFree(dE0); cudaFree(dInvLam);
     cudaFree(dLam); cudaFree(dSsq);
@@ -382,17 +386,23 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
       sa.n_x = nx; sa.n_t = nt; sa.p = p; sa.cap = ucap; sa.adjoint = adjoint; sa.r_max = r_max;
       sa.nflush = nflush; sa.eps0 = eps0; sa.ftz = a.ftz;
       sa.U = U0; sa.ldu = ld; sa.V = V0; sa.ldv = nt;
-      sa.Yg[0] = ybuf; sa.Yg[1] = qbuf; sa.ldy = ld;
+      WS(double, ybuf3, "sw_ybuf3", ld * (int64_t)p);
+      sa.Yg[0] = ybuf; sa.Yg[1] = qbuf; sa.Yg[2] = ybuf3; sa.ldy = ld;
+      sa.n_x_glob = nx;
       sa.yprev = yprev; sa.theta = c->dTheta; sa.rowscale = c->dThetaM;
       sa.B = B; sa.ldb = ldb; sa.rb = rb; sa.rb_dev = rb_dev; sa.W2 = W2; sa.ldw2 = ldw2;
       sa.part = sfpart; sa.ticket = tick; sa.st = sfst;
       sa.trace = trace; sa.info = info; sa.sigma = sig;
       sa.G = Gs; sa.Ggen = 8 * c->num_sms;
       sa.dbg_print = std::getenv("LRK_SF_DEBUG") ? std::atoi(std::getenv("LRK_SF_DEBUG")) : 0;
-      sa.smem_update = (int)sf_smem_update();
-      sa.smem_subtract = (int)sf_smem_subtract();
+      sa.smem_pass = (int)sf_smem_pass();
+      if (!c->aux.stream) {
+        CK(cudaStreamCreateWithFlags(&c->aux.stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->aux.ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->aux.done, cudaEventDisableTiming));
+      }
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
-      CK(launch_sweep_stream(sa, nflush, s, &c->launches));
+      CK(launch_sweep_stream(sa, nflush, s, c->aux, &c->launches));
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
       o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
       o.ucap = ucap; o.nflush = nflush; o.ldu = ld; o.ldv = nt;

@@ -93,20 +93,23 @@ constexpr int SF_N = SF_CAP + SF_P;
 constexpr int SF_LDW = 68;
 
 // Small per-sweep state in global memory (written by the last CTA of each
-// pass, read by the next pass).
+// pass and by sf_finish, read by the next pass).
 struct SFState {
   int r;         // valid pane columns of U (after the last applied update)
   int rn;        // pane rank of the pending update
-  int pcp;       // remainder width of the pending update
+  int pcp;       // width of the remainder block next to U (X = [U, y])
   int pending;   // an update (Wp, Vc) is pending
   int startp;    // flush start of the pending update (time-row selection)
   int drop_all;  // the current remainder is at the rounding floor
-  int pc;        // width of the current flush
+  int pc_new;    // width of the flush being projected (Yn)
   int pad;
   double sig[SF_N];
-  double C[SF_CAP * SF_P];   // C1 (+ P2) of the current flush, [i * SF_P + s]
+  double C[SF_CAP * SF_P];   // C1 (+ P2) of the flush being orthogonalised, [i * SF_P + s]
   double P2[SF_CAP * SF_P];
-  double yn[SF_P];
+  double M[SF_N * SF_P];     // [U, y2]^T Yn of the next flush, [k * SF_P + s]
+  double Wd[SF_N * SF_P];    // -Wp C1: y1 = Yn + [U, y2] Wd, [k * SF_P + s]
+  double yn[SF_P];           // |Y_s|^2 of the flush being orthogonalised
+  double yn_next[SF_P];      // ... of the flush being projected
   double Rc[16];             // remainder R (row-major 4x4)
   double Rinv[16];           // Q = y2 Rinv
   double Wp[SF_N * SF_LDW];  // pending spatial update (n x rn), col-major
@@ -115,11 +118,12 @@ struct SFState {
 
 struct SFArgs {
   int64_t n_x;
+  int64_t n_x_glob;      // rows of the whole (unsharded) field
   int n_t, p, cap, adjoint, r_max, nflush;
   double eps0, ftz;
   double* U; int64_t ldu;
   double* V; int64_t ldv;
-  double* Yg[2]; int64_t ldy;
+  double* Yg[3]; int64_t ldy;   // flush f lives in Yg[f % 3]
   double* yprev;
   const double* theta;
   const double* rowscale;
@@ -133,12 +137,18 @@ struct SFArgs {
   int G;                 // CTAs of the staged row passes
   int Ggen;              // CTAs of the light grid-stride passes
   int dbg_print;         // LRK_SF_DEBUG: flushes to report (diagnostics)
-  int smem_update, smem_subtract;  // dynamic shared memory of the staged passes (bytes)
+  int smem_pass;         // dynamic shared memory of the staged passes (bytes)
 };
-size_t sf_smem_update();
-size_t sf_smem_subtract();
+size_t sf_smem_pass();
 int64_t sf_part_stride();
-cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, int64_t* launches);
+// aux: a second (non-blocking) stream + two events, used to run the next
+// flush's column generation under the single-CTA core SVD.
+struct SFAux {
+  cudaStream_t stream;
+  cudaEvent_t ready, done;
+};
+cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, const SFAux& aux,
+                                int64_t* launches);
 
 // General lr_truncate (lowrank.py:124-144) of W1 (n_x x R) W2^T (n_t x R).
 struct TruncArgs {

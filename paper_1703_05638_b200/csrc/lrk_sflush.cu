@@ -9,30 +9,33 @@
 // differs is the organisation, built for HBM streaming when the CTA row blocks
 // cannot stay resident in shared memory:
 //
-//   sf_update_project  U' = [U, y2] W' (the PREVIOUS flush's basis update,
-//                      the remainder's transform folded into W'), V' likewise
-//                      on the time rows; M = [U, y2]^T Y for the new columns
-//                      (P1 = W'^T M) and |Y|^2                 -> C1
-//   sf_generate        the next flush's columns y_k = theta y_{k-1} + B~ w2_k
-//   sf_sub_project     y1 = Y - U C1, P2 = U^T y1              -> C = C1 + P2
-//   sf_sub_gram        y2 = y1 - U P2, G0 = y2^T y2            -> shifted Cholesky R0
-//   sf_cholqr (x2)     G = (y2 R^-1)^T (y2 R^-1)               -> R <- chol(G) R
-//                      (shifted CholeskyQR3 of the 4-column remainder, pivoted
-//                      and drop-tolerant for numerically rank-deficient
-//                      remainders), then on the last pass the flush's small
-//                      algebra in one CTA: the rank-revealing fix-up with the
-//                      rounding-floor drop of the persistent kernel, the core
-//                      SVD (register Jacobi), _rank_cut (lowrank.py:98-111)
-//                      and the update matrices W' for the next launch.
+//   sf_pass<0> (A)   closes flush f-1 and opens flush f in ONE read of U:
+//                      y2 = y1 - U P2 (second CGS subtraction of flush f-1),
+//                      G0 = y2^T y2 -> shifted Cholesky R0, and the projection
+//                      M = [U, y2]^T Y_f of the next flush's columns plus |Y_f|^2
+//   sf_cholqr (x2)     G = (y2 R^-1)^T (y2 R^-1) -> R <- chol(G) R  (shifted
+//                      CholeskyQR3 of the 4-column remainder, pivoted and
+//                      drop-tolerant for numerically rank-deficient remainders)
+//   sf_finish          one CTA: rank-revealing fix-up with the rounding-floor
+//                      drop of the persistent kernel, core SVD (register
+//                      Jacobi), _rank_cut (lowrank.py:98-111), the update
+//                      matrices W' and, for flush f, C1 = W'^T M and
+//                      Wd = -W' C1                       (runs next to sf_generate)
+//   sf_pass<1> (B)   the basis update of flush f-1 and the first CGS pass of
+//                      flush f in ONE read of U: U' = [U, y2] W' (in place, V'
+//                      likewise on the time rows), y1 = Y_f + [U, y2] Wd
+//                      (= Y_f - U' C1), Pm = [U, y2]^T y1 -> P2 = W'^T Pm
+//   sf_generate        the next flush's columns y_k = theta y_{k-1} + B~ w2_k,
+//                      on a second stream under sf_finish (three Y buffers)
 //
-// Each kernel streams its CTA's contiguous rows in 64-row chunks through a
-// TMA bulk-copy ring (cp.async.bulk + mbarriers, depth sized from the actual
-// pane rank so ~150 KB are in flight per SM), runs the row x small
-// products on the FP64 tensor pipe (DMMA m8n8k4) from shared memory, writes a
-// CTA partial and the LAST CTA to finish (atomic ticket) reduces the partials
-// in CTA order — deterministic, no grid barrier, no cooperative launch.  Per
-// flush the pane basis U is read three times and written once (the persistent
-// kernel read it four times and streamed it at ~1/3 of the HBM share).
+// Per flush the pane basis U is read twice and written once — the compulsory
+// traffic of a truncation (Gram read, update read, update write).
+// Each pass streams its CTA's contiguous rows in 8-row tiles through
+// warp-private cp.async rings (depth sized from the actual pane rank), runs
+// the row x small products on the FP64 tensor pipe (DMMA m8n8k4) from shared
+// memory, writes a CTA partial and the LAST CTA to finish (atomic ticket)
+// reduces the partials in CTA order — deterministic, no grid barrier, no
+// cooperative launch.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -49,7 +52,7 @@ constexpr int ST = 256;           // threads per CTA of the light passes
 constexpr int NW = 16;            // warps of the staged row passes
 constexpr int SPT = 32 * NW;
 constexpr int LDW = 68;           // shared leading dimension of the update matrix (== 4 mod 16)
-constexpr int PSTR = SF_N * SF_P + SF_P + 8;  // per-CTA partial stride (doubles)
+constexpr int PSTR = SF_N * SF_P + 16 + SF_P + 4;  // per-CTA partial stride (doubles)
 
 // ---- warp-private cp.async rings.  Every staged pass works on 8-row tiles
 // and each warp only ever touches its own tiles (the update tile, its share
@@ -167,21 +170,33 @@ __device__ __forceinline__ bool last_cta(unsigned* ticket, int* flag) {
   return *flag != 0;
 }
 
-// out[e] = sum over CTAs of part[c * PSTR + e], e < len: one warp per entry,
-// lanes stride over the CTAs (independent loads in flight), then a fixed
-// shuffle tree — deterministic.
+// out[e] = sum over CTAs of part[c * PSTR + e], e < len: one warp per pair of
+// entries, lanes stride over the CTAs with 16 independent loads in flight,
+// then a fixed tree — deterministic.
 __device__ __forceinline__ void reduce_parts(const double* part, int len, double* out) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = w; e < len; e += nw) {
-    double s0 = 0.0, s1 = 0.0;
-    int c = lane;
-    for (; c + 32 < (int)gridDim.x; c += 64) {
-      s0 += __ldcg(part + (int64_t)c * PSTR + e);
-      s1 += __ldcg(part + (int64_t)(c + 32) * PSTR + e);
+  const int G = (int)gridDim.x;
+  for (int e = 2 * w; e < len; e += 2 * nw) {
+    const bool two = e + 1 < len;
+    double a0 = 0.0, a1 = 0.0;
+    for (int c0 = 0; c0 < G; c0 += 256) {
+      double v[8], u[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = c0 + lane + 32 * i;
+        const bool ok = c < G;
+        v[i] = ok ? __ldcg(part + (int64_t)c * PSTR + e) : 0.0;
+        u[i] = (ok && two) ? __ldcg(part + (int64_t)c * PSTR + e + 1) : 0.0;
+      }
+      a0 += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+      a1 += ((u[0] + u[1]) + (u[2] + u[3])) + ((u[4] + u[5]) + (u[6] + u[7]));
     }
-    if (c < (int)gridDim.x) s0 += __ldcg(part + (int64_t)c * PSTR + e);
-    const double v = warp_sum(s0 + s1);
-    if (lane == 0) out[e] = v;
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    if (lane == 0) {
+      out[e] = a0;
+      if (two) out[e + 1] = a1;
+    }
   }
   __syncthreads();
 }
@@ -302,15 +317,15 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
 
 }  // namespace
 
-// Tail of the second CGS pass (thread 0): the shifted Cholesky factor of
-// G0 = y2^T y2 (Fukaya et al. shifted CholeskyQR3, first step); a remainder at
-// the block's rounding floor 16 eps ||Y|| is dropped whole.  Out of line: keeps
-// the streaming kernel's register count low.
-static __device__ __noinline__ void sf_shifted_chol(const SFArgs& a, SFState* st, const double* tot,
+// Tail of pass A (thread 0): the shifted Cholesky factor of G0 = y2^T y2
+// (Fukaya et al. shifted CholeskyQR3, first step); a remainder at the block's
+// rounding floor 16 eps ||Y|| is dropped whole.  G0 is row-major with stride 4.
+// Out of line: keeps the streaming kernel's register count low.
+static __device__ __noinline__ void sf_shifted_chol(const SFArgs& a, SFState* st, const double* G0,
                                                     int pc) {
   double G[16] = {};
   for (int u = 0; u < pc; ++u)
-    for (int v = 0; v < pc; ++v) G[u * 4 + v] = tot[u * pc + v];
+    for (int v = 0; v < pc; ++v) G[u * 4 + v] = G0[u * 4 + v];
   double tr = 0.0, ysq = 0.0;
   for (int s = 0; s < pc; ++s) { tr += G[s * 5]; ysq += st->yn[s]; }
   const double delta = 16.0 * DEPS * sqrt(ysq);
@@ -319,7 +334,7 @@ static __device__ __noinline__ void sf_shifted_chol(const SFArgs& a, SFState* st
   if (st->drop_all) {
     for (int i = 0; i < 16; ++i) { Rm[i] = 0.0; Zm[i] = 0.0; }
   } else {
-    const double shift = 11.0 * ((double)a.n_x * pc + pc * (pc + 1)) * DEPS * tr;
+    const double shift = 11.0 * ((double)a.n_x_glob * pc + pc * (pc + 1)) * DEPS * tr;
     for (int s = 0; s < pc; ++s) G[s * 5] += shift;
     pivoted_chol4(G, pc, 0.0, Rm, Zm);
   }
@@ -345,75 +360,89 @@ static __device__ __noinline__ void sf_chol_update(SFState* st, const double* to
   for (int i = 0; i < 16; ++i) { st->Rc[i] = Rn[i]; st->Rinv[i] = Zn[i]; }
 }
 
-// --------------------------------------------------------------- update + project
-// Pending update (st->pending): U'[:, :rn] = [U[:, :r], y2] Wp, V' likewise;
-// then (unless final) P1 = U'^T Y evaluated as Wp^T ([U, y2]^T Y).
-// Warp w owns rows 8w..8w+7 of every 128-row chunk: the update tile and its
-// share of the projection need no CTA barrier inside a chunk.
-__global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int f, int final_only) {
+// ------------------------------------------------------------ staged row pass
+// X = [U(:, :r), y] with y the pcp-column block of flush f-1 in Yg[(f-1) % 3]
+// (y1 on entry to pass A, y2 afterwards); Yn = the pcn columns of flush f.
+//
+// MODE 0 (pass A):  y2 = y1 - U P2 = X [-P2; I]            (in place)
+//                   T  = X^T [Yn | y2]: M = X^T Yn (n x 4), G0 = y2^T y2, |Yn_s|^2
+//   last CTA: M, yn_next -> state; shifted Cholesky of G0.
+// MODE 1 (pass B):  [U' | d] = X [Wp | Wd]: U' in place over U (rn columns),
+//                   y1 = Yn + d (in place), V' = [V, E] Vc on this CTA's time rows
+//                   Pm = X^T y1 (n x 4)
+//   last CTA: P2 = Wp^T Pm, C = C1 + P2, pane bookkeeping (r <- rn, pcp <- pcn).
+// Warp w owns tiles w, w+16, ... of the CTA's 8-row tile range: its step-1
+// output tile and its share of the projections need no CTA barrier.
+template <int MODE>
+__global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
   extern __shared__ double smem[];
   SFState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int r = st->r;
-  const bool pend = st->pending != 0;
-  const int pcp = pend ? st->pcp : 0;
-  const int n = r + pcp;                      // columns of X = [U, y2]
-  const int rn = pend ? st->rn : r;           // columns of U'
+  const int r = st->r, pcp = st->pcp;
+  const int n = r + pcp;                      // columns of X
   const int start = f * a.p;
-  const int pc = final_only ? 0 : min(a.p, a.n_t - start);
-  const double* Ycur = a.Yg[f & 1];
-  const double* Y2 = a.Yg[(f + 1) & 1];       // the previous flush's remainder
-  double* W = smem;                           // Wp (n x rn), column c at W + c * LDW
-  double* stage = W + SF_N * LDW;             // V update scratch, then the warp rings
-  const int avail = a.smem_update / (int)sizeof(double) - SF_N * LDW - 16;
+  const int pcn = f < a.nflush ? min(a.p, a.n_t - start) : 0;
+  const int rn = MODE == 1 ? st->rn : 0;
+  const int nwc = MODE == 1 ? rn + pcn : pcp;   // columns of the step-1 matrix W
+  double* Yab = a.Yg[(f + 2) % 3];            // flush f-1
+  double* Ynb = a.Yg[f % 3];                  // flush f
+  double* W = smem;                           // n x nwc, column c at W + c * LDW
+  double* stage = W + (SF_N + SF_P) * LDW;    // V update scratch, then the warp rings
+  const int avail = a.smem_pass / (int)sizeof(double) - (SF_N + SF_P) * LDW - 16;
   int* flag = reinterpret_cast<int*>(stage + avail);
   double* red = stage;                        // reused after the main loop
 
-  if (pend) {
-    for (int idx = tid; idx < n * rn; idx += SPT) {
+  if (MODE == 0) {
+    for (int idx = tid; idx < n * pcp; idx += SPT) {
       const int k = idx % n, c = idx / n;
-      W[c * LDW + k] = st->Wp[k + c * SF_LDW];
+      W[c * LDW + k] = k < r ? -st->P2[k * SF_P + c] : (k - r == c ? 1.0 : 0.0);
     }
-    // time rows of this CTA: V' = [V, E] Vc   (in place, via shared memory)
-    const int64_t tper = ((int64_t)a.n_t + gridDim.x - 1) / gridDim.x;
-    const int64_t nt64 = a.n_t;
-    const int64_t t0 = min(nt64, (int64_t)blockIdx.x * tper), t1 = min(nt64, t0 + tper);
-    const int nrow = (int)(t1 - t0);
-    double* Vs = stage;  // nrow x r
-    double* Vc = stage + nrow * SF_CAP + 8;
-    for (int idx = tid; idx < n * rn; idx += SPT) Vc[idx] = st->Vc[(idx % n) + (idx / n) * SF_LDW];
-    for (int idx = tid; idx < nrow * r; idx += SPT)
-      Vs[idx] = a.V[(t0 + idx % nrow) + (int64_t)(idx / nrow) * a.ldv];
-    __syncthreads();
-    const int sp = st->startp;
-    for (int idx = tid; idx < nrow * rn; idx += SPT) {
-      const int tl = idx % nrow, c = idx / nrow;
-      const int64_t tt = t0 + tl;
-      const int sel = a.adjoint ? (a.n_t - 1 - sp) - (int)tt : (int)tt - sp;
-      double acc = (sel >= 0 && sel < pcp) ? Vc[(r + sel) + c * n] : 0.0;
-      for (int k = 0; k < r; ++k) acc += Vs[tl + k * nrow] * Vc[k + c * n];
-      a.V[tt + (int64_t)c * a.ldv] = acc;
+  } else {
+    for (int idx = tid; idx < n * nwc; idx += SPT) {
+      const int k = idx % n, c = idx / n;
+      W[c * LDW + k] = c < rn ? st->Wp[k + c * SF_LDW] : st->Wd[k * SF_P + (c - rn)];
+    }
+    if (st->pending) {
+      // time rows of this CTA: V' = [V, E] Vc   (in place, via shared memory)
+      const int64_t tper = ((int64_t)a.n_t + gridDim.x - 1) / gridDim.x;
+      const int64_t nt64 = a.n_t;
+      const int64_t t0 = min(nt64, (int64_t)blockIdx.x * tper), t1 = min(nt64, t0 + tper);
+      const int nrow = (int)(t1 - t0);
+      double* Vs = stage;  // nrow x r
+      double* Vc = stage + nrow * SF_CAP + 8;
+      for (int idx = tid; idx < n * rn; idx += SPT) Vc[idx] = st->Vc[(idx % n) + (idx / n) * SF_LDW];
+      for (int idx = tid; idx < nrow * r; idx += SPT)
+        Vs[idx] = a.V[(t0 + idx % nrow) + (int64_t)(idx / nrow) * a.ldv];
+      __syncthreads();
+      const int sp = st->startp;
+      for (int idx = tid; idx < nrow * rn; idx += SPT) {
+        const int tl = idx % nrow, c = idx / nrow;
+        const int64_t tt = t0 + tl;
+        const int sel = a.adjoint ? (a.n_t - 1 - sp) - (int)tt : (int)tt - sp;
+        double acc = (sel >= 0 && sel < pcp) ? Vc[(r + sel) + c * n] : 0.0;
+        for (int k = 0; k < r; ++k) acc += Vs[tl + k * nrow] * Vc[k + c * n];
+        a.V[tt + (int64_t)c * a.ldv] = acc;
+      }
     }
   }
 
   int64_t ct0, ct1;
   cta_tiles(a.n_x, ct0, ct1);
-  const int nk = (n + 3) >> 2, nj = (rn + 7) >> 3, nm = (n + 7) >> 3;
-  const double* U = a.U;
-  const int ncol = n + pc;  // tile: X = [U, y2] columns, then Y
-  __syncthreads();          // W and the V-update scratch are settled
+  const int nk = (n + 3) >> 2, njw = (nwc + 7) >> 3, nm = (n + 7) >> 3;
+  const int ncol = n + pcn;  // tile: X columns, then Yn
+  __syncthreads();           // W and the V-update scratch are settled
   const WRing R = wring(stage, (avail / NW) & ~1, ncol);
   auto src = [&](int c) -> const double* {
-    return c < r ? U + (int64_t)c * a.ldu
-                 : (c < n ? Y2 + (int64_t)(c - r) * a.ldy : Ycur + (int64_t)(c - n) * a.ldy);
+    return c < r ? a.U + (int64_t)c * a.ldu
+                 : (c < n ? Yab + (int64_t)(c - r) * a.ldy : Ynb + (int64_t)(c - n) * a.ldy);
   };
-  // projection M = X^T Y over this warp's rows: tile jt = X columns 8jt..8jt+7
-  double m[9][2];
+  double m[9][2];  // T tile j = X columns 8j..8j+7
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j][0] = m[j][1] = 0.0;
   double ysq = 0.0;
-  const bool do_upd = pend && rn > 0 && n > 0;
+  const bool step1 = n > 0 && nwc > 0;
+  const bool step2 = n > 0 && (pcn > 0 || (MODE == 0 && pcp > 0));
   const int64_t first = ct0 + warp;
   for (int q = 0; q < R.depth - 1; ++q) {
     const int64_t tq = first + (int64_t)q * NW;
@@ -427,38 +456,60 @@ __global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int 
     }
     cp_wait_dyn(R.depth - 1);
     __syncwarp();
-    const double* X = R.base + (int64_t)cur * R.slot;
-    const double* Yt = X + n * LDT;
-    if (do_upd) {
-      double acc[8][2];
+    double* X = R.base + (int64_t)cur * R.slot;
+    double* Ya = X + r * LDT;
+    double* Yt = X + n * LDT;
+    const int64_t row = tile * LDT + g;
+    if (step1) {
+      double acc[9][2];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+      for (int j = 0; j < 9; ++j) acc[j][0] = acc[j][1] = 0.0;
       for (int kk = 0; kk < nk; ++kk) {
         const int k = 4 * kk + t;
         const double av = (k < n) ? X[k * LDT + g] : 0.0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j >= nj) break;
-          const double bv = (k < n && 8 * j + g < rn) ? W[(8 * j + g) * LDW + k] : 0.0;
+        for (int j = 0; j < (MODE == 0 ? 1 : 9); ++j) {
+          if (j >= njw) break;
+          const double bv = (k < n && 8 * j + g < nwc) ? W[(8 * j + g) * LDW + k] : 0.0;
           dmma884(acc[j][0], acc[j][1], av, bv);
         }
       }
-      const int64_t row = tile * LDT + g;
-      if (row < a.n_x) {
+      __syncwarp();  // all lanes have read X before y is overwritten in place
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j >= nj) break;
-          const int c = 8 * j + 2 * t;
-          if (c < rn) a.U[row + (int64_t)c * a.ldu] = acc[j][0];
-          if (c + 1 < rn) a.U[row + (int64_t)(c + 1) * a.ldu] = acc[j][1];
+      for (int j = 0; j < (MODE == 0 ? 1 : 9); ++j) {
+        if (j >= njw) break;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 8 * j + 2 * t + h;
+          const double v = acc[j][h];
+          if (MODE == 0) {
+            if (c < pcp) {
+              Ya[c * LDT + g] = v;
+              if (row < a.n_x) Yab[row + (int64_t)c * a.ldy] = v;
+            }
+          } else {
+            if (c < rn) {
+              if (row < a.n_x) a.U[row + (int64_t)c * a.ldu] = v;
+            } else if (c < nwc) {
+              const int s2 = c - rn;
+              const double y = Yt[s2 * LDT + g] + v;
+              Yt[s2 * LDT + g] = y;
+              if (row < a.n_x) Ynb[row + (int64_t)s2 * a.ldy] = y;
+            }
+          }
         }
       }
+      __syncwarp();
     }
-    if (pc > 0) {
+    if (step2) {
 #pragma unroll
       for (int kk = 0; kk < 2; ++kk) {
         const int rho = 4 * kk + t;
-        const double bv = (g < pc) ? Yt[g * LDT + rho] : 0.0;
+        double bv;
+        if (MODE == 0)
+          bv = g < 4 ? (g < pcn ? Yt[g * LDT + rho] : 0.0) : (g - 4 < pcp ? Ya[(g - 4) * LDT + rho] : 0.0);
+        else
+          bv = g < pcn ? Yt[g * LDT + rho] : 0.0;
 #pragma unroll
         for (int j = 0; j < 9; ++j) {
           if (j >= nm) break;
@@ -466,10 +517,10 @@ __global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int 
           dmma884(m[j][0], m[j][1], av, bv);
         }
       }
-      if ((lane >> 3) < pc) {
-        const double y = Yt[(lane >> 3) * LDT + (lane & 7)];
-        ysq += y * y;
-      }
+    }
+    if (MODE == 0 && (lane >> 3) < pcn) {
+      const double y = Yt[(lane >> 3) * LDT + (lane & 7)];
+      ysq += y * y;
     }
     __syncwarp();  // every lane is done with this slot before it is refilled
     cur = cur + 1 == R.depth ? 0 : cur + 1;
@@ -477,29 +528,33 @@ __global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int 
   }
   cp_wait<0>();
   __syncthreads();
-  // ---- CTA partial: M (n x pc, row-major), then |Y_s|^2; warps meet in
-  // shared memory and are summed in warp order
+  // ---- CTA partial (warps meet in shared memory and are summed in warp order)
+  // MODE 0: M (n x 4 row-major), G0 (4 x 4, stride 4), |Yn_s|^2 (4); MODE 1: Pm (n x 4)
   double* part = a.part + (int64_t)blockIdx.x * PSTR;
-  const int plen = n * pc + pc;
-  if (pc > 0) {
+  const int plen = MODE == 0 ? n * SF_P + 16 + SF_P : n * SF_P;
+  if (plen > 0) {
     double* wp = stage;  // NW x plen
     for (int idx = tid; idx < NW * plen; idx += SPT) wp[idx] = 0.0;
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
       if (j >= nm) break;
-      const int row = 8 * j + g;
+      const int xr = 8 * j + g;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = 2 * t + h;
-        if (row < n && c < pc) wp[warp * plen + row * pc + c] = m[j][h];
+        if (xr < n && c < SF_P) wp[warp * plen + xr * SF_P + c] = m[j][h];
+        if (MODE == 0 && xr >= r && xr < n && c >= SF_P)
+          wp[warp * plen + n * SF_P + (xr - r) * 4 + (c - SF_P)] = m[j][h];
       }
     }
-    double yw = ysq;
-    yw += __shfl_xor_sync(0xffffffffu, yw, 1);
-    yw += __shfl_xor_sync(0xffffffffu, yw, 2);
-    yw += __shfl_xor_sync(0xffffffffu, yw, 4);
-    if ((lane & 7) == 0 && (lane >> 3) < pc) wp[warp * plen + n * pc + (lane >> 3)] = yw;
+    if (MODE == 0) {
+      double yw = ysq;
+      yw += __shfl_xor_sync(0xffffffffu, yw, 1);
+      yw += __shfl_xor_sync(0xffffffffu, yw, 2);
+      yw += __shfl_xor_sync(0xffffffffu, yw, 4);
+      if ((lane & 7) == 0 && (lane >> 3) < SF_P) wp[warp * plen + n * SF_P + 16 + (lane >> 3)] = yw;
+    }
     __syncthreads();
     for (int e = tid; e < plen; e += SPT) {
       double acc = 0.0;
@@ -507,35 +562,47 @@ __global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int 
       part[e] = acc;
     }
   }
-  if (!last_cta(a.ticket + 0, flag)) return;
-  // ---- last CTA: P1 = Wp^T M (or M), pane bookkeeping
-  double* tot = red + NW * (SF_N * SF_P + SF_P) + 64;
-  reduce_parts(a.part, plen * (pc > 0), tot);
-  if (pc > 0) {
-    for (int idx = tid; idx < rn * pc; idx += SPT) {
-      const int i = idx / pc, s2 = idx % pc;
-      double acc = 0.0;
-      if (pend) {
-        for (int k = 0; k < n; ++k) acc += W[i * LDW + k] * tot[k * pc + s2];
+  if (!last_cta(a.ticket + MODE, flag)) return;
+  double* tot = red + NW * PSTR + 64;
+  reduce_parts(a.part, plen, tot);
+  if (MODE == 0) {
+    for (int idx = tid; idx < n * SF_P; idx += SPT) st->M[idx] = tot[idx];
+    if (tid < SF_P) st->yn_next[tid] = tot[n * SF_P + 16 + tid];
+    __syncthreads();
+    if (tid == 0) {
+      st->pc_new = pcn;
+      if (pcp > 0) {
+        sf_shifted_chol(a, st, tot + n * SF_P, pcp);
       } else {
-        acc = tot[i * pc + s2];
+        // nothing to close (first flush): no sf_finish will run before pass B
+        for (int s2 = 0; s2 < SF_P; ++s2) st->yn[s2] = tot[n * SF_P + 16 + s2];
+        st->rn = r;
+        st->pending = 0;
       }
-      st->C[i * SF_P + s2] = acc;
     }
-    if (tid < pc) st->yn[tid] = tot[n * pc + tid];
+    return;
   }
+  // pass B: P2 = Wp^T Pm, C = C1 + P2; the pane now has rn explicit columns
+  for (int idx = tid; idx < rn * pcn; idx += SPT) {
+    const int i = idx / pcn, s2 = idx % pcn;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc += W[i * LDW + k] * tot[k * SF_P + s2];
+    st->P2[i * SF_P + s2] = acc;
+    st->C[i * SF_P + s2] += acc;
+  }
+  const bool final_pass = f >= a.nflush;
+  if (final_pass)
+    for (int k = tid; k < rn; k += SPT) a.sigma[k] = st->sig[k];
   __syncthreads();
   if (tid == 0) {
     st->r = rn;
+    st->pcp = pcn;
     st->pending = 0;
-    st->pc = pc;
-    if (final_only) {
+    if (final_pass) {
       a.info[0] = rn;
       a.trace[a.nflush] = rn;
     }
   }
-  if (final_only)
-    for (int k = tid; k < rn; k += SPT) a.sigma[k] = st->sig[k];
 }
 
 // ------------------------------------------------------------ generation
@@ -543,20 +610,28 @@ __global__ void __launch_bounds__(SPT, 1) sf_update_project(const SFArgs a, int 
 // y_k = theta .* y_{k-1} + rowscale .* (B w2_k), k = the flush's steps.
 __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
   __shared__ double w2s[SF_CAP * SF_P];
+  __shared__ int any;
   const int start = f * a.p;
   const int pc = min(a.p, a.n_t - start);
   const int rb = a.rb_dev ? min(a.rb, *a.rb_dev) : a.rb;
-  for (int idx = threadIdx.x; idx < rb * pc; idx += ST) {
-    const int j = idx / pc, s = idx % pc;
-    const int k = a.adjoint ? (a.n_t - 1 - (start + s)) : (start + s);
-    w2s[j * SF_P + s] = a.W2[k + (int64_t)j * a.ldw2];
-  }
+  if (threadIdx.x == 0) any = 0;
   __syncthreads();
-  double* Y = a.Yg[f & 1];
+  bool nz = false;
+  for (int idx = threadIdx.x; idx < rb * SF_P; idx += ST) {
+    const int j = idx / SF_P, s = idx % SF_P;
+    const int k = a.adjoint ? (a.n_t - 1 - (start + s)) : (start + s);
+    const double v = s < pc ? a.W2[k + (int64_t)j * a.ldw2] : 0.0;
+    w2s[j * SF_P + s] = v;
+    nz |= v != 0.0;
+  }
+  if (nz) any = 1;
+  __syncthreads();
+  const int rbe = any ? rb : 0;  // a flush without a nonzero rhs time row skips B
+  double* Y = a.Yg[f % 3];
   for (int64_t i = (int64_t)blockIdx.x * ST + threadIdx.x; i < a.n_x; i += (int64_t)gridDim.x * ST) {
     double acc[SF_P] = {0.0, 0.0, 0.0, 0.0};
     int j = 0;
-    for (; j + 4 <= rb; j += 4) {
+    for (; j + 4 <= rbe; j += 4) {
       double b[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) b[u] = a.B[i + (int64_t)(j + u) * a.ldb];
@@ -565,7 +640,7 @@ __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
 #pragma unroll
         for (int s = 0; s < SF_P; ++s) acc[s] += b[u] * w2s[(j + u) * SF_P + s];
     }
-    for (; j < rb; ++j) {
+    for (; j < rbe; ++j) {
       const double b = a.B[i + (int64_t)j * a.ldb];
 #pragma unroll
       for (int s = 0; s < SF_P; ++s) acc[s] += b * w2s[j * SF_P + s];
@@ -585,170 +660,35 @@ __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
   }
 }
 
-// ------------------------------------------------------- CGS subtractions
-// mode 0: y1 = Y - U C1 (in place), P2 = U^T y1          -> C += P2
-// mode 1: y2 = y1 - U P2 (in place), G0 = y2^T y2        -> shifted Cholesky
-// Warp w owns rows 8w..8w+7 of every chunk (subtraction tile and its share of
-// the projection / Gram): one CTA barrier per chunk, for the slot refill.
-__global__ void __launch_bounds__(SPT, 1) sf_subtract(const SFArgs a, int f, int mode) {
-  extern __shared__ double smem[];
-  SFState* st = a.st;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int r = st->r;
-  const int pc = st->pc;
-  double* Ybuf = a.Yg[f & 1];
-  double* Cs = smem;                           // r x SF_P (row-major)
-  double* stage = Cs + SF_CAP * SF_P + 8;
-  const int avail = a.smem_subtract / (int)sizeof(double) - SF_CAP * SF_P - 8 - 16;
-  int* flag = reinterpret_cast<int*>(stage + avail);
-  double* red = stage;
-  const double* Csrc = mode == 0 ? st->C : st->P2;
-  for (int idx = tid; idx < r * SF_P; idx += SPT) Cs[idx] = Csrc[idx];
-  int64_t ct0, ct1;
-  cta_tiles(a.n_x, ct0, ct1);
-  const int nk = (r + 3) >> 2, nm = (r + 7) >> 3;
-  const int ncol = r + pc;  // tile: U columns, then Y
-  __syncthreads();          // Cs is settled
-  const WRing R = wring(stage, (avail / NW) & ~1, ncol);
-  auto src = [&](int c) -> const double* {
-    return c < r ? a.U + (int64_t)c * a.ldu : Ybuf + (int64_t)(c - r) * a.ldy;
-  };
-  double p2[8][2];  // mode 0: P2 tile j = U columns 8j.. ; mode 1: p2[0] = Gram
-#pragma unroll
-  for (int j = 0; j < 8; ++j) p2[j][0] = p2[j][1] = 0.0;
-  const int64_t first = ct0 + warp;
-  for (int q = 0; q < R.depth - 1; ++q) {
-    const int64_t tq = first + (int64_t)q * NW;
-    wring_issue(R, q, tq, tq < ct1, ncol, src, a.n_x);
-  }
-  int cur = 0, nxt = R.depth - 1;
-  for (int64_t tile = first; tile < ct1; tile += NW) {
-    {
-      const int64_t tq = tile + (int64_t)(R.depth - 1) * NW;
-      wring_issue(R, nxt, tq, tq < ct1, ncol, src, a.n_x);
-    }
-    cp_wait_dyn(R.depth - 1);
-    __syncwarp();
-    double* X = R.base + (int64_t)cur * R.slot;
-    double* Yt = X + r * LDT;
-    // D = U_rows C  (this tile's 8 rows, columns 0..pc)
-    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-    for (int kk = 0; kk < nk; ++kk) {
-      const int k = 4 * kk + t;
-      const double av = (k < r) ? X[k * LDT + g] : 0.0;
-      const double bv = (k < r && g < pc) ? Cs[k * SF_P + g] : 0.0;
-      if (kk & 1) dmma884(e0, e1, av, bv);
-      else dmma884(d0, d1, av, bv);
-    }
-    d0 += e0;
-    d1 += e1;
-    {
-      const int64_t grow = tile * LDT + g;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = 2 * t + h;
-        if (c < pc) {
-          const double y = Yt[c * LDT + g] - (h ? d1 : d0);
-          Yt[c * LDT + g] = y;
-          if (grow < a.n_x) Ybuf[grow + (int64_t)c * a.ldy] = y;
-        }
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const int rho = 4 * kk + t;
-      const double yv = (g < pc) ? Yt[g * LDT + rho] : 0.0;
-      if (mode == 0) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j >= nm) break;
-          const double av = (8 * j + g < r) ? X[(8 * j + g) * LDT + rho] : 0.0;
-          dmma884(p2[j][0], p2[j][1], av, yv);
-        }
-      } else {
-        dmma884(p2[0][0], p2[0][1], yv, yv);  // G[g][2t..] += y2[rho][g] y2[rho][2t..]
-      }
-    }
-    __syncwarp();  // every lane is done with this slot before it is refilled
-    cur = cur + 1 == R.depth ? 0 : cur + 1;
-    nxt = nxt + 1 == R.depth ? 0 : nxt + 1;
-  }
-  cp_wait<0>();
-  __syncthreads();
-  // ---- CTA partial (warp partials summed in warp order)
-  double* part = a.part + (int64_t)blockIdx.x * PSTR;
-  const int plen = mode == 0 ? r * pc : pc * pc;
-  double* wp = stage;
-  for (int idx = tid; idx < NW * plen; idx += SPT) wp[idx] = 0.0;
-  __syncthreads();
-  if (mode == 0) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= nm) break;
-      const int row = 8 * j + g;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = 2 * t + h;
-        if (row < r && c < pc) wp[warp * plen + row * pc + c] = p2[j][h];
-      }
-    }
-  } else {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = 2 * t + h;
-      if (g < pc && c < pc) wp[warp * plen + g * pc + c] = p2[0][h];
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < plen; e += SPT) {
-    double acc = 0.0;
-    for (int w = 0; w < NW; ++w) acc += wp[w * plen + e];
-    part[e] = acc;
-  }
-  if (!last_cta(a.ticket + 1 + mode, flag)) return;
-  double* tot = red + NW * SF_CAP * SF_P + 64;
-  reduce_parts(a.part, plen, tot);
-  if (mode == 0) {
-    for (int idx = tid; idx < r * pc; idx += SPT) {
-      const int i = idx / pc, s2 = idx % pc;
-      st->P2[i * SF_P + s2] = tot[idx];
-      st->C[i * SF_P + s2] += tot[idx];
-    }
-    return;
-  }
-  if (tid == 0) sf_shifted_chol(a, st, tot, pc);
-}
-
 // ----------------------------------------------------------- CholeskyQR passes
 // G = Q^T Q with Q = y2 Rinv; R <- chol(G) R, Rinv <- Rinv chol(G)^{-1}
-// (pivoted, drop-tolerant).  Light streaming kernel (4 columns, L2-resident).
-__global__ void __launch_bounds__(ST, 4) sf_cholqr(const SFArgs a, int f, int pass) {
+// (pivoted, drop-tolerant).  Light streaming kernel over the 4 columns of
+// flush f (usually still in L2): 4 rows per thread and step, 16 loads in flight.
+__global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pass) {
   SFState* st = a.st;
   __shared__ int flag;
   __shared__ double red[8 * 10 + 16];
   __shared__ double tot[16];
   const int tid = threadIdx.x;
-  const int pc = st->pc;
+  const int pc = st->pcp;
   const bool skip = st->drop_all != 0;
   double gacc[10] = {};
   if (!skip) {
     double Ri[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) Ri[i] = st->Rinv[i];
-    const double* Y = a.Yg[f & 1];
+    const double* Y = a.Yg[f % 3];
     const int64_t stride = (int64_t)gridDim.x * ST;
-    for (int64_t i0 = (int64_t)blockIdx.x * ST + tid; i0 < a.n_x; i0 += 2 * stride) {
-      double y[2][SF_P];
+    for (int64_t i0 = (int64_t)blockIdx.x * ST + tid; i0 < a.n_x; i0 += 4 * stride) {
+      double y[4][SF_P];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < 4; ++h) {
         const int64_t i = i0 + h * stride;
 #pragma unroll
         for (int s = 0; s < SF_P; ++s) y[h][s] = (s < pc && i < a.n_x) ? Y[i + (int64_t)s * a.ldy] : 0.0;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < 4; ++h) {
         double qv[SF_P];
 #pragma unroll
         for (int c = 0; c < SF_P; ++c) {
@@ -774,14 +714,14 @@ __global__ void __launch_bounds__(ST, 4) sf_cholqr(const SFArgs a, int f, int pa
   if (tid == 0 && !skip) sf_chol_update(st, tot, pc);
 }
 
-// The flush's small algebra (one CTA): rank-revealing fix-up of R, core
-// assembly, core SVD, zero test and _rank_cut, update matrices for the next
-// sf_update_project launch.
+// The small algebra closing flush f (one CTA): rank-revealing fix-up of R,
+// core assembly, core SVD, zero test and _rank_cut, the update matrices of the
+// next pass B and the first CGS coefficients of the flush being projected.
 __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
   extern __shared__ double sm[];
   SFState* st = a.st;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int r = st->r, pc = st->pc, n = r + pc;
+  const int r = st->r, pc = st->pcp, n = r + pc;
   const int start = f * a.p;
   double* sT = sm;                // 16: y2 -> Q~ transform
   double* sR = sm + 16;           // 16: R~ (row-major 4x4)
@@ -864,7 +804,8 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
   }
   __syncthreads();
   const int rn = iFlag[0];
-  // W' = [Uc_top; T Uc_bot] (n x rn), Vc, singular values
+  // W' = [Uc_top; T Uc_bot] (n x rn), kept in shared memory (reusing the core) for C1 / Wd
+  double* sW = sCore;  // n x rn, ld n
   for (int idx = tid; idx < n * rn; idx += ST) {
     const int i = idx % n, c = idx / n;
     double w;
@@ -874,13 +815,33 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
       w = 0.0;
       for (int q = 0; q < pc; ++q) w += sT[(i - r) * 4 + q] * Uc[r + q + c * ldc];
     }
+    sW[i + c * n] = w;
     st->Wp[i + c * SF_LDW] = w;
     st->Vc[i + c * SF_LDW] = Vc[i + c * ldc];
   }
   for (int k = tid; k < rn; k += ST) st->sig[k] = sS[k];
+  __syncthreads();
+  // the flush being projected: C1 = W'^T M, Wd = -W' C1
+  const int pcn = st->pc_new;
+  double* sC1 = Uc;  // rn x 4
+  for (int idx = tid; idx < rn * SF_P; idx += ST) {
+    const int i = idx / SF_P, s2 = idx % SF_P;
+    double acc = 0.0;
+    if (s2 < pcn)
+      for (int k = 0; k < n; ++k) acc += sW[k + i * n] * st->M[k * SF_P + s2];
+    sC1[idx] = acc;
+    st->C[idx] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * SF_P; idx += ST) {
+    const int k = idx / SF_P, s2 = idx % SF_P;
+    double acc = 0.0;
+    for (int i = 0; i < rn; ++i) acc += sW[k + i * n] * sC1[i * SF_P + s2];
+    st->Wd[idx] = -acc;
+  }
+  if (tid < SF_P) st->yn[tid] = st->yn_next[tid];
   if (tid == 0) {
     st->rn = rn;
-    st->pcp = pc;
     st->startp = start;
     st->pending = 1;
     a.trace[f] = rn;
@@ -888,8 +849,7 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
 }
 
 // ------------------------------------------------------------------ host side
-size_t sf_smem_update() { return 200 * 1024; }
-size_t sf_smem_subtract() { return 200 * 1024; }
+size_t sf_smem_pass() { return 210 * 1024; }
 size_t sf_smem_finish() {
   return (size_t)(16 + 16 + SF_N + 4 + 512 + 4 * (SF_N * SF_N + 8) + 2 * SF_N + 16) * sizeof(double);
 }
@@ -900,11 +860,11 @@ cudaError_t sf_configure() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(sf_update_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sf_smem_update());
+  cudaError_t e = cudaFuncSetAttribute(sf_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sf_smem_pass());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(sf_subtract, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sf_smem_subtract());
+  e = cudaFuncSetAttribute(sf_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sf_smem_pass());
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(sf_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sf_smem_finish());
@@ -913,44 +873,62 @@ cudaError_t sf_configure() {
   return cudaSuccess;
 }
 
-// The whole sweep: nflush x (update+project, generate, subtract, subtract,
-// CholeskyQR x 2, finish) + one final update.  Returns the number of launches.
-cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, int64_t* launches) {
+// The whole sweep: for f = 0..nflush: pass A(f) [closes f-1, projects f],
+// CholeskyQR x 2 + finish of flush f-1 (with the generation of flush f+1 next
+// to them on the aux stream), pass B(f) [update of f-1, first CGS pass of f].
+// Returns the number of launches.
+cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, const SFAux& aux,
+                                int64_t* launches) {
   cudaError_t e = sf_configure();
   if (e != cudaSuccess) return e;
   const int G = a.G;
   const int Gg = a.Ggen;
-  const size_t su = a.smem_update, ss = a.smem_subtract, sfin = sf_smem_finish();
+  const int Gc = 2 * (Gg / 8 > 0 ? Gg / 8 : 1);  // CholeskyQR passes: 2 CTAs per SM
+  const size_t sp = a.smem_pass, sfin = sf_smem_finish();
   int64_t nl = 0;
   const int dbg = a.dbg_print;
   auto show = [&](const char* what, int f) {
     if (f >= dbg) return;
-    SFState h;
+    SFState* h = new SFState;
     cudaStreamSynchronize(s);
-    cudaMemcpy(&h, a.st, sizeof(h), cudaMemcpyDeviceToHost);
-    std::fprintf(stderr, "[sf] f=%d %-8s r=%d rn=%d pc=%d pend=%d drop=%d err=%s | yn %.3e %.3e | C00 %.6e C01 %.6e P2_00 %.3e | sig %.6e %.6e | Rc %.4e %.4e %.4e %.4e\n",
-                 f, what, h.r, h.rn, h.pc, h.pending, h.drop_all, cudaGetErrorString(cudaGetLastError()),
-                 h.yn[0], h.yn[1], h.C[0], h.C[1], h.P2[0], h.sig[0], h.sig[1], h.Rc[0], h.Rc[5], h.Rc[10], h.Rc[15]);
+    cudaMemcpy(h, a.st, sizeof(*h), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "[sf] f=%d %-8s r=%d rn=%d pcp=%d pcn=%d pend=%d drop=%d err=%s | yn %.3e %.3e | C00 %.6e C01 %.6e P2_00 %.3e M00 %.6e | sig %.6e %.6e | Rc %.4e %.4e %.4e %.4e\n",
+                 f, what, h->r, h->rn, h->pcp, h->pc_new, h->pending, h->drop_all,
+                 cudaGetErrorString(cudaGetLastError()), h->yn[0], h->yn[1], h->C[0], h->C[1],
+                 h->P2[0], h->M[0], h->sig[0], h->sig[1], h->Rc[0], h->Rc[5], h->Rc[10], h->Rc[15]);
+    delete h;
   };
   sf_generate<<<Gg, ST, 0, s>>>(a, 0);
   ++nl;
-  for (int f = 0; f < nflush; ++f) {
-    sf_update_project<<<G, SPT, su, s>>>(a, f, 0);
-    show("update", f);
-    if (f + 1 < nflush) { sf_generate<<<Gg, ST, 0, s>>>(a, f + 1); ++nl; }
-    sf_subtract<<<G, SPT, ss, s>>>(a, f, 0);
-    show("sub1", f);
-    sf_subtract<<<G, SPT, ss, s>>>(a, f, 1);
-    show("sub2", f);
-    sf_cholqr<<<Gg, ST, 0, s>>>(a, f, 0);
-    sf_cholqr<<<Gg, ST, 0, s>>>(a, f, 1);
-    show("cholqr", f);
-    sf_finish<<<1, ST, sfin, s>>>(a, f);
-    show("finish", f);
-    nl += 6;
+  for (int f = 0; f <= nflush; ++f) {
+    sf_pass<0><<<G, SPT, sp, s>>>(a, f);
+    ++nl;
+    show("passA", f);
+    if (f > 0) {
+      sf_cholqr<<<Gc, ST, 0, s>>>(a, f - 1, 0);
+      sf_cholqr<<<Gc, ST, 0, s>>>(a, f - 1, 1);
+      nl += 2;
+    }
+    // flush f+1's columns (buffer (f+1) % 3, last read by pass B(f-1)) are
+    // generated on the aux stream, next to the single-CTA sf_finish
+    const bool gen = f + 1 < nflush;
+    if (gen) {
+      if ((e = cudaEventRecord(aux.ready, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(aux.stream, aux.ready, 0)) != cudaSuccess) return e;
+      sf_generate<<<Gg, ST, 0, aux.stream>>>(a, f + 1);
+      ++nl;
+      if ((e = cudaEventRecord(aux.done, aux.stream)) != cudaSuccess) return e;
+    }
+    if (f > 0) {
+      sf_finish<<<1, ST, sfin, s>>>(a, f - 1);
+      ++nl;
+      show("finish", f);
+    }
+    sf_pass<1><<<G, SPT, sp, s>>>(a, f);
+    ++nl;
+    show("passB", f);
+    if (gen && (e = cudaStreamWaitEvent(s, aux.done, 0)) != cudaSuccess) return e;
   }
-  sf_update_project<<<G, SPT, su, s>>>(a, nflush, 1);
-  ++nl;
   if (launches) *launches += nl;
   return cudaGetLastError();
 }
