@@ -90,6 +90,11 @@ __device__ __forceinline__ void cp_wait_dyn(int n) {
   }
 }
 constexpr int LDT = 8;        // rows per tile = leading dimension of a staged column
+// Row i of staged column c sits at c * LDT + (i ^ swz(c)): flipping bit 2 of
+// the row for every other column pair makes both fragment access patterns
+// (rows as the M/N index, rows as the K index) two wavefronts per 8-byte warp
+// load — the minimum — without padding the 8-row tiles.
+__device__ __forceinline__ int swz(int c) { return (c & 2) << 1; }
 constexpr int MAXDEPTH = 15;  // (cp_wait_dyn covers depth - 1 <= 14)
 
 struct WRing {
@@ -120,7 +125,7 @@ __device__ __forceinline__ void wring_issue(const WRing& R, int sl, int64_t tile
       const int c = q >> 2, j = q & 3;
       const int64_t row = r0 + 2 * j;
       const bool ok = row < n_x;
-      cp16(dst + c * LDT + 2 * j, src(c) + (ok ? row : 0), ok);
+      cp16(dst + c * LDT + 2 * (j ^ (c & 2)), src(c) + (ok ? row : 0), ok);
     }
   }
   cp_commit();
@@ -393,16 +398,19 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
   int* flag = reinterpret_cast<int*>(stage + avail);
   double* red = stage;                        // reused after the main loop
 
-  if (MODE == 0) {
-    for (int idx = tid; idx < n * pcp; idx += SPT) {
-      const int k = idx % n, c = idx / n;
-      W[c * LDW + k] = k < r ? -st->P2[k * SF_P + c] : (k - r == c ? 1.0 : 0.0);
+  {
+    const int nk4 = 4 * ((n + 3) >> 2), nc8 = 8 * ((nwc + 7) >> 3);
+    for (int idx = tid; idx < nk4 * nc8; idx += SPT) {
+      const int k = idx % nk4, c = idx / nk4;
+      double v = 0.0;
+      if (k < n && c < nwc) {
+        if (MODE == 0) v = k < r ? -st->P2[k * SF_P + c] : (k - r == c ? 1.0 : 0.0);
+        else v = c < rn ? st->Wp[k + c * SF_LDW] : st->Wd[k * SF_P + (c - rn)];
+      }
+      W[c * LDW + k] = v;
     }
-  } else {
-    for (int idx = tid; idx < n * nwc; idx += SPT) {
-      const int k = idx % n, c = idx / n;
-      W[c * LDW + k] = c < rn ? st->Wp[k + c * SF_LDW] : st->Wd[k * SF_P + (c - rn)];
-    }
+  }
+  if (MODE == 1) {
     if (st->pending) {
       // time rows of this CTA: V' = [V, E] Vc   (in place, via shared memory)
       const int64_t tper = ((int64_t)a.n_t + gridDim.x - 1) / gridDim.x;
@@ -456,46 +464,44 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
     }
     cp_wait_dyn(R.depth - 1);
     __syncwarp();
-    double* X = R.base + (int64_t)cur * R.slot;
-    double* Ya = X + r * LDT;
-    double* Yt = X + n * LDT;
-    const int64_t row = tile * LDT + g;
+    double* X = R.base + (int64_t)cur * R.slot;   // element (row i, staged column c) at X[c * LDT + (i ^ swz(c))]
+    const int64_t row2 = tile * LDT + 2 * t;     // the lane's row pair of step 1
     if (step1) {
+      // transposed: D = W^T X^T, so the lane holds rows 2t, 2t+1 of output column 8j+g
       double acc[9][2];
 #pragma unroll
       for (int j = 0; j < 9; ++j) acc[j][0] = acc[j][1] = 0.0;
       for (int kk = 0; kk < nk; ++kk) {
         const int k = 4 * kk + t;
-        const double av = (k < n) ? X[k * LDT + g] : 0.0;
+        const double xv = (k < n) ? X[k * LDT + (g ^ swz(k))] : 0.0;
 #pragma unroll
         for (int j = 0; j < (MODE == 0 ? 1 : 9); ++j) {
           if (j >= njw) break;
-          const double bv = (k < n && 8 * j + g < nwc) ? W[(8 * j + g) * LDW + k] : 0.0;
-          dmma884(acc[j][0], acc[j][1], av, bv);
+          dmma884(acc[j][0], acc[j][1], W[(8 * j + g) * LDW + k], xv);
         }
       }
       __syncwarp();  // all lanes have read X before y is overwritten in place
 #pragma unroll
       for (int j = 0; j < (MODE == 0 ? 1 : 9); ++j) {
         if (j >= njw) break;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = 8 * j + 2 * t + h;
-          const double v = acc[j][h];
-          if (MODE == 0) {
-            if (c < pcp) {
-              Ya[c * LDT + g] = v;
-              if (row < a.n_x) Yab[row + (int64_t)c * a.ldy] = v;
-            }
-          } else {
-            if (c < rn) {
-              if (row < a.n_x) a.U[row + (int64_t)c * a.ldu] = v;
-            } else if (c < nwc) {
-              const int s2 = c - rn;
-              const double y = Yt[s2 * LDT + g] + v;
-              Yt[s2 * LDT + g] = y;
-              if (row < a.n_x) Ynb[row + (int64_t)s2 * a.ldy] = y;
-            }
+        const int c = 8 * j + g;
+        double2 v = make_double2(acc[j][0], acc[j][1]);
+        if (MODE == 0) {
+          if (c < pcp) {
+            *reinterpret_cast<double2*>(X + (r + c) * LDT + ((2 * t) ^ swz(r + c))) = v;
+            if (row2 < a.n_x) *reinterpret_cast<double2*>(Yab + row2 + (int64_t)c * a.ldy) = v;
+          }
+        } else {
+          if (c < rn) {
+            if (row2 < a.n_x) *reinterpret_cast<double2*>(a.U + row2 + (int64_t)c * a.ldu) = v;
+          } else if (c < nwc) {
+            const int s2 = c - rn;
+            double2* ys = reinterpret_cast<double2*>(X + (n + s2) * LDT + ((2 * t) ^ swz(n + s2)));
+            const double2 y0 = *ys;
+            v.x += y0.x;
+            v.y += y0.y;
+            *ys = v;
+            if (row2 < a.n_x) *reinterpret_cast<double2*>(Ynb + row2 + (int64_t)s2 * a.ldy) = v;
           }
         }
       }
@@ -506,20 +512,23 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
       for (int kk = 0; kk < 2; ++kk) {
         const int rho = 4 * kk + t;
         double bv;
-        if (MODE == 0)
-          bv = g < 4 ? (g < pcn ? Yt[g * LDT + rho] : 0.0) : (g - 4 < pcp ? Ya[(g - 4) * LDT + rho] : 0.0);
-        else
-          bv = g < pcn ? Yt[g * LDT + rho] : 0.0;
+        {
+          // N index g: Yn column g (g < 4), pass A also y2 column g - 4
+          const int cy = (MODE == 0 && g >= 4) ? r + g - 4 : n + g;
+          const bool ok = (MODE == 0 && g >= 4) ? (g - 4 < pcp) : (g < pcn);
+          bv = ok ? X[cy * LDT + (rho ^ swz(cy))] : 0.0;
+        }
 #pragma unroll
         for (int j = 0; j < 9; ++j) {
           if (j >= nm) break;
-          const double av = (8 * j + g < n) ? X[(8 * j + g) * LDT + rho] : 0.0;
+          const int cx = 8 * j + g;
+          const double av = (cx < n) ? X[cx * LDT + (rho ^ swz(cx))] : 0.0;
           dmma884(m[j][0], m[j][1], av, bv);
         }
       }
     }
     if (MODE == 0 && (lane >> 3) < pcn) {
-      const double y = Yt[(lane >> 3) * LDT + (lane & 7)];
+      const double y = X[(n + (lane >> 3)) * LDT + (lane & 7)];
       ysq += y * y;
     }
     __syncwarp();  // every lane is done with this slot before it is refilled
