@@ -378,9 +378,139 @@ static __device__ __noinline__ void sf_chol_update(SFState* st, const double* to
 //   last CTA: P2 = Wp^T Pm, C = C1 + P2, pane bookkeeping (r <- rn, pcp <- pcn).
 // Warp w owns tiles w, w+16, ... of the CTA's 8-row tile range: its step-1
 // output tile and its share of the projections need no CTA barrier.
+// Runtime sizes and pointers of one pass (uniform over the CTA).
+struct PassRt {
+  int r, pcp, n, pcn, rn, nwc, ncol, per_warp;
+  int64_t ct0, ct1;
+  double *Yab, *Ynb, *W, *ring;
+  const unsigned long long* colp;  // shared: base address of every staged column
+};
+
+// The tile loop of a pass for NT 8-column fragment tiles (compile time: the
+// fragment loops are branch free, every shared-memory operand is one load at
+// an immediate offset from a per-lane base).  See sf_pass for the mathematics.
+template <int MODE, int NT>
+__device__ __forceinline__ void pass_loop(const SFArgs& a, const PassRt& P, double (&m9)[9][2],
+                                          double& ysq_out) {
+  constexpr int NK = NT == 9 ? 17 : 2 * NT;   // k groups of 4 (rows of W are zero past n)
+  constexpr int NJ = MODE == 0 ? 1 : NT;      // column tiles of the step-1 product
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int r = P.r, n = P.n, pcp = P.pcp, pcn = P.pcn, rn = P.rn, nwc = P.nwc, ncol = P.ncol;
+  const int slot = (ncol > 0 ? ncol : 1) * LDT;
+  int depth = P.per_warp / slot;
+  depth = depth < 2 ? 2 : (depth > MAXDEPTH ? MAXDEPTH : depth);
+  double* base = P.ring + (int64_t)warp * P.per_warp;
+  // cp.async: the lane copies row pair jp of columns cg, cg + 8, ...
+  const int jp = lane & 3, cg = lane >> 2;
+  const int dlane = cg * LDT + 2 * (jp ^ (cg & 2));
+  const int nci = (ncol - cg + 7) >> 3;
+  auto issue = [&](int sl, int64_t tile, bool valid) {
+    if (valid) {
+      const int64_t row = tile * LDT + 2 * jp;
+      const bool ok = row < a.n_x;
+      const int64_t roff = ok ? row : 0;
+      double* dst = base + sl * slot + dlane;
+      for (int i = 0; i < nci; ++i)
+        cp16(dst + i * 8 * LDT, reinterpret_cast<const double*>(P.colp[cg + 8 * i]) + roff, ok);
+    }
+    cp_commit();
+  };
+  // step 1 (transposed: D = W^T X^T): X[k][row g], k = 4kk + t; W[k][col 8j + g]
+  const int xo1 = t * LDT + (g ^ ((t & 2) << 1));
+  const double* Wl = P.W + g * LDW + t;
+  // step 2: A = X^T[col 8j + g][row 4kk + t], B = [Yn | y2][row 4kk + t][col g]
+  const int sg = (g & 2) << 1;
+  const int ao0 = g * LDT + (t ^ sg), ao1 = g * LDT + ((4 + t) ^ sg);
+  const int cy = (MODE == 0 && g >= 4) ? r + g - 4 : n + g;
+  const bool bok = (MODE == 0 && g >= 4) ? (g - 4 < pcp) : (g < pcn);
+  const int bo0 = cy * LDT + (t ^ swz(cy)), bo1 = cy * LDT + ((4 + t) ^ swz(cy));
+  const bool step1 = n > 0 && nwc > 0;
+  const bool step2 = n > 0 && (pcn > 0 || (MODE == 0 && pcp > 0));
+  double m[NT][2];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) m[j][0] = m[j][1] = 0.0;
+  double ysq = 0.0;
+  const int64_t first = P.ct0 + warp;
+  for (int q = 0; q < depth - 1; ++q) {
+    const int64_t tq = first + (int64_t)q * NW;
+    issue(q, tq, tq < P.ct1);
+  }
+  int cur = 0, nxt = depth - 1;
+  for (int64_t tile = first; tile < P.ct1; tile += NW) {
+    {
+      const int64_t tq = tile + (int64_t)(depth - 1) * NW;
+      issue(nxt, tq, tq < P.ct1);
+    }
+    cp_wait_dyn(depth - 1);
+    __syncwarp();
+    double* X = base + cur * slot;   // element (row i, staged column c) at X[c * LDT + (i ^ swz(c))]
+    const int64_t row2 = tile * LDT + 2 * t;     // the lane's row pair of step 1
+    const bool rok = row2 < a.n_x;
+    if (step1) {
+      double acc[NJ][2];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NK; ++kk) {
+        const double xv = X[kk * 4 * LDT + xo1];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma884(acc[j][0], acc[j][1], Wl[j * 8 * LDW + 4 * kk], xv);
+      }
+      __syncwarp();  // all lanes have read X before y is overwritten in place
+      if (MODE == 0) {
+        if (g < pcp) {
+          const double2 v = make_double2(acc[0][0], acc[0][1]);
+          *reinterpret_cast<double2*>(X + (r + g) * LDT + ((2 * t) ^ swz(r + g))) = v;
+          if (rok) *reinterpret_cast<double2*>(P.Yab + row2 + (int64_t)g * a.ldy) = v;
+        }
+      } else {
+        double* pu = a.U + row2 + (int64_t)g * a.ldu;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int c = 8 * j + g;
+          double2 v = make_double2(acc[j][0], acc[j][1]);
+          if (c < rn) {
+            if (rok) *reinterpret_cast<double2*>(pu) = v;
+          } else if (c < nwc) {
+            const int s2 = c - rn;
+            double2* ys = reinterpret_cast<double2*>(X + (n + s2) * LDT + ((2 * t) ^ swz(n + s2)));
+            const double2 y0 = *ys;
+            v.x += y0.x;
+            v.y += y0.y;
+            *ys = v;
+            if (rok) *reinterpret_cast<double2*>(P.Ynb + row2 + (int64_t)s2 * a.ldy) = v;
+          }
+          pu += 8 * a.ldu;
+        }
+      }
+      __syncwarp();
+    }
+    if (step2) {
+      const double b0 = bok ? X[bo0] : 0.0, b1 = bok ? X[bo1] : 0.0;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma884(m[j][0], m[j][1], X[j * 8 * LDT + ao0], b0);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma884(m[j][0], m[j][1], X[j * 8 * LDT + ao1], b1);
+    }
+    if (MODE == 0 && (lane >> 3) < pcn) {
+      const double y = X[(n + (lane >> 3)) * LDT + (lane & 7)];
+      ysq += y * y;
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    cur = cur + 1 == depth ? 0 : cur + 1;
+    nxt = nxt + 1 == depth ? 0 : nxt + 1;
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int j = 0; j < NT; ++j) { m9[j][0] = m[j][0]; m9[j][1] = m[j][1]; }
+  ysq_out = ysq;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long colp[SF_N + SF_P + 8];
   SFState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -398,8 +528,11 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
   int* flag = reinterpret_cast<int*>(stage + avail);
   double* red = stage;                        // reused after the main loop
 
+  // NT: 8-column tiles of the widest fragment loop (X columns or W columns);
+  // W is zero padded to 8 NT columns and min(8 NT, 68) rows
+  const int NT = max(1, max((n + 7) >> 3, (nwc + 7) >> 3));
   {
-    const int nk4 = 4 * ((n + 3) >> 2), nc8 = 8 * ((nwc + 7) >> 3);
+    const int nk4 = min(8 * NT, SF_N), nc8 = 8 * NT;
     for (int idx = tid; idx < nk4 * nc8; idx += SPT) {
       const int k = idx % nk4, c = idx / nk4;
       double v = 0.0;
@@ -435,107 +568,36 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
     }
   }
 
-  int64_t ct0, ct1;
-  cta_tiles(a.n_x, ct0, ct1);
-  const int nk = (n + 3) >> 2, njw = (nwc + 7) >> 3, nm = (n + 7) >> 3;
+  const int nm = (n + 7) >> 3;
   const int ncol = n + pcn;  // tile: X columns, then Yn
-  __syncthreads();           // W and the V-update scratch are settled
-  const WRing R = wring(stage, (avail / NW) & ~1, ncol);
-  auto src = [&](int c) -> const double* {
-    return c < r ? a.U + (int64_t)c * a.ldu
-                 : (c < n ? Yab + (int64_t)(c - r) * a.ldy : Ynb + (int64_t)(c - n) * a.ldy);
-  };
+  for (int c = tid; c < ncol; c += SPT)
+    colp[c] = reinterpret_cast<unsigned long long>(
+        c < r ? a.U + (int64_t)c * a.ldu
+              : (c < n ? Yab + (int64_t)(c - r) * a.ldy : Ynb + (int64_t)(c - n) * a.ldy));
+  __syncthreads();           // the V-update scratch is free again
+  // columns past ncol are read by the padded (branch-free) fragment loops and
+  // multiplied by zero rows of W: they must hold finite numbers
+  for (int idx = tid; idx < avail; idx += SPT) stage[idx] = 0.0;
+  __syncthreads();
+  PassRt P;
+  P.r = r; P.pcp = pcp; P.n = n; P.pcn = pcn; P.rn = rn; P.nwc = nwc; P.ncol = ncol;
+  cta_tiles(a.n_x, P.ct0, P.ct1);
+  P.Yab = Yab; P.Ynb = Ynb; P.W = W; P.ring = stage; P.per_warp = ((avail - 128) / NW) & ~1;  /* headroom: padded fragment loops read up to 7 columns past a slot */ P.colp = colp;
   double m[9][2];  // T tile j = X columns 8j..8j+7
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j][0] = m[j][1] = 0.0;
   double ysq = 0.0;
-  const bool step1 = n > 0 && nwc > 0;
-  const bool step2 = n > 0 && (pcn > 0 || (MODE == 0 && pcp > 0));
-  const int64_t first = ct0 + warp;
-  for (int q = 0; q < R.depth - 1; ++q) {
-    const int64_t tq = first + (int64_t)q * NW;
-    wring_issue(R, q, tq, tq < ct1, ncol, src, a.n_x);
+  switch (NT) {
+    case 1: pass_loop<MODE, 1>(a, P, m, ysq); break;
+    case 2: pass_loop<MODE, 2>(a, P, m, ysq); break;
+    case 3: pass_loop<MODE, 3>(a, P, m, ysq); break;
+    case 4: pass_loop<MODE, 4>(a, P, m, ysq); break;
+    case 5: pass_loop<MODE, 5>(a, P, m, ysq); break;
+    case 6: pass_loop<MODE, 6>(a, P, m, ysq); break;
+    case 7: pass_loop<MODE, 7>(a, P, m, ysq); break;
+    case 8: pass_loop<MODE, 8>(a, P, m, ysq); break;
+    default: pass_loop<MODE, 9>(a, P, m, ysq); break;
   }
-  int cur = 0, nxt = R.depth - 1;
-  for (int64_t tile = first; tile < ct1; tile += NW) {
-    {
-      const int64_t tq = tile + (int64_t)(R.depth - 1) * NW;
-      wring_issue(R, nxt, tq, tq < ct1, ncol, src, a.n_x);
-    }
-    cp_wait_dyn(R.depth - 1);
-    __syncwarp();
-    double* X = R.base + (int64_t)cur * R.slot;   // element (row i, staged column c) at X[c * LDT + (i ^ swz(c))]
-    const int64_t row2 = tile * LDT + 2 * t;     // the lane's row pair of step 1
-    if (step1) {
-      // transposed: D = W^T X^T, so the lane holds rows 2t, 2t+1 of output column 8j+g
-      double acc[9][2];
-#pragma unroll
-      for (int j = 0; j < 9; ++j) acc[j][0] = acc[j][1] = 0.0;
-      for (int kk = 0; kk < nk; ++kk) {
-        const int k = 4 * kk + t;
-        const double xv = (k < n) ? X[k * LDT + (g ^ swz(k))] : 0.0;
-#pragma unroll
-        for (int j = 0; j < (MODE == 0 ? 1 : 9); ++j) {
-          if (j >= njw) break;
-          dmma884(acc[j][0], acc[j][1], W[(8 * j + g) * LDW + k], xv);
-        }
-      }
-      __syncwarp();  // all lanes have read X before y is overwritten in place
-#pragma unroll
-      for (int j = 0; j < (MODE == 0 ? 1 : 9); ++j) {
-        if (j >= njw) break;
-        const int c = 8 * j + g;
-        double2 v = make_double2(acc[j][0], acc[j][1]);
-        if (MODE == 0) {
-          if (c < pcp) {
-            *reinterpret_cast<double2*>(X + (r + c) * LDT + ((2 * t) ^ swz(r + c))) = v;
-            if (row2 < a.n_x) *reinterpret_cast<double2*>(Yab + row2 + (int64_t)c * a.ldy) = v;
-          }
-        } else {
-          if (c < rn) {
-            if (row2 < a.n_x) *reinterpret_cast<double2*>(a.U + row2 + (int64_t)c * a.ldu) = v;
-          } else if (c < nwc) {
-            const int s2 = c - rn;
-            double2* ys = reinterpret_cast<double2*>(X + (n + s2) * LDT + ((2 * t) ^ swz(n + s2)));
-            const double2 y0 = *ys;
-            v.x += y0.x;
-            v.y += y0.y;
-            *ys = v;
-            if (row2 < a.n_x) *reinterpret_cast<double2*>(Ynb + row2 + (int64_t)s2 * a.ldy) = v;
-          }
-        }
-      }
-      __syncwarp();
-    }
-    if (step2) {
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        const int rho = 4 * kk + t;
-        double bv;
-        {
-          // N index g: Yn column g (g < 4), pass A also y2 column g - 4
-          const int cy = (MODE == 0 && g >= 4) ? r + g - 4 : n + g;
-          const bool ok = (MODE == 0 && g >= 4) ? (g - 4 < pcp) : (g < pcn);
-          bv = ok ? X[cy * LDT + (rho ^ swz(cy))] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < 9; ++j) {
-          if (j >= nm) break;
-          const int cx = 8 * j + g;
-          const double av = (cx < n) ? X[cx * LDT + (rho ^ swz(cx))] : 0.0;
-          dmma884(m[j][0], m[j][1], av, bv);
-        }
-      }
-    }
-    if (MODE == 0 && (lane >> 3) < pcn) {
-      const double y = X[(n + (lane >> 3)) * LDT + (lane & 7)];
-      ysq += y * y;
-    }
-    __syncwarp();  // every lane is done with this slot before it is refilled
-    cur = cur + 1 == R.depth ? 0 : cur + 1;
-    nxt = nxt + 1 == R.depth ? 0 : nxt + 1;
-  }
-  cp_wait<0>();
   __syncthreads();
   // ---- CTA partial (warps meet in shared memory and are summed in warp order)
   // MODE 0: M (n x 4 row-major), G0 (4 x 4, stride 4), |Yn_s|^2 (4); MODE 1: Pm (n x 4)
