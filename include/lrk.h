@@ -248,6 +248,24 @@ int lrk_prior_diag(lrk_ctx* ctx, double delta, double gamma, int power, double* 
  * through a per-shard table, one shared barrier) emulated as nshard groups of
  * ONE cooperative launch on this device.  Results are bit-identical to the
  * unsharded sweep when the CTA count divides evenly; used by the tests. */
+/* n_x sharding across GPUs (the reference's time loop
+ * forward.py:179-186 and flush truncation lowrank.py:133-135, sharded by
+ * rows).  One process per GPU; every rank installs the same operator and
+ * observation, then
+ *   lrk_shard_setup(ctx, rank, world, handle)   -> 64-byte IPC handle of this
+ *       rank's peer-shared arena (exchange slots + the two sweep panes);
+ *   all-gather the handles (torch.distributed / MPI / a file);
+ *   lrk_shard_connect(ctx, handles)             -> maps the peers' arenas.
+ * Afterwards lrk_hessian_apply_ic runs its two sweeps on this rank's row slab
+ * (streaming-flush form): every pass ends in a small rank total that the last
+ * CTA stores straight into all peers' exchange slots over NVLink, followed by
+ * a system-scope release flag; the rank's slab of the final pane is pushed
+ * into the peers' panes the same way.  Inputs and outputs stay replicated
+ * n_x vectors, all ranks return identical results.  world <= 8. */
+int lrk_shard_setup(lrk_ctx* ctx, int rank, int world, void* handle_out);
+int lrk_shard_connect(lrk_ctx* ctx, const void* handles);
+/* Single-device emulation of the same sharded sweeps (tests): nshard row
+ * slabs driven by one process, launched pass by pass. */
 int lrk_set_emulated_shards(lrk_ctx* ctx, int nshard);
 int lrk_profile_enable(lrk_ctx* ctx, int enable);
 int lrk_profile_read(lrk_ctx* ctx, double* sweep_ms, int64_t* sweep_launches,

@@ -16,6 +16,7 @@
 #include "../../include/lrk.h"
 #include "lrk_device.cuh"
 #include "lrk_kernels.h"
+#include "lrk_sflush.h"
 #include "lrk_misc.h"
 
 using namespace lrk;
@@ -24,6 +25,17 @@ namespace {
 struct Buf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool ext = false;  // lives in the peer-shared arena: never freed or regrown here
+};
+// n_x sharding across processes (one per GPU): this rank's shard index, the
+// peer-mapped arenas (exchange buffer + the two sweep panes) of all ranks.
+struct Dist {
+  int rank = 0, world = 1;
+  char* arena = nullptr;
+  size_t bytes = 0, off_f = 0, off_b = 0;
+  int64_t pane_doubles = 0;
+  char* peer[SF_XMAXR] = {};
+  bool connected = false;
 };
 }  // namespace
 
@@ -47,6 +59,8 @@ struct lrk_ctx {
   double* dInvLam = nullptr;  // n_x: 1/lambda (steady Poisson solve)
   double* dLam = nullptr;     // n_x: lambda (config prior (delta + gamma lambda)^{-1})
   int emu_shards = 1;         // sweeps as G emulated n_x shards (one launch, tests)
+  Dist dist;                  // n_x sharding across processes (lrk_shard_setup)
+  unsigned long long xseq = 0;  // exchange sequence number of the sharded streaming sweep
   int rich_it = 0;            // physical step solves: Richardson sweeps (0 unknown, -1 GMRES)
   double rich_q = 1.0;        // measured contraction of I - P^{-1} S
   // observation
@@ -69,7 +83,10 @@ struct lrk_ctx {
     if (aux.ready) cudaEventDestroy(aux.ready);
     if (aux.done) cudaEventDestroy(aux.done);
     if (aux.stream) cudaStreamDestroy(aux.stream);
-    for (auto& kv : ws) cudaFree(kv.second.p);
+    for (auto& kv : ws) if (!kv.second.ext) cudaFree(kv.second.p);
+    for (int q = 0; q < SF_XMAXR; ++q)
+      if (dist.peer[q] && q != dist.rank) cudaIpcCloseMemHandle(dist.peer[q]);
+    cudaFree(dist.arena);
     cudaFree(dS); cudaFree(dTheta); cudaFree(dThetaM); cudaFree(dE0); cudaFree(dInvLam);
     cudaFree(dLam); cudaFree(dSsq);
     cudaFree(dList); cudaFree(dS1T); cudaFree(dS2); cudaFree(dS1); cudaFree(dS2T);
@@ -109,6 +126,10 @@ T* wsp(lrk_ctx* c, const std::string& name, size_t count, bool zero = false) {
   Buf& b = c->ws[name];
   const size_t need = count * sizeof(T) + 256;
   if (b.bytes < need) {
+    if (b.ext) {
+      c->err = "peer-shared workspace " + name + " is too small for this call";
+      return nullptr;
+    }
     if (b.p) {
       cudaDeviceSynchronize();
       cudaFree(b.p);
@@ -368,42 +389,91 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
   // Large n_x (rows not resident in shared memory): the streaming-flush form
   // (lrk_sflush.cu) — one kernel per row pass instead of the persistent
   // kernel's global-row phases.  LRK_SFLUSH=0 forces the persistent kernel,
-  // LRK_SFLUSH=1 forces the streaming form (tests).
+  // LRK_SFLUSH=1 forces the streaming form (tests).  n_x shards (one per
+  // process after lrk_shard_setup, or emulated on this device) always take
+  // the streaming form.
   {
     const char* sfe = std::getenv("LRK_SFLUSH");
     const int force = sfe ? std::atoi(sfe) : -1;
-    const bool fits = p <= SF_P && ucap <= SF_CAP && rb <= SF_CAP && (nx % 2) == 0 && G == 1 &&
+    const bool dist = c->dist.world > 1;
+    const int S = dist ? c->dist.world : std::max(1, std::min(c->emu_shards, (int)SF_XMAXR));
+    const bool fits = p <= SF_P && ucap <= SF_CAP && rb <= SF_CAP && (nx % 2) == 0 &&
                       !std::getenv("LRK_DUMP_CORES") && !std::getenv("LRK_DEBUG");
-    const bool want = force == 1 || (force != 0 && !a.resident);
+    const bool want = dist || force == 1 || (force != 0 && !a.resident);
+    if (dist && !fits)
+      return fail(c, LRK_ERR_UNSUPPORTED,
+                  "sharded sweeps need compress_every <= 4, r_max <= 64 and an even n_x");
+    if (dist && !c->dist.connected)
+      return fail(c, LRK_ERR_CONFIG, "lrk_shard_setup without lrk_shard_connect");
     if (fits && want) {
-      WS(SFState, sfst, tag + "sfst", 1);
-      WS(unsigned, tick, "sf_tick", 8);
+      const int nlocal = dist ? 1 : S;
+      // contiguous row slabs in multiples of 8 rows
+      const int64_t per = ((nx / 8 + S - 1) / S) * 8 + (nx < 8 ? 8 : 0);
+      if (S > 1 && per * (int64_t)(S - 1) >= nx)
+        return fail(c, LRK_ERR_UNSUPPORTED, "too few rows for this many n_x shards");
+      WS(SFState, sfst, tag + "sfst", nlocal);
+      WS(unsigned, tick, "sf_tick", 8 * nlocal);
       const int Gs = c->num_sms;
-      WS(double, sfpart, "sf_part", (int64_t)(8 * Gs) * sf_part_stride());
-      CK(cudaMemsetAsync(sfst, 0, sizeof(SFState), s));
-      CK(cudaMemsetAsync(yprev, 0, nx * sizeof(double), s));
-      SFArgs sa{};
-      sa.n_x = nx; sa.n_t = nt; sa.p = p; sa.cap = ucap; sa.adjoint = adjoint; sa.r_max = r_max;
-      sa.nflush = nflush; sa.eps0 = eps0; sa.ftz = a.ftz;
-      sa.U = U0; sa.ldu = ld; sa.V = V0; sa.ldv = nt;
+      WS(double, sfpart, "sf_part", (int64_t)nlocal * (8 * Gs) * sf_part_stride());
       WS(double, ybuf3, "sw_ybuf3", ld * (int64_t)p);
-      sa.Yg[0] = ybuf; sa.Yg[1] = qbuf; sa.Yg[2] = ybuf3; sa.ldy = ld;
-      sa.n_x_glob = nx;
-      sa.yprev = yprev; sa.theta = c->dTheta; sa.rowscale = c->dThetaM;
-      sa.B = B; sa.ldb = ldb; sa.rb = rb; sa.rb_dev = rb_dev; sa.W2 = W2; sa.ldw2 = ldw2;
-      sa.part = sfpart; sa.ticket = tick; sa.st = sfst;
-      sa.trace = trace; sa.info = info; sa.sigma = sig;
-      sa.G = Gs; sa.Ggen = 8 * c->num_sms;
-      sa.dbg_print = std::getenv("LRK_SF_DEBUG") ? std::atoi(std::getenv("LRK_SF_DEBUG")) : 0;
-      sa.smem_pass = (int)sf_smem_pass();
+      WS(double, Vg, tag + "sfVsh", (int64_t)std::max(nlocal - 1, 1) * nt * ucap);
+      WS(double, sg, tag + "sfsigsh", (int64_t)nlocal * NMAX);
+      WS(int, ig, tag + "sfinfosh", 8 * nlocal);
+      WS(int, tg, tag + "sftracesh", (int64_t)nlocal * (nflush + 1));
+      SFXBuf* xb = nullptr;
+      if (S > 1 && !dist) {
+        WS(SFXBuf, xbe, "sf_xbuf", S);
+        xb = xbe;
+      }
+      CK(cudaMemsetAsync(sfst, 0, sizeof(SFState) * nlocal, s));
+      CK(cudaMemsetAsync(yprev, 0, nx * sizeof(double), s));
+      if (nlocal > 1) CK(cudaMemsetAsync(ig, 0, 8 * nlocal * sizeof(int), s));
       if (!c->aux.stream) {
         CK(cudaStreamCreateWithFlags(&c->aux.stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->aux.ready, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->aux.done, cudaEventDisableTiming));
       }
+      std::vector<SFArgs> sh(nlocal);
+      int64_t my_x0 = 0, my_rows = nx;
+      for (int l = 0; l < nlocal; ++l) {
+        const int g = dist ? c->dist.rank : l;
+        const int64_t x0 = S > 1 ? std::min(nx, (int64_t)g * per) : 0;
+        const int64_t x1 = S > 1 ? std::min(nx, x0 + per) : nx;
+        if (l == 0) { my_x0 = x0; my_rows = x1 - x0; }
+        SFArgs& sa = sh[l];
+        sa = SFArgs{};
+        sa.n_x = x1 - x0; sa.n_x_glob = nx; sa.nshard = S; sa.shard = g;
+        for (int q = 0; q < S && S > 1; ++q)
+          sa.xpeer[q] = dist ? reinterpret_cast<SFXBuf*>(c->dist.peer[q]) : xb + q;
+        sa.n_t = nt; sa.p = p; sa.cap = ucap; sa.adjoint = adjoint; sa.r_max = r_max;
+        sa.nflush = nflush; sa.eps0 = eps0; sa.ftz = a.ftz;
+        sa.U = U0 + x0; sa.ldu = ld;
+        sa.V = l == 0 ? V0 : Vg + (int64_t)(l - 1) * nt * ucap; sa.ldv = nt;
+        sa.Yg[0] = ybuf + x0; sa.Yg[1] = qbuf + x0; sa.Yg[2] = ybuf3 + x0; sa.ldy = ld;
+        sa.yprev = yprev + x0; sa.theta = c->dTheta + x0;
+        sa.rowscale = c->dThetaM ? c->dThetaM + x0 : nullptr;
+        sa.B = B + x0; sa.ldb = ldb; sa.rb = rb; sa.rb_dev = rb_dev; sa.W2 = W2; sa.ldw2 = ldw2;
+        sa.part = sfpart + (int64_t)l * (8 * Gs) * sf_part_stride();
+        sa.ticket = tick + 8 * l; sa.st = sfst + l;
+        sa.trace = l == 0 ? trace : tg + (int64_t)l * (nflush + 1);
+        sa.info = l == 0 ? info : ig + 8 * l;
+        sa.sigma = l == 0 ? sig : sg + (int64_t)l * NMAX;
+        sa.G = Gs; sa.Ggen = 8 * c->num_sms;
+        sa.dbg_print = std::getenv("LRK_SF_DEBUG") ? std::atoi(std::getenv("LRK_SF_DEBUG")) : 0;
+        sa.smem_pass = (int)sf_smem_pass();
+      }
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
-      CK(launch_sweep_stream(sa, nflush, s, c->aux, &c->launches));
+      CK(launch_sweep_stream(sh.data(), nlocal, nflush, s, c->aux, &c->xseq, &c->launches));
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot + 1], s));
+      if (dist) {
+        // every rank needs the whole pane basis for the replicated stages
+        double* panes[SF_XMAXR] = {};
+        const size_t off = tag == "f_" ? c->dist.off_f : c->dist.off_b;
+        if (reinterpret_cast<char*>(U0) != c->dist.arena + off)
+          return fail(c, LRK_ERR_CONFIG, "sharded sweep pane is not in the peer-shared arena");
+        for (int q = 0; q < S; ++q) panes[q] = reinterpret_cast<double*>(c->dist.peer[q] + off);
+        CK(sf_allgather_pane(sh[0], panes, ld, my_x0, my_rows, ucap, s, &c->xseq, &c->launches));
+      }
       o.U = U0; o.V = V0; o.sigma = sig; o.info = info; o.trace = trace;
       o.ucap = ucap; o.nflush = nflush; o.ldu = ld; o.ldv = nt;
       return LRK_OK;
@@ -996,6 +1066,8 @@ int host_max_rank(lrk_ctx* c, const SweepOut& f, const int* zinfo, const SweepOu
   if (fi[2] != 0 || gi[2] != 0)
     return fail(c, LRK_ERR_UNSUPPORTED,
                 "sweep core exceeded the 160-column device limit (set r_max <= 160 - compress_every)");
+  if (fi[5] != 0 || gi[5] != 0)
+    return fail(c, LRK_ERR_CUDA, "n_x-sharded sweep: a peer never reached an exchange (timed out)");
   if (zr[2] != 0) return fail(c, LRK_ERR_SHAPE, "observation truncation exceeded its capacity");
   int m = zr[0];
   for (int v : t1) m = std::max(m, v);
@@ -1116,6 +1188,69 @@ int lrk_set_emulated_shards(lrk_ctx* c, int nshard) {
   if (!c) return LRK_ERR_CONFIG;
   if (nshard < 1 || nshard > SHARD_MAX) return fail(c, LRK_ERR_CONFIG, "nshard must lie in [1, 8]");
   c->emu_shards = nshard;
+  return LRK_OK;
+}
+
+// n_x sharding across processes: one process per GPU, each with
+// its own context holding the whole operator; the sweeps run on this rank's
+// row slab and exchange their small rank totals through peer memory.
+int lrk_shard_setup(lrk_ctx* c, int rank, int world, void* handle_out) {
+  if (!c || !handle_out) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  TRY(check_op(c));
+  if (world < 1 || world > SF_XMAXR || rank < 0 || rank >= world)
+    return fail(c, LRK_ERR_CONFIG, "shard rank/world out of range (world <= 8)");
+  if (c->dist.arena) return fail(c, LRK_ERR_CONFIG, "context is already sharded");
+  const int64_t ld = padld(c->n_x);
+  const size_t xb = (sizeof(SFXBuf) + 4095) / 4096 * 4096;
+  const size_t pane = ((size_t)ld * SF_CAP * sizeof(double) + 256 + 4095) / 4096 * 4096;
+  c->dist.bytes = xb + 2 * pane;
+  c->dist.off_f = xb;
+  c->dist.off_b = xb + pane;
+  void* p = nullptr;
+  if (cudaMalloc(&p, c->dist.bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, LRK_ERR_CUDA, "cudaMalloc failed for the peer-shared arena");
+  }
+  CK(cudaMemset(p, 0, xb));
+  c->dist.arena = static_cast<char*>(p);
+  c->dist.rank = rank;
+  c->dist.world = world;
+  c->dist.peer[rank] = c->dist.arena;
+  for (const char* tag : {"f_U0", "b_U0"}) {
+    Buf& b = c->ws[tag];
+    if (b.p && !b.ext) cudaFree(b.p);
+    b.p = c->dist.arena + (std::string(tag) == "f_U0" ? c->dist.off_f : c->dist.off_b);
+    b.bytes = pane;
+    b.ext = true;
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, p));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  c->dist.connected = world == 1;
+  return LRK_OK;
+}
+
+// handles: world x 64 bytes, the lrk_shard_setup outputs of all ranks in rank order.
+int lrk_shard_connect(lrk_ctx* c, const void* handles) {
+  if (!c || !handles) return LRK_ERR_CONFIG;
+  CK(cudaSetDevice(c->device));
+  if (!c->dist.arena) return fail(c, LRK_ERR_CONFIG, "lrk_shard_connect before lrk_shard_setup");
+  for (int q = 0; q < c->dist.world; ++q) {
+    if (q == c->dist.rank || c->dist.peer[q]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)q * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, LRK_ERR_CUDA, std::string("cudaIpcOpenMemHandle failed for a peer arena: ") +
+                                       cudaGetErrorString(e));
+    }
+    c->dist.peer[q] = static_cast<char*>(p);
+  }
+  c->dist.connected = true;
   return LRK_OK;
 }
 

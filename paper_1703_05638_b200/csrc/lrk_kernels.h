@@ -85,71 +85,6 @@ int64_t sweep_scratch_stride(int ncta);
 int64_t sweep_part_stride();
 cudaError_t launch_sweep(const SweepBatch& batch, cudaStream_t s);
 
-// Streaming-flush sweep (lrk_sflush.cu): the large-n_x form of the sweep,
-// one kernel per row pass, flush width <= 4, pane rank <= 64.
-constexpr int SF_CAP = 64;
-constexpr int SF_P = 4;
-constexpr int SF_N = SF_CAP + SF_P;
-constexpr int SF_LDW = 68;
-
-// Small per-sweep state in global memory (written by the last CTA of each
-// pass and by sf_finish, read by the next pass).
-struct SFState {
-  int r;         // valid pane columns of U (after the last applied update)
-  int rn;        // pane rank of the pending update
-  int pcp;       // width of the remainder block next to U (X = [U, y])
-  int pending;   // an update (Wp, Vc) is pending
-  int startp;    // flush start of the pending update (time-row selection)
-  int drop_all;  // the current remainder is at the rounding floor
-  int pc_new;    // width of the flush being projected (Yn)
-  int pad;
-  double sig[SF_N];
-  double C[SF_CAP * SF_P];   // C1 (+ P2) of the flush being orthogonalised, [i * SF_P + s]
-  double P2[SF_CAP * SF_P];
-  double M[SF_N * SF_P];     // [U, y2]^T Yn of the next flush, [k * SF_P + s]
-  double Wd[SF_N * SF_P];    // -Wp C1: y1 = Yn + [U, y2] Wd, [k * SF_P + s]
-  double yn[SF_P];           // |Y_s|^2 of the flush being orthogonalised
-  double yn_next[SF_P];      // ... of the flush being projected
-  double Rc[16];             // remainder R (row-major 4x4)
-  double Rinv[16];           // Q = y2 Rinv
-  double Wp[SF_N * SF_LDW];  // pending spatial update (n x rn), col-major
-  double Vc[SF_N * SF_LDW];  // pending time update (n x rn), col-major
-};
-
-struct SFArgs {
-  int64_t n_x;
-  int64_t n_x_glob;      // rows of the whole (unsharded) field
-  int n_t, p, cap, adjoint, r_max, nflush;
-  double eps0, ftz;
-  double* U; int64_t ldu;
-  double* V; int64_t ldv;
-  double* Yg[3]; int64_t ldy;   // flush f lives in Yg[f % 3]
-  double* yprev;
-  const double* theta;
-  const double* rowscale;
-  const double* B; int64_t ldb; int rb;
-  const int* rb_dev;
-  const double* W2; int64_t ldw2;
-  double* part;          // G * sf_part_stride() doubles
-  unsigned* ticket;      // 8 counters (zero)
-  SFState* st;
-  int* trace; int* info; double* sigma;
-  int G;                 // CTAs of the staged row passes
-  int Ggen;              // CTAs of the light grid-stride passes
-  int dbg_print;         // LRK_SF_DEBUG: flushes to report (diagnostics)
-  int smem_pass;         // dynamic shared memory of the staged passes (bytes)
-};
-size_t sf_smem_pass();
-int64_t sf_part_stride();
-// aux: a second (non-blocking) stream + two events, used to run the next
-// flush's column generation under the single-CTA core SVD.
-struct SFAux {
-  cudaStream_t stream;
-  cudaEvent_t ready, done;
-};
-cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, const SFAux& aux,
-                                int64_t* launches);
-
 // General lr_truncate (lowrank.py:124-144) of W1 (n_x x R) W2^T (n_t x R).
 struct TruncArgs {
   int64_t n_x;

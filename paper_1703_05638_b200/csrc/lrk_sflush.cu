@@ -42,6 +42,7 @@
 
 #include "lrk_device.cuh"
 #include "lrk_kernels.h"
+#include "lrk_sflush.h"
 #include "lrk_small.cuh"
 
 namespace lrk {
@@ -52,6 +53,7 @@ constexpr int ST = 256;           // threads per CTA of the light passes
 constexpr int NW = 16;            // warps of the staged row passes
 constexpr int SPT = 32 * NW;
 constexpr int LDW = 68;           // shared leading dimension of the update matrix (== 4 mod 16)
+static_assert(LDW == SF_LDW, "pass_b_tail reads the shared and the global update matrix alike");
 constexpr int PSTR = SF_N * SF_P + 16 + SF_P + 4;  // per-CTA partial stride (doubles)
 
 // ---- warp-private cp.async rings.  Every staged pass works on 8-row tiles
@@ -202,6 +204,53 @@ __device__ __forceinline__ void reduce_parts(const double* part, int len, double
       out[e] = a0;
       if (two) out[e + 1] = a1;
     }
+  }
+  __syncthreads();
+}
+
+static_assert(PSTR <= SF_XLEN, "rank totals must fit an exchange slot");
+
+// Sharded sweeps: store this shard's total into every shard's exchange slot,
+// then release the flags (see SFXBuf).  Called by the whole last CTA.
+__device__ __forceinline__ void xr_deposit(const SFArgs& a, unsigned long long seq, const double* tot,
+                                           int len) {
+  const int par = (int)(seq & 1ull);
+  for (int q = 0; q < a.nshard; ++q) {
+    double* dst = a.xpeer[q]->data[par][a.shard];
+    for (int e = threadIdx.x; e < len; e += blockDim.x) dst[e] = tot[e];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if ((int)threadIdx.x < a.nshard) {
+    unsigned long long* fl = &a.xpeer[threadIdx.x]->flag[par][a.shard];
+    asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(fl), "l"(seq) : "memory");
+  }
+}
+
+// Wait for every shard's deposit of exchange `seq` and sum the slots in shard
+// order.  A shard that never arrives (lost peer) is reported through info[5]
+// after ~4e9 cycles instead of hanging the device.
+__device__ __forceinline__ void xr_collect(const SFArgs& a, unsigned long long seq, int len, double* tot) {
+  const int par = (int)(seq & 1ull);
+  SFXBuf* own = a.xpeer[a.shard];
+  if ((int)threadIdx.x < a.nshard) {
+    const unsigned long long* fl = &own->flag[par][threadIdx.x];
+    const long long t0 = clock64();
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(fl) : "memory");
+      if (v >= seq) break;
+      if (clock64() - t0 > (1ll << 32)) {
+        a.info[5] = 1;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < len; e += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < a.nshard; ++q) s += __ldcv(&own->data[par][q][e]);
+    tot[e] = s;
   }
   __syncthreads();
 }
@@ -378,6 +427,58 @@ static __device__ __noinline__ void sf_chol_update(SFState* st, const double* to
 //   last CTA: P2 = Wp^T Pm, C = C1 + P2, pane bookkeeping (r <- rn, pcp <- pcn).
 // Warp w owns tiles w, w+16, ... of the CTA's 8-row tile range: its step-1
 // output tile and its share of the projections need no CTA barrier.
+// Tail of pass A (whole CTA; tot = M (n x 4) | G0 (4 x 4) | |Yn_s|^2): the
+// projection of the flush being opened goes to the state, the remainder of
+// the flush being closed gets its shifted Cholesky factor.
+__device__ __forceinline__ void pass_a_tail(const SFArgs& a, SFState* st, const double* tot, int f) {
+  const int tid = threadIdx.x;
+  const int r = st->r, pcp = st->pcp, n = r + pcp;
+  const int pcn = f < a.nflush ? min(a.p, a.n_t - f * a.p) : 0;
+  for (int idx = tid; idx < n * SF_P; idx += blockDim.x) st->M[idx] = tot[idx];
+  if (tid < SF_P) st->yn_next[tid] = tot[n * SF_P + 16 + tid];
+  __syncthreads();
+  if (tid == 0) {
+    st->pc_new = pcn;
+    if (pcp > 0) {
+      sf_shifted_chol(a, st, tot + n * SF_P, pcp);
+    } else {
+      // nothing to close (first flush): no sf_finish will run before pass B
+      for (int s2 = 0; s2 < SF_P; ++s2) st->yn[s2] = tot[n * SF_P + 16 + s2];
+      st->rn = r;
+      st->pending = 0;
+    }
+  }
+}
+
+// Tail of pass B (whole CTA; tot = Pm (n x 4); Wp: n x rn, column stride LDW):
+// P2 = Wp^T Pm, C = C1 + P2; the pane now has rn explicit columns.
+__device__ __forceinline__ void pass_b_tail(const SFArgs& a, SFState* st, const double* tot,
+                                            const double* Wp, int f) {
+  const int tid = threadIdx.x;
+  const int r = st->r, pcp = st->pcp, n = r + pcp, rn = st->rn;
+  const int pcn = f < a.nflush ? min(a.p, a.n_t - f * a.p) : 0;
+  for (int idx = tid; idx < rn * pcn; idx += blockDim.x) {
+    const int i = idx / pcn, s2 = idx % pcn;
+    double acc = 0.0;
+    for (int k = 0; k < n; ++k) acc += Wp[i * LDW + k] * tot[k * SF_P + s2];
+    st->P2[i * SF_P + s2] = acc;
+    st->C[i * SF_P + s2] += acc;
+  }
+  const bool final_pass = f >= a.nflush;
+  if (final_pass)
+    for (int k = tid; k < rn; k += blockDim.x) a.sigma[k] = st->sig[k];
+  __syncthreads();
+  if (tid == 0) {
+    st->r = rn;
+    st->pcp = pcn;
+    st->pending = 0;
+    if (final_pass) {
+      a.info[0] = rn;
+      a.trace[a.nflush] = rn;
+    }
+  }
+}
+
 // Runtime sizes and pointers of one pass (uniform over the CTA).
 struct PassRt {
   int r, pcp, n, pcn, rn, nwc, ncol, per_warp;
@@ -508,7 +609,7 @@ __device__ __forceinline__ void pass_loop(const SFArgs& a, const PassRt& P, doub
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
+__global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f, unsigned long long seq) {
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long colp[SF_N + SF_P + 8];
   SFState* st = a.st;
@@ -636,44 +737,27 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f) {
   if (!last_cta(a.ticket + MODE, flag)) return;
   double* tot = red + NW * PSTR + 64;
   reduce_parts(a.part, plen, tot);
-  if (MODE == 0) {
-    for (int idx = tid; idx < n * SF_P; idx += SPT) st->M[idx] = tot[idx];
-    if (tid < SF_P) st->yn_next[tid] = tot[n * SF_P + 16 + tid];
-    __syncthreads();
-    if (tid == 0) {
-      st->pc_new = pcn;
-      if (pcp > 0) {
-        sf_shifted_chol(a, st, tot + n * SF_P, pcp);
-      } else {
-        // nothing to close (first flush): no sf_finish will run before pass B
-        for (int s2 = 0; s2 < SF_P; ++s2) st->yn[s2] = tot[n * SF_P + 16 + s2];
-        st->rn = r;
-        st->pending = 0;
-      }
-    }
+  if (a.nshard > 1) {  // the tail runs in sf_tail once every shard has deposited
+    xr_deposit(a, seq, tot, plen);
     return;
   }
-  // pass B: P2 = Wp^T Pm, C = C1 + P2; the pane now has rn explicit columns
-  for (int idx = tid; idx < rn * pcn; idx += SPT) {
-    const int i = idx / pcn, s2 = idx % pcn;
-    double acc = 0.0;
-    for (int k = 0; k < n; ++k) acc += W[i * LDW + k] * tot[k * SF_P + s2];
-    st->P2[i * SF_P + s2] = acc;
-    st->C[i * SF_P + s2] += acc;
-  }
-  const bool final_pass = f >= a.nflush;
-  if (final_pass)
-    for (int k = tid; k < rn; k += SPT) a.sigma[k] = st->sig[k];
-  __syncthreads();
-  if (tid == 0) {
-    st->r = rn;
-    st->pcp = pcn;
-    st->pending = 0;
-    if (final_pass) {
-      a.info[0] = rn;
-      a.trace[a.nflush] = rn;
-    }
-  }
+  if (MODE == 0) pass_a_tail(a, st, tot, f);
+  else pass_b_tail(a, st, tot, W, f);
+}
+
+// One-CTA tail of a sharded pass: collect the shard totals, then the same
+// small algebra the last CTA runs in an unsharded sweep.
+// KIND 0: pass A, 1: pass B, 2: CholeskyQR pass.
+template <int KIND>
+__global__ void __launch_bounds__(ST) sf_tail(const SFArgs a, int f, unsigned long long seq) {
+  __shared__ double tot[SF_XLEN];
+  SFState* st = a.st;
+  const int n = st->r + st->pcp;
+  const int len = KIND == 0 ? n * SF_P + 16 + SF_P : (KIND == 1 ? n * SF_P : 10);
+  xr_collect(a, seq, len, tot);
+  if (KIND == 0) pass_a_tail(a, st, tot, f);
+  else if (KIND == 1) pass_b_tail(a, st, tot, st->Wp, f);
+  else if (threadIdx.x == 0 && !st->drop_all) sf_chol_update(st, tot, st->pcp);
 }
 
 // ------------------------------------------------------------ generation
@@ -735,7 +819,8 @@ __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
 // G = Q^T Q with Q = y2 Rinv; R <- chol(G) R, Rinv <- Rinv chol(G)^{-1}
 // (pivoted, drop-tolerant).  Light streaming kernel over the 4 columns of
 // flush f (usually still in L2): 4 rows per thread and step, 16 loads in flight.
-__global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pass) {
+__global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pass,
+                                                     unsigned long long seq) {
   SFState* st = a.st;
   __shared__ int flag;
   __shared__ double red[8 * 10 + 16];
@@ -782,6 +867,10 @@ __global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pa
   if (tid < 10) part[tid] = outv[tid];
   if (!last_cta(a.ticket + 3 + pass, &flag)) return;
   reduce_parts(a.part, 10, tot);
+  if (a.nshard > 1) {
+    xr_deposit(a, seq, tot, 10);
+    return;
+  }
   if (tid == 0 && !skip) sf_chol_update(st, tot, pc);
 }
 
@@ -919,6 +1008,45 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
   }
 }
 
+// ---------------------------------------------------- pane all-gather (sharded)
+// After a sharded sweep every rank holds its own row slab of the pane basis;
+// the stages that follow (observation, extraction) run replicated on the full
+// basis, so each rank pushes its slab into every peer's pane over NVLink and
+// all ranks meet at a flag barrier (the same exchange slots, zero payload).
+struct SFPanes {
+  double* p[SF_XMAXR];
+};
+__global__ void __launch_bounds__(ST) sf_push_rows(const SFPanes panes, int nshard, int shard, int64_t ld,
+                                                   int64_t x0, int64_t rows, const int* r_dev, int cap) {
+  const int col = blockIdx.y;
+  const int r = r_dev ? min(cap, *r_dev) : cap;
+  if (col >= r) return;
+  const double* src = panes.p[shard] + x0 + (int64_t)col * ld;
+  for (int64_t i = (int64_t)blockIdx.x * ST + threadIdx.x; i < rows; i += (int64_t)gridDim.x * ST) {
+    const double v = src[i];
+    for (int q = 0; q < nshard; ++q)
+      if (q != shard) panes.p[q][x0 + i + (int64_t)col * ld] = v;
+  }
+}
+__global__ void __launch_bounds__(32) sf_barrier(const SFArgs a, unsigned long long seq) {
+  __shared__ double dummy[1];
+  xr_deposit(a, seq, dummy, 0);
+  xr_collect(a, seq, 0, dummy);
+}
+
+cudaError_t sf_allgather_pane(const SFArgs& a, double* const* pane, int64_t ld, int64_t x0, int64_t rows,
+                              int cap, cudaStream_t s, unsigned long long* xseq, int64_t* launches) {
+  SFPanes P{};
+  for (int q = 0; q < a.nshard; ++q) P.p[q] = pane[q];
+  int gx = (int)std::min<int64_t>((rows + ST - 1) / ST, 1184);
+  if (gx < 1) gx = 1;
+  sf_push_rows<<<dim3(gx, cap), ST, 0, s>>>(P, a.nshard, a.shard, ld, x0, rows, a.info, cap);
+  const unsigned long long seq = ++(*xseq);
+  sf_barrier<<<1, 32, 0, s>>>(a, seq);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host side
 size_t sf_smem_pass() { return 210 * 1024; }
 size_t sf_smem_finish() {
@@ -947,59 +1075,80 @@ cudaError_t sf_configure() {
 // The whole sweep: for f = 0..nflush: pass A(f) [closes f-1, projects f],
 // CholeskyQR x 2 + finish of flush f-1 (with the generation of flush f+1 next
 // to them on the aux stream), pass B(f) [update of f-1, first CGS pass of f].
-// Returns the number of launches.
-cudaError_t launch_sweep_stream(const SFArgs& a, int nflush, cudaStream_t s, const SFAux& aux,
-                                int64_t* launches) {
+// Sharded sweeps (nshard > 1) add a one-CTA tail kernel after every pass that
+// ends in a rank total.  With several local shards (single-device emulation)
+// every step is launched for all shards before the next step, on one stream.
+cudaError_t launch_sweep_stream(const SFArgs* sh, int nlocal, int nflush, cudaStream_t s,
+                                const SFAux& aux, unsigned long long* xseq, int64_t* launches) {
   cudaError_t e = sf_configure();
   if (e != cudaSuccess) return e;
-  const int G = a.G;
-  const int Gg = a.Ggen;
+  const SFArgs& a0 = sh[0];
+  const int G = a0.G;
+  const int Gg = a0.Ggen;
   const int Gc = 2 * (Gg / 8 > 0 ? Gg / 8 : 1);  // CholeskyQR passes: 2 CTAs per SM
-  const size_t sp = a.smem_pass, sfin = sf_smem_finish();
+  const size_t sp = a0.smem_pass, sfin = sf_smem_finish();
+  const bool sharded = a0.nshard > 1;
+  const bool use_aux = nlocal == 1 && aux.stream != nullptr;
+  unsigned long long seq = xseq ? *xseq : 0ull;
   int64_t nl = 0;
-  const int dbg = a.dbg_print;
+  const int dbg = a0.dbg_print;
   auto show = [&](const char* what, int f) {
     if (f >= dbg) return;
     SFState* h = new SFState;
     cudaStreamSynchronize(s);
-    cudaMemcpy(h, a.st, sizeof(*h), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, a0.st, sizeof(*h), cudaMemcpyDeviceToHost);
     std::fprintf(stderr, "[sf] f=%d %-8s r=%d rn=%d pcp=%d pcn=%d pend=%d drop=%d err=%s | yn %.3e %.3e | C00 %.6e C01 %.6e P2_00 %.3e M00 %.6e | sig %.6e %.6e | Rc %.4e %.4e %.4e %.4e\n",
                  f, what, h->r, h->rn, h->pcp, h->pc_new, h->pending, h->drop_all,
                  cudaGetErrorString(cudaGetLastError()), h->yn[0], h->yn[1], h->C[0], h->C[1],
                  h->P2[0], h->M[0], h->sig[0], h->sig[1], h->Rc[0], h->Rc[5], h->Rc[10], h->Rc[15]);
     delete h;
   };
-  sf_generate<<<Gg, ST, 0, s>>>(a, 0);
-  ++nl;
+  for (int g = 0; g < nlocal; ++g) sf_generate<<<Gg, ST, 0, s>>>(sh[g], 0);
+  nl += nlocal;
   for (int f = 0; f <= nflush; ++f) {
-    sf_pass<0><<<G, SPT, sp, s>>>(a, f);
-    ++nl;
+    ++seq;
+    for (int g = 0; g < nlocal; ++g) sf_pass<0><<<G, SPT, sp, s>>>(sh[g], f, seq);
+    if (sharded)
+      for (int g = 0; g < nlocal; ++g) sf_tail<0><<<1, ST, 0, s>>>(sh[g], f, seq);
+    nl += nlocal * (sharded ? 2 : 1);
     show("passA", f);
     if (f > 0) {
-      sf_cholqr<<<Gc, ST, 0, s>>>(a, f - 1, 0);
-      sf_cholqr<<<Gc, ST, 0, s>>>(a, f - 1, 1);
-      nl += 2;
+      for (int pass = 0; pass < 2; ++pass) {
+        ++seq;
+        for (int g = 0; g < nlocal; ++g) sf_cholqr<<<Gc, ST, 0, s>>>(sh[g], f - 1, pass, seq);
+        if (sharded)
+          for (int g = 0; g < nlocal; ++g) sf_tail<2><<<1, ST, 0, s>>>(sh[g], f - 1, seq);
+        nl += nlocal * (sharded ? 2 : 1);
+      }
     }
     // flush f+1's columns (buffer (f+1) % 3, last read by pass B(f-1)) are
     // generated on the aux stream, next to the single-CTA sf_finish
     const bool gen = f + 1 < nflush;
     if (gen) {
-      if ((e = cudaEventRecord(aux.ready, s)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(aux.stream, aux.ready, 0)) != cudaSuccess) return e;
-      sf_generate<<<Gg, ST, 0, aux.stream>>>(a, f + 1);
-      ++nl;
-      if ((e = cudaEventRecord(aux.done, aux.stream)) != cudaSuccess) return e;
+      if (use_aux) {
+        if ((e = cudaEventRecord(aux.ready, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(aux.stream, aux.ready, 0)) != cudaSuccess) return e;
+        sf_generate<<<Gg, ST, 0, aux.stream>>>(sh[0], f + 1);
+        if ((e = cudaEventRecord(aux.done, aux.stream)) != cudaSuccess) return e;
+      } else {
+        for (int g = 0; g < nlocal; ++g) sf_generate<<<Gg, ST, 0, s>>>(sh[g], f + 1);
+      }
+      nl += nlocal;
     }
     if (f > 0) {
-      sf_finish<<<1, ST, sfin, s>>>(a, f - 1);
-      ++nl;
+      for (int g = 0; g < nlocal; ++g) sf_finish<<<1, ST, sfin, s>>>(sh[g], f - 1);
+      nl += nlocal;
       show("finish", f);
     }
-    sf_pass<1><<<G, SPT, sp, s>>>(a, f);
-    ++nl;
+    ++seq;
+    for (int g = 0; g < nlocal; ++g) sf_pass<1><<<G, SPT, sp, s>>>(sh[g], f, seq);
+    if (sharded)
+      for (int g = 0; g < nlocal; ++g) sf_tail<1><<<1, ST, 0, s>>>(sh[g], f, seq);
+    nl += nlocal * (sharded ? 2 : 1);
     show("passB", f);
-    if (gen && (e = cudaStreamWaitEvent(s, aux.done, 0)) != cudaSuccess) return e;
+    if (gen && use_aux && (e = cudaStreamWaitEvent(s, aux.done, 0)) != cudaSuccess) return e;
   }
+  if (xseq) *xseq = seq;
   if (launches) *launches += nl;
   return cudaGetLastError();
 }

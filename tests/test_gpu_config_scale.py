@@ -271,3 +271,41 @@ def test_streaming_flush_small_fixtures_vs_reference(golden, monkeypatch, name):
         assert np.linalg.norm(out - Oref[:, j]) <= 1e-9 * np.linalg.norm(Oref[:, j])
         if refr.size == V.shape[1]:
             assert ctx.rank_trace[-1] == refr[j]
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+def test_nx_sharded_streaming_sweep_c4_path_vs_reference(shards):
+    """The n_x-sharded streaming sweep — row slabs with their
+    own partial tables, rank totals exchanged through the SFXBuf slots and
+    release/acquire flags, one-CTA tail kernels — driven for all shards by one
+    process (single-device emulation: the kernels and the exchange protocol
+    are the ones the multi-process path runs over peer memory).  C4-path
+    apply against the reference fixture: values and rank trace."""
+    from paper_1703_05638_b200 import _lib
+
+    ctx, grid, _ = _ctx(48, 3, "fd", 32, 12, 4, 0.005, 1.0, 0.02, 64)
+    assert _lib.get_lib().lrk_set_emulated_shards(ctx._dev.handle, shards) == 0
+    fx = _fx("c4_sweep3d")
+    v = np.random.default_rng(3).standard_normal(grid.n_x)
+    _check_apply(ctx, v / np.linalg.norm(v), fx)
+
+
+def test_nx_sharded_streaming_sweep_c2_config_vs_unsharded(monkeypatch):
+    """C2 bench configuration with the streaming form forced: 2 and 8 row
+    shards against the unsharded streaming sweep — identical rank traces,
+    values equal to rounding (the shard totals are summed in a different
+    order than the CTA partials of one device)."""
+    from paper_1703_05638_b200 import _lib
+
+    monkeypatch.setenv("LRK_SFLUSH", "1")
+    ctx, grid, _ = _c2()
+    v = np.random.default_rng(1).standard_normal(grid.n_x)
+    v /= np.linalg.norm(v)
+    a = ctx.apply(v)
+    tr_a = ctx.last_traces()
+    for shards in (2, 8):
+        assert _lib.get_lib().lrk_set_emulated_shards(ctx._dev.handle, shards) == 0
+        b = ctx.apply(v)
+        tr_b = ctx.last_traces()
+        assert tr_a == tr_b
+        np.testing.assert_allclose(b, a, rtol=0, atol=1e-11 * np.abs(a).max())
