@@ -349,10 +349,40 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     ctx, grid = make_context(cfg, lp)
     nprobe = args.steps + args.warmup
-    V = probes(grid.n_x, nprobe, cfg["seed"] * 1000 + rank)
-    Vd = torch.as_tensor(V, device="cuda").T.contiguous()  # resident in HBM, one row per probe
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     lib = _lib.get_lib()
+
+    # N > 1: the sweeps of every apply are sharded by n_x rows across the ranks
+    # (strong scaling: all ranks apply the SAME probes and return the same
+    # result).  If the peer-memory setup or the first sharded applies fail on
+    # this box, every rank falls back to independent probes (replicas) and the
+    # line says so.
+    mode, note = "single", ""
+    if world > 1 and args.parallel == "shard":
+        ok = torch.ones(1, device="cuda")
+        try:
+            ctx.shard()
+            Vw = torch.as_tensor(probes(grid.n_x, 1, cfg["seed"] * 1000), device="cuda").T.contiguous()
+            ctx.apply(Vw[0])
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 - reported in the JSON line
+            ok.zero_()
+            note = f"{type(exc).__name__}: {exc}"[:200]
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if float(ok.item()) == 1.0:
+            mode = "shard"
+        else:
+            mode = "replicas"
+            notes = [None] * world
+            dist.all_gather_object(notes, note)
+            note = next((x for x in notes if x), "a peer failed")
+            del ctx
+            torch.cuda.synchronize()
+            ctx, grid = make_context(cfg, lp)
+    elif world > 1:
+        mode = "replicas"
+    V = probes(grid.n_x, nprobe, cfg["seed"] * 1000 + (rank if mode == "replicas" else 0))
+    Vd = torch.as_tensor(V, device="cuda").T.contiguous()  # resident in HBM, one row per probe
     h_dev = ctx._dev.handle
 
     for i in range(args.warmup):
@@ -409,6 +439,7 @@ def gpu_arm(args, cfg, rank, world, local_rank):
         "total_ms": float(stats[0]), "e2e_s": float(stats[1]), "launches": launches,
         "ranks": ranks, "sweep_ms": sw_ms.value, "sweep_n": sw_n.value,
         "sweep_bytes": sw_bytes.value, "clocks": clk.summary(), "n_x": grid.n_x,
+        "mode": mode, "note": note,
     }
 
 
@@ -452,6 +483,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parallel", default="shard", choices=["shard", "replicas"],
+                    help="N > 1: n_x-sharded sweeps (strong scaling) or independent probes per rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -489,14 +522,25 @@ def main():
         per_launch_bytes = res["sweep_bytes"] / max(res["sweep_n"], 1)
         achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
         traffic, tsrc = ncu_traffic(args.config)
-        n = args.gpus
+        n = args.gpus if res["mode"] == "replicas" else 1   # applies completed per step, whole job
         line = dict(base)
+        if res["mode"] == "shard":
+            line["scaling"] = "strong"
+            line["config"] = dict(config, parallelism=(
+                f"n_x row-sharded sweeps x{args.gpus} (peer-memory exchange of the per-pass rank "
+                "totals, pane all-gather; inputs/outputs replicated)"))
+        elif res["mode"] == "replicas" and res["note"]:
+            line["config"] = dict(config, parallelism=(
+                f"independent probes x{args.gpus} (replicas; n_x sharding unavailable here: "
+                f"{res['note']})"))
         line.update({
             "value": n * args.steps / (res["total_ms"] * 1e-3),
             "ms_per_step": res["total_ms"] / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
-                         "kernel": "lrk::sweep_kernel", "peak_kind": peak_kind,
+                         "kernel": ("streaming-flush sweep (per flush: lrk::sf_pass<0>, sf_pass<1>, "
+                                    "2 x sf_cholqr, sf_finish, sf_generate)" if args.config == "C4"
+                                    else "lrk::sweep_kernel"), "peak_kind": peak_kind,
                          "alg_bytes_per_launch": per_launch_bytes,
                          "ms_per_launch": per_launch_ms, "build": build_hash()},
             "cpu_baseline": cpu,

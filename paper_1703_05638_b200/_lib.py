@@ -90,6 +90,8 @@ _SIGNATURES = {
     "lrk_launch_count": (c_int64, [c_void_p]),
     "lrk_profile_enable": (c_int, [c_void_p, c_int]),
     "lrk_set_emulated_shards": (c_int, [c_void_p, c_int]),
+    "lrk_shard_setup": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+    "lrk_shard_connect": (c_int, [c_void_p, c_void_p]),
     "lrk_prior_apply": (c_int, [c_void_p, c_double, c_double, c_int, c_void_p, c_int64, c_int,
                                 c_void_p, c_int64, c_void_p]),
     "lrk_prior_diag": (c_int, [c_void_p, c_double, c_double, c_int, c_void_p, c_void_p]),

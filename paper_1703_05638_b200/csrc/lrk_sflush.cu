@@ -233,7 +233,9 @@ __device__ __forceinline__ void xr_deposit(const SFArgs& a, unsigned long long s
 __device__ __forceinline__ void xr_collect(const SFArgs& a, unsigned long long seq, int len, double* tot) {
   const int par = (int)(seq & 1ull);
   SFXBuf* own = a.xpeer[a.shard];
-  if ((int)threadIdx.x < a.nshard) {
+  // (after one timeout every later exchange of the sweep is let through: the
+  // host reports the failure once the sweep has drained)
+  if ((int)threadIdx.x < a.nshard && *reinterpret_cast<volatile int*>(a.info + 5) == 0) {
     const unsigned long long* fl = &own->flag[par][threadIdx.x];
     const long long t0 = clock64();
     for (;;) {

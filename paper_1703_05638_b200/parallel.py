@@ -1,5 +1,12 @@
 """Multi-GPU host logic: one process per GPU, torch.distributed for plumbing.
 
+`shard_context` turns the sweeps of a device context into n_x-sharded sweeps
+across the ranks of a process group: each rank keeps the whole
+operator and replicated n_x inputs/outputs, runs the forward and adjoint
+sweeps on its own row slab, and exchanges the small per-pass rank totals
+through peer-mapped memory inside the kernels (include/lrk.h, lrk_shard_*);
+torch.distributed only carries the 64-byte CUDA IPC handles at setup.
+
 Two decompositions:
 
 * **Probe sharding** (used by bench.py at N>1): Hessian applies on different
@@ -72,3 +79,48 @@ def reduce_partials_fixed_order(local, group=None):
     for p in parts:
         out += p
     return out
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def exchange_handles(mine: bytes, group=None, device=None) -> bytes:
+    """All-gather one fixed-size byte string per rank, in rank order (the CUDA
+    IPC handles of lrk_shard_setup).  Works on any backend: the payload rides
+    in a uint8 tensor on `device` (CPU for gloo, the rank's GPU for nccl)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if device is None:
+        device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(mine), dtype=torch.uint8, device=device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return b"".join(bytes(p.cpu().tolist()) for p in parts)
+
+
+def shard_context(dev_ctx, group=None, device=None) -> tuple[int, int]:
+    """Shard the sweeps of `dev_ctx` (a _lib.Context with its operator
+    installed) by n_x rows across the ranks of `group`.  Returns (rank, world).
+    With a world of one this is a no-op."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import _lib
+
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if world == 1:
+        return 0, 1
+    lib = _lib.get_lib()
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _lib.check(lib.lrk_shard_setup(dev_ctx.handle, rank, world, h), dev_ctx.handle,
+               "shard_context")
+    handles = exchange_handles(h.raw, group=group, device=device)
+    buf = ctypes.create_string_buffer(handles, len(handles))
+    _lib.check(lib.lrk_shard_connect(dev_ctx.handle, buf), dev_ctx.handle, "shard_context")
+    dist.barrier(group=group)
+    return rank, world

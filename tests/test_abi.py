@@ -4,6 +4,7 @@
 import os
 import re
 
+import numpy as np
 import pytest
 
 from paper_1703_05638_b200 import _lib
@@ -59,3 +60,18 @@ def test_error_mapping():
         _lib.check(_lib.LRK_ERR_CONVERGENCE)
     with pytest.raises(NotImplementedError):
         _lib.check(_lib.LRK_ERR_UNSUPPORTED)
+
+
+def test_start_vector_matches_the_reference_rule():
+    """cli.py:247-266: all-ones default, otherwise PCG64 standard_normal(seed), normalised."""
+    import paper_1703_05638_b200 as lp
+
+    v = lp.start_vector(50)
+    np.testing.assert_array_equal(v, np.ones(50) / np.sqrt(50.0))
+    w = lp.start_vector(50, start="random", seed=7)
+    ref = np.random.default_rng(7).standard_normal(50)
+    np.testing.assert_array_equal(w, ref / np.linalg.norm(ref))
+    with pytest.raises(ValueError):
+        lp.start_vector(5, start="zeros")
+    with pytest.raises(ValueError):
+        lp.start_vector(5, mode="source")

@@ -309,3 +309,21 @@ def test_nx_sharded_streaming_sweep_c2_config_vs_unsharded(monkeypatch):
         tr_b = ctx.last_traces()
         assert tr_a == tr_b
         np.testing.assert_allclose(b, a, rtol=0, atol=1e-11 * np.abs(a).max())
+
+
+def test_shard_arena_world_one_c4_path_vs_reference():
+    """lrk_shard_setup with a world of one: the sweep panes move into the
+    IPC-exportable arena (the layout every rank of a sharded job uses) and the
+    apply still reproduces the reference."""
+    import ctypes
+
+    from paper_1703_05638_b200 import _lib
+
+    ctx, grid, _ = _ctx(48, 3, "fd", 32, 12, 4, 0.005, 1.0, 0.02, 64)
+    h = ctypes.create_string_buffer(64)
+    assert _lib.get_lib().lrk_shard_setup(ctx._dev.handle, 0, 1, h) == 0
+    assert any(h.raw)
+    assert _lib.get_lib().lrk_shard_connect(ctx._dev.handle, h) == 0
+    fx = _fx("c4_sweep3d")
+    v = np.random.default_rng(3).standard_normal(grid.n_x)
+    _check_apply(ctx, v / np.linalg.norm(v), fx)

@@ -136,3 +136,42 @@ def test_shard_range_partitions():
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
+
+
+def _handle_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = bytes((17 * rank + i) % 256 for i in range(par.IPC_HANDLE_BYTES))
+        q.put((rank, par.exchange_handles(mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ipc_handle_exchange_is_rank_ordered():
+    """The setup step of the n_x-sharded sweeps: every rank's 64-byte CUDA IPC
+    handle (lrk_shard_setup) reaches every rank, concatenated in rank order,
+    which is what lrk_shard_connect indexes by peer rank."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_handle_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    want = b"".join(bytes((17 * r + i) % 256 for i in range(par.IPC_HANDLE_BYTES))
+                    for r in range(world))
+    assert res[0][1] == want and res[1][1] == want
+
+
+def test_shard_context_is_a_noop_without_a_process_group():
+    class _Ctx:
+        handle = None
+
+    assert par.shard_context(_Ctx()) == (0, 1)
