@@ -788,6 +788,15 @@ __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
   for (int64_t i = (int64_t)blockIdx.x * ST + threadIdx.x; i < a.n_x; i += (int64_t)gridDim.x * ST) {
     double acc[SF_P] = {0.0, 0.0, 0.0, 0.0};
     int j = 0;
+    for (; j + 16 <= rbe; j += 16) {  // 16 independent loads in flight per thread
+      double b[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) b[u] = a.B[i + (int64_t)(j + u) * a.ldb];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+#pragma unroll
+        for (int s = 0; s < SF_P; ++s) acc[s] += b[u] * w2s[(j + u) * SF_P + s];
+    }
     for (; j + 4 <= rbe; j += 4) {
       double b[4];
 #pragma unroll
