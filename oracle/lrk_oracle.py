@@ -89,6 +89,50 @@ def fd_operator(n_side: int, kind: str = "heat", nu: float = 1.0, wind=(0.0, 0.0
     return sp.csr_matrix(L), h, h * h
 
 
+def galerkin_q1_convection(n_side: int, w0=(0.0, 0.0), rotating: bool = False):
+    """Config C3 convection as specified (extension; unpinned by the reference,
+    which has first-order upwind only): Galerkin Q1,
+    N_ij = ∫ (w·∇φ_j) φ_i, wind at the element centres, assembled element by
+    element with explicit 2-point Gauss quadrature of the bilinear shape
+    functions (an independent route to the closed-form element matrix the
+    device generates on the fly).  Returns N / h² (lumped mass), x1 fastest."""
+    n = int(n_side)
+    h = 1.0 / (n + 1)
+    gp = 0.5 + np.array([-0.5, 0.5]) / np.sqrt(3.0)      # Gauss points on [0, 1]
+
+    def shape(a, t):                                   # 1-D hat on the unit element
+        return (1.0 - t, t)[a]
+
+    def dshape(a):
+        return (-1.0 / h, 1.0 / h)[a]
+
+    N = sp.lil_matrix((n * n, n * n))
+    for p2 in range(-1, n):
+        for p1 in range(-1, n):
+            xc, yc = h * (p1 + 1.5), h * (p2 + 1.5)
+            wx = w0[0] + (2 * yc * (1 - xc**2) if rotating else 0.0)
+            wy = w0[1] - (2 * xc * (1 - yc**2) if rotating else 0.0)
+            for a2 in (0, 1):
+                for a1 in (0, 1):
+                    i1, i2 = p1 + a1, p2 + a2
+                    if not (0 <= i1 < n and 0 <= i2 < n):
+                        continue
+                    for b2 in (0, 1):
+                        for b1 in (0, 1):
+                            j1, j2 = p1 + b1, p2 + b2
+                            if not (0 <= j1 < n and 0 <= j2 < n):
+                                continue
+                            acc = 0.0
+                            for s in gp:
+                                for t in gp:
+                                    phi_i = shape(a1, s) * shape(a2, t)
+                                    gx = dshape(b1) * shape(b2, t)
+                                    gy = shape(b1, s) * dshape(b2)
+                                    acc += 0.25 * h * h * phi_i * (wx * gx + wy * gy)
+                            N[i2 * n + i1, j2 * n + j1] += acc
+    return sp.csr_matrix(N) / h**2
+
+
 def config_operator(n_side: int, dim: int = 2, stencil: str = "fd", kind: str = "heat",
                     nu: float = 1.0, wind=(0.0, 0.0, 0.0), wind_field: str = "const"):
     """Config-extension operators (SURVEY §8(c) "Config features beyond the
@@ -99,6 +143,10 @@ def config_operator(n_side: int, dim: int = 2, stencil: str = "fd", kind: str = 
                     M1 = (h/6)tridiag(1,4,1) (Q1 stiffness, lumped mass h²);
       dim 3 "fd":   7-point nu·(-Δ) + first-order upwind per axis.
     Returns (L, h, m_scale) with x1 fastest."""
+    if kind != "heat" and stencil == "q1":
+        Kq, h, m = config_operator(n_side, 2, "q1", "heat")
+        conv = galerkin_q1_convection(n_side, tuple(wind)[:2], wind_field == "rotating")
+        return sp.csr_matrix(nu * Kq + conv), h, m
     if kind != "heat" and wind_field == "rotating":
         Ld, h, m = config_operator(n_side, dim, "fd", "heat")
         w3 = tuple(float(v) for v in (tuple(wind) + (0.0,) * 3)[:3])

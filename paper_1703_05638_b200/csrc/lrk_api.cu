@@ -257,8 +257,8 @@ StencilArgs make_stencil(const lrk_operator_desc& op, bool adjoint) {
   if (op.stencil == LRK_STENCIL_Q1) {
     // K_Q1 / h^2 with lumped mass: centre 8/3, all eight neighbours -1/3
     for (int d2 = -1; d2 <= 1; ++d2)
-      for (int d1 = -1; d1 <= 1; ++d1) cf(d1, d2, 0) = -ih2 / 3.0;
-    cf(0, 0, 0) = 8.0 * ih2 / 3.0;
+      for (int d1 = -1; d1 <= 1; ++d1) cf(d1, d2, 0) = -sc * ih2 / 3.0;
+    cf(0, 0, 0) = 8.0 * sc * ih2 / 3.0;
   } else {
     cf(0, 0, 0) = 2.0 * op.dim * sc * ih2;
     cf(-1, 0, 0) = cf(1, 0, 0) = cf(0, -1, 0) = cf(0, 1, 0) = -sc * ih2;
@@ -277,7 +277,10 @@ StencilArgs make_stencil(const lrk_operator_desc& op, bool adjoint) {
   if (adjoint)
     for (int k = 0; k < 13; ++k) std::swap(a.coef[k], a.coef[26 - k]);
   a.n = op.n_side; a.dim = op.dim; a.m_scale = op.m_scale; a.tau = op.tau;
-  a.wind_field = op.kind != LRK_OP_HEAT ? op.wind_field : 0;
+  const bool galerkin = op.kind != LRK_OP_HEAT && op.stencil == LRK_STENCIL_Q1;
+  a.wind_field = (op.kind != LRK_OP_HEAT && !galerkin) ? op.wind_field : 0;
+  a.galerkin = galerkin ? 1 : 0;     // Galerkin Q1 convection, wind at the element centres
+  a.rotating = galerkin && op.wind_field == LRK_WIND_ROTATING ? 1 : 0;
   a.adjoint = adjoint ? 1 : 0;
   a.w0[0] = op.wind[0]; a.w0[1] = op.wind[1]; a.w0[2] = op.wind[2];
   a.h = h;
@@ -1295,8 +1298,8 @@ int lrk_set_operator(lrk_ctx* c, const lrk_operator_desc* op) {
     return fail(c, LRK_ERR_CONFIG, "unknown stencil");
   if (op->wind_field != LRK_WIND_CONST && op->wind_field != LRK_WIND_ROTATING)
     return fail(c, LRK_ERR_CONFIG, "unknown wind field");
-  if (op->stencil == LRK_STENCIL_Q1 && (op->dim != 2 || op->kind != LRK_OP_HEAT))
-    return fail(c, LRK_ERR_UNSUPPORTED, "the Q1-lumped stencil is implemented for 2-D heat");
+  if (op->stencil == LRK_STENCIL_Q1 && op->dim != 2)
+    return fail(c, LRK_ERR_UNSUPPORTED, "the Q1 stencils are implemented in 2-D");
   if (op->n_side < 2 || op->n_t < 1 || !(op->tau > 0) || !(op->h > 0) || !(op->m_scale > 0))
     return fail(c, LRK_ERR_CONFIG, "invalid operator descriptor");
   const int n = op->n_side;

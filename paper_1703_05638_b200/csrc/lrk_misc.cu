@@ -51,6 +51,41 @@ __device__ __forceinline__ double var_upwind(const StencilArgs& a, const double*
   return acc;
 }
 
+// Galerkin Q1 convection row (or column, for the adjoint) at interior node
+// (i1, i2) from its 3 x 3 neighbourhood v[(d2+1)*3 + (d1+1)] (zero outside the
+// domain).  Element (p1, p2) spans nodes p..p+1 per axis (node -1 and n are
+// the Dirichlet boundary); with the wind (wx, wy) of its centre,
+//   N^e_ab = h [ wx (s_b1 / 2) m(a2, b2) + wy m(a1, b1) (s_b2 / 2) ],
+//   s_0 = -1, s_1 = +1, m(equal) = 1/3, m(different) = 1/6.
+// Returns (N v)_i / h^2 (lumped mass h^2), i.e. the term added to L v.
+__device__ __forceinline__ double galerkin_nb(const StencilArgs& a, int i1, int i2, const double (&v)[9]) {
+  double acc = 0.0;
+#pragma unroll
+  for (int e2 = 0; e2 < 2; ++e2)
+#pragma unroll
+    for (int e1 = 0; e1 < 2; ++e1) {
+      const int p1 = i1 - 1 + e1, p2 = i2 - 1 + e2;       // lower-left node of the element
+      const double xc = a.h * (p1 + 1.5), yc = a.h * (p2 + 1.5);
+      const double wx = a.w0[0] + (a.rotating ? 2.0 * yc * (1.0 - xc * xc) : 0.0);
+      const double wy = a.w0[1] - (a.rotating ? 2.0 * xc * (1.0 - yc * yc) : 0.0);
+      const int l1 = 1 - e1, l2 = 1 - e2;                 // local index of node i in the element
+#pragma unroll
+      for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+        for (int q1 = 0; q1 < 2; ++q1) {
+          // forward: a = (l1, l2) is the test node, b = (q1, q2); adjoint: swapped
+          const int a1 = a.adjoint ? q1 : l1, a2 = a.adjoint ? q2 : l2;
+          const int b1 = a.adjoint ? l1 : q1, b2 = a.adjoint ? l2 : q2;
+          const double m1 = a1 == b1 ? (1.0 / 3.0) : (1.0 / 6.0);
+          const double m2 = a2 == b2 ? (1.0 / 3.0) : (1.0 / 6.0);
+          const double ne = wx * (b1 ? 0.5 : -0.5) * m2 + wy * m1 * (b2 ? 0.5 : -0.5);
+          const int d1 = p1 + q1 - i1, d2 = p2 + q2 - i2;
+          acc += ne * v[(d2 + 1) * 3 + (d1 + 1)];
+        }
+    }
+  return acc / a.h;
+}
+
 __global__ void stencil_kernel(StencilArgs a) {
   const int c = blockIdx.y;
   const int n = a.n;
@@ -77,6 +112,17 @@ __global__ void stencil_kernel(StencilArgs a) {
     }
   }
   if (a.wind_field) lx += var_upwind(a, x, i, i1, i2, i3, plane);
+  if (a.galerkin) {
+    double v[9];
+#pragma unroll
+    for (int d2 = -1; d2 <= 1; ++d2)
+#pragma unroll
+      for (int d1 = -1; d1 <= 1; ++d1) {
+        const bool in = i1 + d1 >= 0 && i1 + d1 < n && i2 + d2 >= 0 && i2 + d2 < n;
+        v[(d2 + 1) * 3 + (d1 + 1)] = in ? x[i + d1 + (int64_t)d2 * n] : 0.0;
+      }
+    lx += galerkin_nb(a, i1, i2, v);
+  }
   const double sx = a.m_scale * (xc + a.tau * lx);
   a.Y[i + (int64_t)c * a.ldy] = a.Bres ? a.Bres[i + (int64_t)c * a.ldbres] - sx : sx;
   if (a.Ycopy) a.Ycopy[i + (int64_t)c * a.ldycopy] = a.copy_scale * xc;
@@ -219,8 +265,13 @@ __global__ void __launch_bounds__(256, WIND ? 3 : 4) stencil_march_kernel(Stenci
         xm[0] = p0[k - 1]; xp[0] = p0[k + 1];
         xm[1] = pm[k]; xp[1] = pp[k];
         xm[2] = 0.0; xp[2] = 0.0;
+        if (WIND && a.galerkin) {
+          const double v[9] = {pm[k - 1], pm[k], pm[k + 1], p0[k - 1], cur, p0[k + 1],
+                               pp[k - 1], pp[k], pp[k + 1]};
+          lx_acc += galerkin_nb(a, gx, gy, v);
+        }
       }
-      if (WIND) lx_acc += upwind_nb(a, gx, gy, cur, xm, xp);
+      if (WIND && a.wind_field) lx_acc += upwind_nb(a, gx, gy, cur, xm, xp);
       const double sx = a.m_scale * (cur + a.tau * lx_acc);
       const int64_t i = D == 3 ? (int64_t)z * pstride + (int64_t)gy * n + gx
                                : (int64_t)gy * n + gx;
@@ -237,7 +288,7 @@ static void launch_march_mz(const StencilArgs& a, cudaStream_t s) {
   const int n = a.n;
   const int nzb = (n + MZ - 1) / MZ;
   dim3 grid((n + TX - 1) / TX, D == 3 ? (n + TY - 1) / TY : 1, nzb * a.ncols);
-  if (a.wind_field)
+  if (a.wind_field || a.galerkin)
     stencil_march_kernel<D, true, MZ><<<grid, 256, 0, s>>>(a, nzb);
   else
     stencil_march_kernel<D, false, MZ><<<grid, 256, 0, s>>>(a, nzb);

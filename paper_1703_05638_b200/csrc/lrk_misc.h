@@ -20,6 +20,12 @@ struct StencilArgs {
   // variable wind (wind_field = 1): per-node upwind of w = w0 + rotating field,
   // added on top of coef (which then holds the diffusion part only)
   int wind_field;
+  // Galerkin Q1 convection (config C3, SUPG delta_k = 0 at
+  // element Peclet < 1): N_ij = int (w . grad phi_j) phi_i with the wind taken
+  // at the element centres (w0, plus the rotating field when `rotating`),
+  // lumped mass; coef then holds nu K_Q1 / h^2
+  int galerkin;
+  int rotating;
   int adjoint;
   double w0[3];
   double h;

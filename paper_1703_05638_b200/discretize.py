@@ -198,14 +198,60 @@ def _upwind_field(grid: Grid, W) -> sp.csr_matrix:
                          shape=(N, N))
 
 
-def assemble_convdiff(grid: Grid, nu: float, wind, field: str = "const") -> SpatialOperator:
+def _galerkin_q1_convection(grid: Grid, w0, rotating: bool) -> sp.csr_matrix:
+    """Galerkin Q1 convection N_ij = ∫ (w·∇φ_j) φ_i on the uniform grid, the wind
+    taken at the element centres (w0, plus the rotating field of config C3),
+    divided by the lumped mass h².  Per element with
+    lower-left node p and local nodes a, b in {0,1}²:
+    N^e_ab = h [ w_x (s_b1/2) m(a2,b2) + w_y m(a1,b1) (s_b2/2) ], s = (-1, +1),
+    m(equal) = 1/3, m(different) = 1/6."""
+    n, h = grid.n_side, grid.h
+    p = np.arange(-1, n)
+    p1, p2 = np.meshgrid(p, p, indexing="xy")      # p1 along axis 1 (x1 fastest when flattened)
+    xc, yc = h * (p1 + 1.5), h * (p2 + 1.5)
+    wx = w0[0] + (2 * yc * (1 - xc**2) if rotating else 0.0) + 0.0 * xc
+    wy = w0[1] - (2 * xc * (1 - yc**2) if rotating else 0.0) + 0.0 * xc
+    rows, cols, vals = [], [], []
+    for a2 in (0, 1):
+        for a1 in (0, 1):
+            for b2 in (0, 1):
+                for b1 in (0, 1):
+                    m1 = 1 / 3 if a1 == b1 else 1 / 6
+                    m2 = 1 / 3 if a2 == b2 else 1 / 6
+                    ne = h * (wx * (0.5 if b1 else -0.5) * m2 + wy * m1 * (0.5 if b2 else -0.5))
+                    ia1, ia2, ib1, ib2 = p1 + a1, p2 + a2, p1 + b1, p2 + b2
+                    ok = ((ia1 >= 0) & (ia1 < n) & (ia2 >= 0) & (ia2 < n)
+                          & (ib1 >= 0) & (ib1 < n) & (ib2 >= 0) & (ib2 < n))
+                    rows.append((ia2 * n + ia1)[ok])
+                    cols.append((ib2 * n + ib1)[ok])
+                    vals.append(ne[ok])
+    N = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(grid.n_x, grid.n_x))
+    return N / h**2
+
+
+def assemble_convdiff(grid: Grid, nu: float, wind, field: str = "const",
+                      scheme: str = "upwind") -> SpatialOperator:
     """-nu Δ + w·∇ with first-order upwind (discretize.py:115-127).  field
     "rotating" (config extension) adds the C3/C5 rotating field to `wind` and
-    upwinds node by node."""
+    upwinds node by node.  scheme "galerkin" (config C3 as specified, SURVEY
+    Appendix D3: Q1 FEM whose SUPG parameter vanishes because the element
+    Péclet number |w| h / (2 nu) is below one) is the 2-D Q1 stiffness plus the
+    Galerkin Q1 convection matrix, lumped mass."""
     if nu <= 0:
         raise InvalidConfigError(f"viscosity nu must be positive, got {nu}")
     if field not in ("const", "rotating"):
         raise InvalidConfigError(f"unknown wind field {field!r}")
+    if scheme not in ("upwind", "galerkin"):
+        raise InvalidConfigError(f"unknown convection scheme {scheme!r}")
+    if scheme == "galerkin":
+        if grid.d != 2:
+            raise InvalidConfigError("the Galerkin Q1 operator is 2-D")
+        w2 = (float(wind[0]), float(wind[1]))
+        L = sp.csr_matrix(float(nu) * _assemble_q1(grid)
+                          + _galerkin_q1_convection(grid, w2, field == "rotating"))
+        return SpatialOperator(kind="convdiff", grid=grid, L=L, nu=float(nu), wind=w2,
+                               stencil="q1", wind_field=field)
     if field == "rotating":
         w3 = tuple(float(x) for x in (tuple(wind) + (0.0,) * 3)[:3])
         lap = _assemble_3d(grid, float(nu)) if grid.d == 3 else \

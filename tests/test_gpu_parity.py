@@ -105,7 +105,7 @@ def test_stencil_apply_is_the_dense_operator():
         K = lp.SpaceTimeOperator(op, lp.build_time_grid(5))
         Y = lp.LowRankMat(rng.standard_normal((op.grid.n_x, 3)), rng.standard_normal((5, 3)))
         Yd = _dense(Y)
-        A = K.step_matrix.toarray()
+        A = K.step_matrix
         ref = A @ Yd
         ref[:, 1:] -= op.grid.m_scale * Yd[:, :-1]
         assert np.abs(_dense(K.apply(Y)) - ref).max() < 1e-12 * np.abs(ref).max()
@@ -424,11 +424,16 @@ def test_config_stencil_apply_is_the_dense_operator():
                lp.assemble_convdiff(lp.build_grid(5, 3), 0.02, (0.5, -1.0, 0.25)),
                lp.assemble_convdiff(lp.build_grid(8), 0.05, (0.0, 0.0), field="rotating"),
                lp.assemble_convdiff(lp.build_grid(5, 3), 0.02, (0.577, 0.577, 0.577),
-                                    field="rotating")):
+                                    field="rotating"),
+               lp.assemble_convdiff(lp.build_grid(9), 0.05, (0.7, -1.3), scheme="galerkin"),
+               lp.assemble_convdiff(lp.build_grid(300), 0.05, (0.1, 0.0), field="rotating",
+                                    scheme="galerkin"),
+               lp.assemble_convdiff(lp.build_grid(11), 0.05, (0.0, 0.0), field="rotating",
+                                    scheme="galerkin")):
         K = lp.SpaceTimeOperator(op, lp.build_time_grid(4))
         Y = lp.LowRankMat(rng.standard_normal((op.grid.n_x, 2)), rng.standard_normal((4, 2)))
         Yd = _dense(Y)
-        A = K.step_matrix.toarray()
+        A = K.step_matrix
         ref = A @ Yd
         ref[:, 1:] -= op.grid.m_scale * Yd[:, :-1]
         assert np.abs(_dense(K.apply(Y)) - ref).max() < 1e-12 * np.abs(ref).max()
@@ -752,3 +757,35 @@ def test_sweep_rank_cap_vs_oracle(rmax):
     assert tr == tr_ref and max(tr) <= rmax
     ref = Y1 @ Y2.T
     assert np.linalg.norm(_dense(Y) - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+def test_galerkin_q1_convdiff_c3_operator_vs_oracle():
+    """Config C3 as specified: Galerkin Q1 convection-
+    diffusion, nu = 1/20, rotating wind (element Peclet < 1, so the SUPG term
+    vanishes), lumped mass, (I + 0.05 L)^-1 prior, point-sensor subgrid: step
+    solves (S and S^T) against SuperLU on the oracle's independently assembled
+    matrix, and one IC Hessian apply against the oracle with its rank."""
+    n_side, n_t = 24, 16
+    grid = lp.build_grid(n_side)
+    op = lp.assemble_convdiff(grid, 1 / 20, (0.0, 0.0), field="rotating", scheme="galerkin")
+    K = lp.SpaceTimeOperator(op, lp.build_time_grid(n_t))
+    L, h, m = O.config_operator(n_side, 2, "q1", "convdiff", 1 / 20, (0.0, 0.0), "rotating")
+    assert abs(L - op.L).max() < 1e-12 * abs(L).max()
+    solver = O.StepSolver(L, m, 1.0 / n_t, n_t)
+    B = np.random.default_rng(41).standard_normal((grid.n_x, 3))
+    for adj in (False, True):
+        ref = solver.solve(B, adjoint=adj)
+        out = K.solve_step(B, adjoint=adj)
+        assert np.linalg.norm(out - ref) <= 1e-11 * np.linalg.norm(ref)
+    bn = 1.0 / (0.01**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    layout = lp.make_sensor_subgrid(grid, 6)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                            pol=lp.TruncationPolicy(1e-8, 48))
+    P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, 48, kind="convdiff", nu=1 / 20,
+                  wind=(0.0, 0.0), stencil="q1", prior=(1.0, 0.05), wind_field="rotating")
+    v = np.random.default_rng(42).standard_normal(grid.n_x)
+    ref, rank = O.hessian_ic(P, v)
+    got = ctx.apply(v)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert ctx.rank_trace[-1] == rank

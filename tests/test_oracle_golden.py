@@ -179,3 +179,29 @@ def test_rank_cut_semantics():
     assert O.rank_cut(np.array([1.0, 0.5, 0.1]), 1e-8, r_max=2) == 2
     assert O.rank_cut(np.zeros(3), 1e-8) == 0
     assert O.rank_cut(np.array([1.0, 1e-16]), 1e-20) == 1  # noise floor
+
+
+def test_galerkin_q1_convection_assembly():
+    """Config C3 operator (extension): the product's
+    vectorised closed-form element matrices, the oracle's Gauss-quadrature
+    assembly, and (constant wind) the Kronecker closed form
+    N = w1 M1 (x) C1 + w2 C1 (x) M1 agree."""
+    import scipy.sparse as sp
+
+    import paper_1703_05638_b200 as lp
+
+    n = 7
+    g = lp.build_grid(n)
+    for field, w in (("const", (0.7, -1.3)), ("rotating", (0.0, 0.0)), ("rotating", (0.3, 0.2))):
+        A = lp.assemble_convdiff(g, 0.05, w, field=field, scheme="galerkin").L
+        B, h, m = O.config_operator(n, 2, "q1", "convdiff", 0.05, w, field)
+        assert abs(A - B).max() < 1e-13 * abs(A).max()
+        assert m == h * h
+    h, one, w = g.h, np.ones(n), (0.7, -1.3)
+    C1 = sp.diags([-one[1:], one[1:]], [-1, 1]) * 0.5
+    M1 = sp.diags([one[1:], 4 * one, one[1:]], [-1, 0, 1]) * (h / 6)
+    N = (w[0] * sp.kron(M1, C1) + w[1] * sp.kron(C1, M1)) / h**2
+    A = lp.assemble_convdiff(g, 0.05, w, scheme="galerkin").L - 0.05 * lp.assemble_heat(g, "q1").L
+    assert abs(A - N).max() < 1e-13 * abs(N).max()
+    # element Peclet number of config C3 (nu = 1/20, n_side 512, |w| <= 2): SUPG inactive
+    assert 2.0 * (1.0 / 513) / (2 * (1 / 20)) < 1.0

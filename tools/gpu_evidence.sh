@@ -1,0 +1,29 @@
+#!/bin/bash
+# Round-end evidence set on one B200: tests, bench lines, ncu launch list and full captures,
+# DRAM traffic of one apply, DMMA pipe counters, DGEMM peak, compute-sanitizer logs.
+set -x
+TAG=${1:-r02h}
+O=gpurun_out
+mkdir -p $O
+python -m pytest tests -m gpu -x -q > $O/${TAG}_gputest.log 2>&1; echo "pytest rc=$?" >> $O/${TAG}_gputest.log
+python bench.py --steps 5 --warmup 3 > $O/${TAG}_bench_c4.json 2> $O/${TAG}_bench_c4.err
+python bench.py --steps 10 --warmup 3 --config C2 > $O/${TAG}_bench_c2.json 2> $O/${TAG}_bench_c2.err
+python bench.py --impl reference --steps 2 --warmup 1 > $O/${TAG}_bench_ref_c4.json 2> $O/${TAG}_bench_ref_c4.err
+python tools/dgemm_peak.py > $O/${TAG}_dgemm_peak.txt 2>&1
+python tools/hbm_roofline.py > $O/${TAG}_streaming_kernels.jsonl 2>&1
+# launch list of the bench command (first 7000 launches: setup + the first apply)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 7000 --csv --log-file $O/${TAG}_launches_bench_c4.csv \
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/${TAG}_ncu_bench.log 2>&1
+# DRAM traffic + time of every launch of one full C4 apply
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  --log-file $O/${TAG}_traffic_c4_apply.csv python tools/c4_probe.py 128 2048 1 > $O/${TAG}_ncu_traffic.log 2>&1
+# full captures of pass A / pass B in the adjoint sweep at full size (rank ~35-40)
+ncu --set full --clock-control none --import-source on -k regex:sf_pass --launch-skip 1600 --launch-count 2 \
+  -f -o $O/${TAG}_ncu_sf_pass python tools/c4_probe.py 128 2048 1 > $O/${TAG}_ncu_sf_pass.log 2>&1
+# which counters see the FP64 tensor pipe
+ncu --query-metrics 2>/dev/null | grep -i -E "dmma|pipe_fp64|pipe_tensor" > $O/${TAG}_metric_names.txt
+for t in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $t python tools/sanitize_small.py > $O/${TAG}_sanitizer_$t.log 2>&1
+  echo "rc=$?" >> $O/${TAG}_sanitizer_$t.log
+done
+tail -3 $O/${TAG}_gputest.log
