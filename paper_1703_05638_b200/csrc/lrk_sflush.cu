@@ -50,7 +50,7 @@ namespace lrk {
 namespace {
 
 constexpr int ST = 256;           // threads per CTA of the light passes
-constexpr int NW = 16;            // warps of the staged row passes
+constexpr int NW = 20;            // warps of the staged row passes (96 registers per thread)
 constexpr int SPT = 32 * NW;
 constexpr int LDW = 68;           // shared leading dimension of the update matrix (== 4 mod 16)
 static_assert(LDW == SF_LDW, "pass_b_tail reads the shared and the global update matrix alike");
@@ -484,6 +484,7 @@ __device__ __forceinline__ void pass_b_tail(const SFArgs& a, SFState* st, const 
 // Runtime sizes and pointers of one pass (uniform over the CTA).
 struct PassRt {
   int r, pcp, n, pcn, rn, nwc, ncol, per_warp;
+  int nwa;  // warps that stream tiles (all NW unless the rank is so high that two slots per warp need more room)
   int64_t ct0, ct1;
   double *Yab, *Ynb, *W, *ring;
   const unsigned long long* colp;  // shared: base address of every staged column
@@ -534,15 +535,17 @@ __device__ __forceinline__ void pass_loop(const SFArgs& a, const PassRt& P, doub
 #pragma unroll
   for (int j = 0; j < NT; ++j) m[j][0] = m[j][1] = 0.0;
   double ysq = 0.0;
-  const int64_t first = P.ct0 + warp;
+  const int nwa = P.nwa;
+  // (warps past nwa own no tiles: their loop below is empty)
+  const int64_t first = warp < nwa ? P.ct0 + warp : P.ct1;
   for (int q = 0; q < depth - 1; ++q) {
-    const int64_t tq = first + (int64_t)q * NW;
+    const int64_t tq = first + (int64_t)q * nwa;
     issue(q, tq, tq < P.ct1);
   }
   int cur = 0, nxt = depth - 1;
-  for (int64_t tile = first; tile < P.ct1; tile += NW) {
+  for (int64_t tile = first; tile < P.ct1; tile += nwa) {
     {
-      const int64_t tq = tile + (int64_t)(depth - 1) * NW;
+      const int64_t tq = tile + (int64_t)(depth - 1) * nwa;
       issue(nxt, tq, tq < P.ct1);
     }
     cp_wait_dyn(depth - 1);
@@ -685,7 +688,11 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f, unsigne
   PassRt P;
   P.r = r; P.pcp = pcp; P.n = n; P.pcn = pcn; P.rn = rn; P.nwc = nwc; P.ncol = ncol;
   cta_tiles(a.n_x, P.ct0, P.ct1);
-  P.Yab = Yab; P.Ynb = Ynb; P.W = W; P.ring = stage; P.per_warp = ((avail - 128) / NW) & ~1;  /* headroom: padded fragment loops read up to 7 columns past a slot */ P.colp = colp;
+  P.Yab = Yab; P.Ynb = Ynb; P.W = W; P.ring = stage; P.colp = colp;
+  // two ring slots per streaming warp must fit (headroom: the padded fragment
+  // loops read up to 7 columns past a slot)
+  P.nwa = min(NW, max(1, (avail - 128) / (2 * (ncol > 0 ? ncol : 1) * LDT)));
+  P.per_warp = ((avail - 128) / P.nwa) & ~1;
   double m[9][2];  // T tile j = X columns 8j..8j+7
 #pragma unroll
   for (int j = 0; j < 9; ++j) m[j][0] = m[j][1] = 0.0;

@@ -327,3 +327,26 @@ def test_shard_arena_world_one_c4_path_vs_reference():
     fx = _fx("c4_sweep3d")
     v = np.random.default_rng(3).standard_normal(grid.n_x)
     _check_apply(ctx, v / np.linalg.norm(v), fx)
+
+
+def test_streaming_flush_at_the_rank_cap_matches_persistent(monkeypatch):
+    """Pane ranks up to the 64-column cap (72 staged columns per tile: the
+    passes then stream with fewer warps so that two ring slots per warp still
+    fit): the streaming-flush sweep against the persistent kernel on a
+    full-rank forcing — identical rank traces, values to rounding."""
+    rng = np.random.default_rng(77)
+    n_side, n_t = 48, 96
+    grid = lp.build_grid(n_side)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid), lp.build_time_grid(n_t))
+    rhs = lp.LowRankMat(rng.standard_normal((grid.n_x, 40)), rng.standard_normal((n_t, 40)))
+    pol = lp.TruncationPolicy(1e-13, 64)
+    out = {}
+    for form in ("0", "1"):
+        monkeypatch.setenv("LRK_SFLUSH", form)
+        tr = []
+        Y = lp.st_solve_sweep(K, rhs, pol, trace=tr)
+        out[form] = (tr, (Y.W1 @ Y.W2.T).cpu().numpy())
+    assert max(out["1"][0]) == 64, out["1"][0]
+    assert out["0"][0] == out["1"][0]
+    ref = out["0"][1]
+    assert np.abs(out["1"][1] - ref).max() <= 1e-10 * np.abs(ref).max()
