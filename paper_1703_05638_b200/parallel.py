@@ -100,10 +100,25 @@ def exchange_handles(mine: bytes, group=None, device=None) -> bytes:
     return b"".join(bytes(p.cpu().tolist()) for p in parts)
 
 
+def _all_ranks_ok(ok: bool, group=None, device=None) -> bool:
+    """True when `ok` holds on every rank (one small MIN all-reduce): every
+    rank learns about a failure anywhere, so nobody is left waiting in the
+    next collective."""
+    import torch
+    import torch.distributed as dist
+
+    if device is None:
+        device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([1.0 if ok else 0.0], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item() == 1.0)
+
+
 def shard_context(dev_ctx, group=None, device=None) -> tuple[int, int]:
     """Shard the sweeps of `dev_ctx` (a _lib.Context with its operator
     installed) by n_x rows across the ranks of `group`.  Returns (rank, world).
-    With a world of one this is a no-op."""
+    With a world of one this is a no-op.  Collective: every rank must call it;
+    a failure on any rank raises RuntimeError on all of them."""
     import ctypes
 
     import torch.distributed as dist
@@ -117,10 +132,14 @@ def shard_context(dev_ctx, group=None, device=None) -> tuple[int, int]:
         return 0, 1
     lib = _lib.get_lib()
     h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
-    _lib.check(lib.lrk_shard_setup(dev_ctx.handle, rank, world, h), dev_ctx.handle,
-               "shard_context")
+    st = lib.lrk_shard_setup(dev_ctx.handle, rank, world, h)
+    msg = lib.lrk_last_error(dev_ctx.handle).decode() if st else ""
+    if not _all_ranks_ok(st == 0, group, device):
+        raise RuntimeError(f"lrk_shard_setup failed on a rank (here: status {st} {msg})")
     handles = exchange_handles(h.raw, group=group, device=device)
     buf = ctypes.create_string_buffer(handles, len(handles))
-    _lib.check(lib.lrk_shard_connect(dev_ctx.handle, buf), dev_ctx.handle, "shard_context")
-    dist.barrier(group=group)
+    st = lib.lrk_shard_connect(dev_ctx.handle, buf)
+    msg = lib.lrk_last_error(dev_ctx.handle).decode() if st else ""
+    if not _all_ranks_ok(st == 0, group, device):
+        raise RuntimeError(f"lrk_shard_connect failed on a rank (here: status {st} {msg})")
     return rank, world

@@ -145,7 +145,11 @@ def _handle_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         mine = bytes((17 * rank + i) % 256 for i in range(par.IPC_HANDLE_BYTES))
-        q.put((rank, par.exchange_handles(mine)))
+        got = par.exchange_handles(mine)
+        # a failure on ONE rank is seen by every rank (no rank left in a collective)
+        assert par._all_ranks_ok(True) is True
+        assert par._all_ranks_ok(rank != 1) is False
+        q.put((rank, got))
     finally:
         dist.destroy_process_group()
 
