@@ -157,7 +157,16 @@ def exported_symbols():
     return list(_SIGNATURES)
 
 
+_cuda_seen = False
+
+
 def require_cuda():
+    """Fail loudly without a GPU.  torch.cuda.is_available() costs milliseconds
+    (an NVML query) and sits on the per-apply path, so a positive answer is
+    remembered; a negative one is re-checked every time."""
+    global _cuda_seen
+    if _cuda_seen:
+        return
     import torch
 
     if not torch.cuda.is_available():
@@ -165,6 +174,7 @@ def require_cuda():
             "paper_1703_05638_b200 runs its hot path on a CUDA device (B200, sm_100a); "
             "no GPU is visible and there is no CPU fallback"
         )
+    _cuda_seen = True
 
 
 def stream_handle():

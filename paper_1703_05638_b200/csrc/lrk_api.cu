@@ -1732,9 +1732,13 @@ int lrk_cgs2(lrk_ctx* c, const double* Q, int64_t ldq, int k, double* w, int n, 
   cudaStream_t s = (cudaStream_t)stream;
   const int g = grid1(n, 4096, 2 * c->num_sms);
   const int kk = std::max(k, 1);
-  WS(double, part, "cg_part", (int64_t)g * kk);
-  WS(double, hp, "cg_h", kk);
-  WS(double, hacc, "cg_hacc", kk + 1);
+  // the basis grows by one column per Arnoldi step: size the workspace in
+  // powers of two so that it is reallocated O(log k) times, not every call
+  int kcap = 64;
+  while (kcap < kk) kcap *= 2;
+  WS(double, part, "cg_part", (int64_t)g * kcap);
+  WS(double, hp, "cg_h", kcap);
+  WS(double, hacc, "cg_hacc", kcap + 1);
   CK(cudaMemsetAsync(hacc, 0, (kk + 1) * sizeof(double), s));
   for (int pass = 0; pass < 2 && k > 0; ++pass) {
     launch_gram(Q, ldq, k, w, n, 1, n, part, g, s);

@@ -99,40 +99,6 @@ constexpr int LDT = 8;        // rows per tile = leading dimension of a staged c
 __device__ __forceinline__ int swz(int c) { return (c & 2) << 1; }
 constexpr int MAXDEPTH = 15;  // (cp_wait_dyn covers depth - 1 <= 14)
 
-struct WRing {
-  double* base;  // this warp's region
-  int slot;      // doubles per tile (ncols * LDT)
-  int depth;
-};
-
-__device__ __forceinline__ WRing wring(double* region, int per_warp, int ncols) {
-  WRing R;
-  R.base = region + (int64_t)(threadIdx.x >> 5) * per_warp;
-  R.slot = (ncols > 0 ? ncols : 1) * LDT;
-  R.depth = per_warp / R.slot;
-  R.depth = R.depth < 2 ? 2 : (R.depth > MAXDEPTH ? MAXDEPTH : R.depth);
-  return R;
-}
-
-// Copy tile `tile` (rows tile*8 .. +8) of ncols columns into slot `sl`; every
-// lane commits one group (possibly empty) so the group counts stay aligned.
-template <typename ColFn>
-__device__ __forceinline__ void wring_issue(const WRing& R, int sl, int64_t tile, bool valid, int ncols,
-                                            ColFn src, int64_t n_x) {
-  if (valid) {
-    const int lane = threadIdx.x & 31;
-    double* dst = R.base + (int64_t)sl * R.slot;
-    const int64_t r0 = tile * LDT;
-    for (int q = lane; q < ncols * 4; q += 32) {
-      const int c = q >> 2, j = q & 3;
-      const int64_t row = r0 + 2 * j;
-      const bool ok = row < n_x;
-      cp16(dst + c * LDT + 2 * (j ^ (c & 2)), src(c) + (ok ? row : 0), ok);
-    }
-  }
-  cp_commit();
-}
-
 // Tiles of this CTA: a contiguous range [t0, t1) of the 8-row tile grid;
 // warp w takes tiles t0 + w, t0 + w + NW, ...
 __device__ __forceinline__ void cta_tiles(int64_t n_x, int64_t& t0, int64_t& t1) {
