@@ -436,6 +436,12 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
         CK(cudaEventCreateWithFlags(&c->aux.ready, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->aux.done, cudaEventDisableTiming));
       }
+      long long* sfdbg = nullptr;
+      if (std::getenv("LRK_SF_TIMING")) {
+        WS(long long, d, "sf_dbg", 32);
+        CK(cudaMemsetAsync(d, 0, 32 * sizeof(long long), s));
+        sfdbg = d;
+      }
       std::vector<SFArgs> sh(nlocal);
       int64_t my_x0 = 0, my_rows = nx;
       for (int l = 0; l < nlocal; ++l) {
@@ -464,6 +470,7 @@ int run_sweep(lrk_ctx* c, const std::string& tag, const double* B, int64_t ldb, 
         sa.G = Gs; sa.Ggen = 8 * c->num_sms;
         sa.dbg_print = std::getenv("LRK_SF_DEBUG") ? std::atoi(std::getenv("LRK_SF_DEBUG")) : 0;
         sa.smem_pass = (int)sf_smem_pass();
+        sa.dbg = sfdbg;
       }
       if (c->prof) CK(cudaEventRecord(c->ev[2 * slot], s));
       CK(launch_sweep_stream(sh.data(), nlocal, nflush, s, c->aux, &c->xseq, &c->launches));

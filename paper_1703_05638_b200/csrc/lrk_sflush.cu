@@ -143,33 +143,37 @@ __device__ __forceinline__ bool last_cta(unsigned* ticket, int* flag) {
   return *flag != 0;
 }
 
-// out[e] = sum over CTAs of part[c * PSTR + e], e < len: one warp per pair of
-// entries, lanes stride over the CTAs with 16 independent loads in flight,
-// then a fixed tree — deterministic.
-__device__ __forceinline__ void reduce_parts(const double* part, int len, double* out) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// out[e] = sum over CTAs of part[c * PSTR + e], e < len.  The gather runs on
+// ONE SM, whose rate of distinct sector requests is the limit (a lane-per-CTA
+// layout asked for one sector per 8 bytes: 26k cycles per pass), so lanes
+// take consecutive entries (coalesced) and RG thread groups split the CTAs:
+// group g adds c = g, g + RG, ... in increasing order with 8 loads in flight,
+// the RG group sums meet in shared memory and are added in a fixed tree —
+// deterministic.  scr: RG * len doubles of shared scratch.
+constexpr int RG = 8;
+__device__ __forceinline__ void reduce_parts(const double* part, int len, double* out, double* scr) {
   const int G = (int)gridDim.x;
-  for (int e = 2 * w; e < len; e += 2 * nw) {
-    const bool two = e + 1 < len;
-    double a0 = 0.0, a1 = 0.0;
-    for (int c0 = 0; c0 < G; c0 += 256) {
-      double v[8], u[8];
+  for (int idx = threadIdx.x; idx < len * RG; idx += blockDim.x) {
+    const int e = idx % len, g = idx / len;
+    const double* p = part + e;
+    double acc = 0.0;
+    int c = g;
+    for (; c + 7 * RG < G; c += 8 * RG) {
+      double v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = c0 + lane + 32 * i;
-        const bool ok = c < G;
-        v[i] = ok ? __ldcg(part + (int64_t)c * PSTR + e) : 0.0;
-        u[i] = (ok && two) ? __ldcg(part + (int64_t)c * PSTR + e + 1) : 0.0;
-      }
-      a0 += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
-      a1 += ((u[0] + u[1]) + (u[2] + u[3])) + ((u[4] + u[5]) + (u[6] + u[7]));
+      for (int i = 0; i < 8; ++i) v[i] = __ldcg(p + (int64_t)(c + i * RG) * PSTR);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += v[i];
     }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    if (lane == 0) {
-      out[e] = a0;
-      if (two) out[e + 1] = a1;
-    }
+    for (; c < G; c += RG) acc += __ldcg(p + (int64_t)c * PSTR);
+    scr[g * len + e] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < len; e += blockDim.x) {
+    double v[RG];
+#pragma unroll
+    for (int g = 0; g < RG; ++g) v[g] = scr[g * len + e];
+    out[e] = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
   }
   __syncthreads();
 }
@@ -265,6 +269,7 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
   int kept = 0;
   bool stop = false;
   double d0 = 0.0;
+  double iL[4] = {0.0, 0.0, 0.0, 0.0};  // 1 / L[k][k]
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (k >= n || stop) continue;
@@ -289,10 +294,11 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
     const double d = A[k][k];
     if (k == 0) d0 = d;
     if (!(d > tol * d0) || !(d > 0.0)) { stop = true; continue; }
-    const double l = sqrt(d);
-    L[k][k] = l;
+    const double il = rsqrt_fast(d);  // Newton-refined MUFU reciprocal square root (a few ulp)
+    L[k][k] = d * il;
+    iL[k] = il;
 #pragma unroll
-    for (int i = k + 1; i < 4; ++i) L[i][k] = (i < n) ? A[i][k] / l : 0.0;
+    for (int i = k + 1; i < 4; ++i) L[i][k] = (i < n) ? A[i][k] * il : 0.0;
 #pragma unroll
     for (int i = k + 1; i < 4; ++i)
 #pragma unroll
@@ -308,7 +314,7 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     if (i >= kept) continue;
-    Li[i][i] = 1.0 / L[i][i];
+    Li[i][i] = iL[i];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (j >= i) continue;
@@ -316,7 +322,7 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         if (q >= j && q < i) s += L[i][q] * Li[q][j];
-      Li[i][j] = -s / L[i][i];
+      Li[i][j] = -s * iL[i];
     }
   }
   // R[a][c] = L[j][a] with perm[j] == c (j >= a); Z[c][a] = Li[a][j] with perm[j] == c
@@ -339,28 +345,32 @@ __device__ __forceinline__ int pivoted_chol4(const double* G, int n, double tol,
 
 }  // namespace
 
-// Tail of pass A (thread 0): the shifted Cholesky factor of G0 = y2^T y2
-// (Fukaya et al. shifted CholeskyQR3, first step); a remainder at the block's
-// rounding floor 16 eps ||Y|| is dropped whole.  G0 is row-major with stride 4.
-// Out of line: keeps the streaming kernel's register count low.
-static __device__ __noinline__ void sf_shifted_chol(const SFArgs& a, SFState* st, const double* G0,
-                                                    int pc) {
+// Start of the first CholeskyQR pass (thread 0 of EVERY CTA, redundantly: the
+// code stays hot in the instruction caches of all SMs, whereas in the tail of
+// pass A — once per launch on whichever SM finished last — the same ~1,500
+// instructions took 28k cycles of cold instruction fetch): the shifted
+// Cholesky factor of G0 = y2^T y2 (Fukaya et al. shifted CholeskyQR3, first
+// step); a remainder at the block's rounding floor 16 eps ||Y|| is dropped
+// whole.  G0 row-major with stride 4.  Returns drop_all; R, Z: 16 doubles each.
+static __device__ __noinline__ int sf_shifted_chol(int64_t n_x_glob, const double* G0, const double* yn,
+                                                   int pc, double* R, double* Z) {
   double G[16] = {};
   for (int u = 0; u < pc; ++u)
     for (int v = 0; v < pc; ++v) G[u * 4 + v] = G0[u * 4 + v];
   double tr = 0.0, ysq = 0.0;
-  for (int s = 0; s < pc; ++s) { tr += G[s * 5]; ysq += st->yn[s]; }
+  for (int s = 0; s < pc; ++s) { tr += G[s * 5]; ysq += yn[s]; }
   const double delta = 16.0 * DEPS * sqrt(ysq);
-  st->drop_all = !(sqrt(tr) > delta);
+  const int drop = !(sqrt(tr) > delta);
   double Rm[16], Zm[16];
-  if (st->drop_all) {
+  if (drop) {
     for (int i = 0; i < 16; ++i) { Rm[i] = 0.0; Zm[i] = 0.0; }
   } else {
-    const double shift = 11.0 * ((double)a.n_x_glob * pc + pc * (pc + 1)) * DEPS * tr;
+    const double shift = 11.0 * ((double)n_x_glob * pc + pc * (pc + 1)) * DEPS * tr;
     for (int s = 0; s < pc; ++s) G[s * 5] += shift;
     pivoted_chol4(G, pc, 0.0, Rm, Zm);
   }
-  for (int i = 0; i < 16; ++i) { st->Rc[i] = Rm[i]; st->Rinv[i] = Zm[i]; }
+  for (int i = 0; i < 16; ++i) { R[i] = Rm[i]; Z[i] = Zm[i]; }
+  return drop;
 }
 
 // CholeskyQR pass tail (thread 0): R <- chol(G) R, Rinv <- Rinv chol(G)^{-1};
@@ -408,7 +418,7 @@ __device__ __forceinline__ void pass_a_tail(const SFArgs& a, SFState* st, const 
   if (tid == 0) {
     st->pc_new = pcn;
     if (pcp > 0) {
-      sf_shifted_chol(a, st, tot + n * SF_P, pcp);
+      for (int i = 0; i < 16; ++i) st->G0[i] = tot[n * SF_P + i];  // shifted Cholesky: first CholeskyQR pass
     } else {
       // nothing to close (first flush): no sf_finish will run before pass B
       for (int s2 = 0; s2 < SF_P; ++s2) st->yn[s2] = tot[n * SF_P + 16 + s2];
@@ -583,6 +593,7 @@ template <int MODE>
 __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f, unsigned long long seq) {
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long colp[SF_N + SF_P + 8];
+  const long long tstart = a.dbg ? clock64() : 0;
   SFState* st = a.st;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -709,15 +720,26 @@ __global__ void __launch_bounds__(SPT, 1) sf_pass(const SFArgs a, int f, unsigne
       part[e] = acc;
     }
   }
+  const long long tq0 = a.dbg ? clock64() : 0;
   if (!last_cta(a.ticket + MODE, flag)) return;
+  const long long tq1 = a.dbg ? clock64() : 0;
   double* tot = red + NW * PSTR + 64;
-  reduce_parts(a.part, plen, tot);
+  reduce_parts(a.part, plen, tot, tot + PSTR + 8);
+  const long long tq2 = a.dbg ? clock64() : 0;
   if (a.nshard > 1) {  // the tail runs in sf_tail once every shard has deposited
     xr_deposit(a, seq, tot, plen);
     return;
   }
   if (MODE == 0) pass_a_tail(a, st, tot, f);
   else pass_b_tail(a, st, tot, W, f);
+  if (a.dbg && tid == 0) {  // diagnostics: cycles of the election, the reduction and the tail algebra
+    long long* d = a.dbg + 8 * MODE;
+    d[0] += tq1 - tq0;
+    d[1] += tq2 - tq1;
+    d[2] += clock64() - tq2;
+    d[3] += 1;
+    d[4] += tq0 - tstart;
+  }
 }
 
 // One-CTA tail of a sharded pass: collect the shard totals, then the same
@@ -806,17 +828,36 @@ __global__ void __launch_bounds__(ST) sf_generate(const SFArgs a, int f) {
 __global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pass,
                                                      unsigned long long seq) {
   SFState* st = a.st;
+  const long long tstart = a.dbg ? clock64() : 0;
   __shared__ int flag;
   __shared__ double red[8 * 10 + 16];
   __shared__ double tot[16];
   const int tid = threadIdx.x;
   const int pc = st->pcp;
-  const bool skip = st->drop_all != 0;
+  __shared__ double sRc[16], sRi[16], sG0[16], sYn[SF_P];
+  __shared__ int sdrop;
+  if (pass == 0) {
+    if (tid < 16) sG0[tid] = st->G0[tid];
+    if (tid < SF_P) sYn[tid] = st->yn[tid];
+    __syncthreads();
+    if (tid == 0) {
+      sdrop = sf_shifted_chol(a.n_x_glob, sG0, sYn, pc, sRc, sRi);
+      if (blockIdx.x == 0) {  // the state the later kernels (and this pass's tail) read
+        st->drop_all = sdrop;
+        for (int i = 0; i < 16; ++i) { st->Rc[i] = sRc[i]; st->Rinv[i] = sRi[i]; }
+      }
+    }
+  } else {
+    if (tid < 16) sRi[tid] = st->Rinv[tid];
+    if (tid == 0) sdrop = st->drop_all;
+  }
+  __syncthreads();
+  const bool skip = sdrop != 0;
   double gacc[10] = {};
   if (!skip) {
     double Ri[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) Ri[i] = st->Rinv[i];
+    for (int i = 0; i < 16; ++i) Ri[i] = sRi[i];
     const double* Y = a.Yg[f % 3];
     const int64_t stride = (int64_t)gridDim.x * ST;
     for (int64_t i0 = (int64_t)blockIdx.x * ST + tid; i0 < a.n_x; i0 += 4 * stride) {
@@ -849,13 +890,24 @@ __global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pa
   cta_sum<10>(gacc, red, outv);
   double* part = a.part + (int64_t)blockIdx.x * PSTR;
   if (tid < 10) part[tid] = outv[tid];
+  const long long tq0 = a.dbg ? clock64() : 0;
   if (!last_cta(a.ticket + 3 + pass, &flag)) return;
-  reduce_parts(a.part, 10, tot);
+  const long long tq1 = a.dbg ? clock64() : 0;
+  reduce_parts(a.part, 10, tot, red);
+  const long long tq2 = a.dbg ? clock64() : 0;
   if (a.nshard > 1) {
     xr_deposit(a, seq, tot, 10);
     return;
   }
   if (tid == 0 && !skip) sf_chol_update(st, tot, pc);
+  if (a.dbg && tid == 0) {
+    long long* d = a.dbg + 16;
+    d[0] += tq1 - tq0;
+    d[1] += tq2 - tq1;
+    d[2] += clock64() - tq2;
+    d[3] += 1;
+    d[4] += tq0 - tstart;
+  }
 }
 
 // The small algebra closing flush f (one CTA): rank-revealing fix-up of R,
@@ -864,6 +916,7 @@ __global__ void __launch_bounds__(ST, 2) sf_cholqr(const SFArgs a, int f, int pa
 __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
   extern __shared__ double sm[];
   SFState* st = a.st;
+  const long long tf0 = a.dbg ? clock64() : 0;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int r = st->r, pc = st->pcp, n = r + pc;
   const int start = f * a.p;
@@ -877,14 +930,22 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
   double* Vj = Vc + SF_N * SF_N + 8;
   int* iPerm = reinterpret_cast<int*>(Vj + SF_N * SF_N + 8);
   int* iFlag = iPerm + SF_N + 4;
+  // the small state the single-thread sections read is staged by all threads
+  // first (one parallel round trip to L2 instead of a serial chain of loads)
+  __shared__ double gRc[16], gRi[16], gYn[SF_P], gSig[SF_N], gM[SF_N * SF_P];
+  if (tid < 16) { gRc[tid] = st->Rc[tid]; gRi[tid] = st->Rinv[tid]; }
+  if (tid < SF_P) gYn[tid] = st->yn[tid];
+  for (int i = tid; i < r; i += ST) gSig[i] = st->sig[i];
+  for (int i = tid; i < n * SF_P; i += ST) gM[i] = st->M[i];
+  __syncthreads();
   if (tid == 0) {
     double A[4][4], X[4][4];
     int pv[4];
     for (int i = 0; i < 4; ++i)
-      for (int k = 0; k < 4; ++k) A[i][k] = (i < pc && k < pc) ? st->Rc[i * 4 + k] : 0.0;
+      for (int k = 0; k < 4; ++k) A[i][k] = (i < pc && k < pc) ? gRc[i * 4 + k] : 0.0;
     pivoted_qr_reg<4>(A, pc, X, pv);
     double ysq = 0.0;
-    for (int s = 0; s < pc; ++s) ysq += st->yn[s];
+    for (int s = 0; s < pc; ++s) ysq += gYn[s];
     const double delta = 16.0 * DEPS * sqrt(ysq);
     for (int j = 0; j < 4; ++j)
       if (fabs(A[j][j]) <= delta || st->drop_all) {
@@ -897,13 +958,14 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
     for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 4; ++j) {
         double acc = 0.0;
-        for (int k = 0; k < 4; ++k) acc += st->Rinv[i * 4 + k] * X[k][j];
+        for (int k = 0; k < 4; ++k) acc += gRi[i * 4 + k] * X[k][j];
         sT[i * 4 + j] = (i < pc && j < pc) ? acc : 0.0;
       }
   }
   __syncthreads();
+  const long long tf1 = a.dbg ? clock64() : 0;
   auto Kel = [&](int i, int j) -> double {
-    if (i < r) return (j < r) ? (i == j ? st->sig[i] : 0.0) : st->C[i * SF_P + (j - r)];
+    if (i < r) return (j < r) ? (i == j ? gSig[i] : 0.0) : st->C[i * SF_P + (j - r)];
     return (j >= r) ? sR[(i - r) * 4 + (j - r)] : 0.0;
   };
   const int ldc = n;
@@ -937,10 +999,11 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
     }
     __syncthreads();
   }
+  const long long tf2 = a.dbg ? clock64() : 0;
   if (tid == 0) {
     double ysq = 0.0, ssq = 0.0;
-    for (int s = 0; s < pc; ++s) ysq += st->yn[s];
-    for (int i = 0; i < r; ++i) ssq += st->sig[i] * st->sig[i];
+    for (int s = 0; s < pc; ++s) ysq += gYn[s];
+    for (int i = 0; i < r; ++i) ssq += gSig[i] * gSig[i];
     const double fs = sqrt((double)r + ysq) * sqrt(ssq + (double)pc);
     int rn = (sS[0] <= NOISE_FLOOR * fs) ? 0 : rank_cut_dev(sS, n, a.eps0, a.r_max);
     if (rn > a.cap) { rn = a.cap; a.info[2] = 2; }
@@ -948,6 +1011,7 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
   }
   __syncthreads();
   const int rn = iFlag[0];
+  const long long tf3 = a.dbg ? clock64() : 0;
   // W' = [Uc_top; T Uc_bot] (n x rn), kept in shared memory (reusing the core) for C1 / Wd
   double* sW = sCore;  // n x rn, ld n
   for (int idx = tid; idx < n * rn; idx += ST) {
@@ -972,7 +1036,7 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
     const int i = idx / SF_P, s2 = idx % SF_P;
     double acc = 0.0;
     if (s2 < pcn)
-      for (int k = 0; k < n; ++k) acc += sW[k + i * n] * st->M[k * SF_P + s2];
+      for (int k = 0; k < n; ++k) acc += sW[k + i * n] * gM[k * SF_P + s2];
     sC1[idx] = acc;
     st->C[idx] = acc;
   }
@@ -989,6 +1053,14 @@ __global__ void __launch_bounds__(ST, 1) sf_finish(const SFArgs a, int f) {
     st->startp = start;
     st->pending = 1;
     a.trace[f] = rn;
+  }
+  if (a.dbg && tid == 0) {
+    long long* d = a.dbg + 24;
+    d[0] += tf1 - tf0;
+    d[1] += tf2 - tf1;
+    d[2] += tf3 - tf2;
+    d[3] += 1;
+    d[4] += clock64() - tf3;
   }
 }
 
@@ -1131,6 +1203,22 @@ cudaError_t launch_sweep_stream(const SFArgs* sh, int nlocal, int nflush, cudaSt
     nl += nlocal * (sharded ? 2 : 1);
     show("passB", f);
     if (gen && use_aux && (e = cudaStreamWaitEvent(s, aux.done, 0)) != cudaSuccess) return e;
+  }
+  if (a0.dbg) {
+    long long h[32];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, a0.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    if (h[16 + 3] > 0)
+      std::fprintf(stderr, "[sf timing] cholqr last CTA, mean cycles over %lld launches: main loop %lld, election %lld, reduce %lld, tail %lld\n",
+                   h[19], h[20] / h[19], h[16] / h[19], h[17] / h[19], h[18] / h[19]);
+    if (h[24 + 3] > 0)
+      std::fprintf(stderr, "[sf timing] finish, mean cycles over %lld launches: fix-up (thread 0) %lld, core SVD %lld, rank cut (thread 0) %lld, update matrices %lld\n",
+                   h[27], h[24] / h[27], h[25] / h[27], h[26] / h[27], h[28] / h[27]);
+    for (int m = 0; m < 2; ++m)
+      if (h[8 * m + 3] > 0)
+        std::fprintf(stderr, "[sf timing] pass %c last CTA, mean cycles over %lld launches: main loop %lld, election %lld, reduce %lld, tail %lld\n",
+                     m ? 'B' : 'A', h[8 * m + 3], h[8 * m + 4] / h[8 * m + 3], h[8 * m] / h[8 * m + 3],
+                     h[8 * m + 1] / h[8 * m + 3], h[8 * m + 2] / h[8 * m + 3]);
   }
   if (xseq) *xseq = seq;
   if (launches) *launches += nl;

@@ -29,6 +29,7 @@ struct SFState {
   double P2[SF_CAP * SF_P];
   double M[SF_N * SF_P];     // [U, y2]^T Yn of the next flush, [k * SF_P + s]
   double Wd[SF_N * SF_P];    // -Wp C1: y1 = Yn + [U, y2] Wd, [k * SF_P + s]
+  double G0[16];             // remainder Gram y2^T y2 (row-major 4x4), input of the shifted Cholesky
   double yn[SF_P];           // |Y_s|^2 of the flush being orthogonalised
   double yn_next[SF_P];      // ... of the flush being projected
   double Rc[16];             // remainder R (row-major 4x4)
@@ -75,6 +76,7 @@ struct SFArgs {
   int Ggen;              // CTAs of the light grid-stride passes
   int dbg_print;         // LRK_SF_DEBUG: flushes to report (diagnostics)
   int smem_pass;         // dynamic shared memory of the staged passes (bytes)
+  long long* dbg;        // LRK_SF_TIMING: cycle sums of the last-CTA tails (diagnostics), else null
 };
 size_t sf_smem_pass();
 int64_t sf_part_stride();
