@@ -10,6 +10,10 @@ python bench.py --steps 5 --warmup 3 > $O/${TAG}_bench_c4.json 2> $O/${TAG}_benc
 python bench.py --steps 10 --warmup 3 --config C2 > $O/${TAG}_bench_c2.json 2> $O/${TAG}_bench_c2.err
 python bench.py --impl reference --steps 2 --warmup 1 > $O/${TAG}_bench_ref_c4.json 2> $O/${TAG}_bench_ref_c4.err
 python tools/dgemm_peak.py > $O/${TAG}_dgemm_peak.txt 2>&1
+for c in C2 C4 C3; do python tools/config_arnoldi.py $c > $O/${TAG}_arnoldi_$c.json 2> $O/${TAG}_arnoldi_$c.err; done
+LRK_SF_TIMING=1 python tools/c4_probe.py 128 2048 1 > $O/${TAG}_sf_timing.txt 2>&1
+python tools/c3_probe.py 512 1024 > $O/${TAG}_c3_probe.txt 2>&1
+python tools/c5_probe.py 256 16 > $O/${TAG}_c5_probe.txt 2>&1
 python tools/hbm_roofline.py > $O/${TAG}_streaming_kernels.jsonl 2>&1
 # launch list of the bench command (first 7000 launches: setup + the first apply)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 7000 --csv --log-file $O/${TAG}_launches_bench_c4.csv \
