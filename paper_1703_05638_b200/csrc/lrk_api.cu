@@ -574,12 +574,18 @@ int gmres_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, double rto
     return LRK_OK;
   }
   TRY(precond_apply(c, b, x, s));  // x0 = P^{-1} b
+  double beta_prev = 0.0;
   for (int restart = 0;; ++restart) {
     TRY(step_apply(c, x, w, adjoint, s));
     TRY(axpby(c, b, 1.0, w, -1.0, Qb, s));  // r = b - S x
     double beta = 0.0;
     TRY(lrk_cgs2(c, nullptr, nx, 0, Qb, n, nullptr, &beta, s));
     if (beta <= rtol * bnorm) break;
+    // attainable accuracy: for large tau the step matrix is ill conditioned and the
+    // true residual stalls at ~eps cond(S) ||b|| (what a direct solve delivers too);
+    // a restart that no longer halves a residual already below 1e-10 ||b|| is accepted
+    if (restart >= 2 && beta > 0.5 * beta_prev && beta <= 1e-10 * bnorm) break;
+    beta_prev = beta;
     if (restart >= 25)
       return fail(c, LRK_ERR_CONVERGENCE, "GMRES step solve did not reach its tolerance");
     TRY(axpby(c, Qb, 1.0 / beta, nullptr, 0.0, Qb, s));
