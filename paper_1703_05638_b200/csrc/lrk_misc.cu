@@ -298,6 +298,16 @@ static void launch_march_mz(const StencilArgs& a, cudaStream_t s) {
 // 3-D 16/32/64 -> 717/710/709 us)
 template <int D>
 static void launch_march(const StencilArgs& a, cudaStream_t s) {
+  if (D == 2) {
+    // few columns (the step solves of the physical-space sweep work on ONE column):
+    // a CTA's run time is its chain of dependent plane steps, so short marches on
+    // more CTAs (512^2 x 1 column: 64 CTAs x 19 steps -> 256 CTAs x 7 steps)
+    const int64_t ctas16 = (int64_t)((a.n + 255) / 256) * ((a.n + 15) / 16) * a.ncols;
+    if (ctas16 < 2 * 148) {
+      launch_march_mz<D, 4>(a, s);
+      return;
+    }
+  }
   launch_march_mz<D, D == 2 ? 16 : 32>(a, s);
 }
 
