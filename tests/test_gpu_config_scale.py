@@ -350,3 +350,19 @@ def test_streaming_flush_at_the_rank_cap_matches_persistent(monkeypatch):
     assert out["0"][0] == out["1"][0]
     ref = out["0"][1]
     assert np.abs(out["1"][1] - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("shards", [1, 4])
+def test_streaming_sweep_is_bitwise_reproducible(shards):
+    """Every reduction of the streaming-flush sweep runs in a fixed order (CTA
+    partials by the last CTA, shard totals in shard order), so repeated applies
+    of the same vector return the same bits — also with the generation running
+    concurrently on the second stream."""
+    from paper_1703_05638_b200 import _lib
+
+    ctx, grid, _ = _ctx(48, 3, "fd", 32, 12, 4, 0.005, 1.0, 0.02, 64)
+    if shards > 1:
+        assert _lib.get_lib().lrk_set_emulated_shards(ctx._dev.handle, shards) == 0
+    v = np.random.default_rng(5).standard_normal(grid.n_x)
+    outs = [ctx.apply(v) for _ in range(3)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
