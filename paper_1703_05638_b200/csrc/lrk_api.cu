@@ -641,8 +641,23 @@ int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, 
   WS(double, r, "rs_r", nx);
   WS(double, part, "rs_part", 2 * 296);
   WS(unsigned, cnt, "rs_cnt", 1);
-  TRY(precond_apply(c, b, x, s));
   StencilArgs a = make_stencil(c->op, adjoint);
+  // one persistent kernel per solve where it applies (2-D, even n): every phase of
+  // the iteration in one cooperative launch instead of ~70 dependent launches
+  if (flag && !std::getenv("LRK_RICH_MULTI")) {
+    WS(double, T1, "rs_T1", nx);
+    WS(double, T2, "rs_T2", nx);
+    WS(unsigned, rbar, "rs_bar", 4);
+    const cudaError_t e = launch_rich(a, c->n, c->rich_it, c->dS, c->dThetaM, b, x, r, T1, T2, rbar,
+                                      part, flag, STEP_RTOL * STEP_RTOL, c->num_sms, s);
+    if (e == cudaSuccess) {
+      ++c->launches;
+      return LRK_OK;
+    }
+    if (e != cudaErrorNotSupported) CK(e);
+    cudaGetLastError();
+  }
+  TRY(precond_apply(c, b, x, s));
   a.X = x; a.ldx = nx; a.Y = r; a.ldy = nx; a.ncols = 1; a.Bres = b; a.ldbres = nx;
   for (int it = 0; it < c->rich_it; ++it) {
     launch_stencil(a, s);

@@ -34,6 +34,13 @@ struct StencilArgs {
 };
 
 __global__ void stencil_kernel(StencilArgs a);
+// Persistent preconditioned Richardson step solve (lrk_rich.cu): x = S^{-1} b by
+// x0 = P^{-1} b and `sweeps` corrections in one cooperative launch, then the
+// true-residual check (flag raised when ||b - S x||^2 > tol2 ||b||^2).
+// cudaErrorNotSupported: shape outside its scope (3-D, odd n, per-node upwind).
+cudaError_t launch_rich(const StencilArgs& st, int n, int sweeps, const double* S1, const double* D,
+                        const double* b, double* x, double* r, double* T1, double* T2, unsigned* bar,
+                        double* part, int* flag, double tol2, int num_sms, cudaStream_t s);
 // tiled kernels (2-D box, 3-D 7-point) or the generic one; a.ncols columns
 void launch_stencil(const StencilArgs& a, cudaStream_t s);
 __global__ void shift_kernel(const double* W2, int64_t ld2, int n_t, int ncols, int adjoint,
