@@ -338,6 +338,24 @@ def make_context(cfg, lp):
                              compress_every=cfg["p"]), grid
 
 
+# FP64 tensor-pipe ceiling of this pool's B200s: cuBLAS DGEMM 8192^3, measured with
+# tools/dgemm_peak.py (profiles/dgemm_peak_r02l.txt; 4096^3 gives 35.3).  MEASURED_PEAKS.json
+# carries no FP64 figure, so this is our own measurement.
+FP64_DGEMM_PEAK_TFLOPS = 35.5
+
+
+def sweep_fp64_flops(n_x, trace, p):
+    """Algorithmic FP64 flops of one sweep from its rank trace (one entry per flush + final):
+    per row and flush, block CGS2 of the p new columns against the rank-r pane (two passes of
+    project + subtract, 8pr), the remainder QR (4p^2) and the basis update [U, Q](r+p) x r'
+    (2(r+p)r') — forward.py:172's truncate restated as the incremental update the kernels run."""
+    flops, r = 0.0, 0
+    for rn in trace[:-1] if len(trace) > 1 else trace:
+        flops += n_x * (8.0 * p * r + 4.0 * p * p + 2.0 * (r + p) * rn)
+        r = rn
+    return flops
+
+
 def gpu_arm(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -416,6 +434,9 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     sw_ms, sw_n, sw_bytes = c_double(0), c_int64(0), c_double(0)
     lib.lrk_profile_read(h_dev, byref(sw_ms), byref(sw_n), byref(sw_bytes), 1)
     lib.lrk_profile_enable(h_dev, 0)
+    fw, _, bw = ctx.last_traces()
+    sweep_flops = 0.5 * (sweep_fp64_flops(grid.n_x, fw, cfg["p"]) +
+                         sweep_fp64_flops(grid.n_x, bw, cfg["p"]))
 
     # ---------------- end to end through the public API with host buffers
     vh = torch.empty(grid.n_x, dtype=torch.float64).pin_memory()
@@ -438,7 +459,8 @@ def gpu_arm(args, cfg, rank, world, local_rank):
     return {
         "total_ms": float(stats[0]), "e2e_s": float(stats[1]), "launches": launches,
         "ranks": ranks, "sweep_ms": sw_ms.value, "sweep_n": sw_n.value,
-        "sweep_bytes": sw_bytes.value, "clocks": clk.summary(), "n_x": grid.n_x,
+        "sweep_bytes": sw_bytes.value, "sweep_flops": sweep_flops, "clocks": clk.summary(),
+        "n_x": grid.n_x,
         "mode": mode, "note": note,
     }
 
@@ -542,7 +564,17 @@ def main():
                                     "2 x sf_cholqr, sf_finish, sf_generate)" if args.config == "C4"
                                     else "lrk::sweep_kernel"), "peak_kind": peak_kind,
                          "alg_bytes_per_launch": per_launch_bytes,
-                         "ms_per_launch": per_launch_ms, "build": build_hash()},
+                         "ms_per_launch": per_launch_ms, "build": build_hash(),
+                         # the same launch against the FP64 tensor pipe: at pane ranks ~40 the
+                         # basis update puts the sweep at the ridge of the two rooflines
+                         "fp64_tensor": {
+                             "flops_per_launch": res["sweep_flops"],
+                             "achieved": res["sweep_flops"] / (per_launch_ms * 1e-3) / 1e12
+                             if per_launch_ms > 0 else 0.0,
+                             "peak": FP64_DGEMM_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": (res["sweep_flops"] / (per_launch_ms * 1e-3) / 1e12 /
+                                      FP64_DGEMM_PEAK_TFLOPS) if per_launch_ms > 0 else 0.0,
+                             "peak_kind": "cuBLAS DGEMM 8192^3 measured on this pool"}},
             "cpu_baseline": cpu,
             "e2e": {"value": n * args.steps / res["e2e_s"], "unit": "matvec/s",
                     "h2d_bytes_per_step": 8 * res["n_x"], "d2h_bytes_per_step": 8 * res["n_x"],
