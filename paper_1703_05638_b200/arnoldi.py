@@ -97,6 +97,7 @@ class ArnoldiResult:
 def _torch():
     import torch
 
+    _lib.require_cuda()
     return torch
 
 
@@ -348,7 +349,9 @@ def _combine_dense(basis: list, coeffs: np.ndarray):
     """All Ritz vectors as one device product basis @ coeffs, columns normalised."""
     torch = _torch()
     Q = torch.stack([_to_dev_vec(b) for b in basis], dim=1)
-    Y = Q @ torch.as_tensor(np.ascontiguousarray(np.real(coeffs)), dtype=torch.float64,
+    # a fresh copy: a 1 x 1 slice of a reversed array keeps its negative stride through
+    # ascontiguousarray, which torch refuses
+    Y = Q @ torch.as_tensor(np.array(np.real(coeffs), dtype=float, order="C"), dtype=torch.float64,
                              device=Q.device)
     nrm = Y.norm(dim=0)
     return Y / torch.where(nrm > 0, nrm, torch.ones_like(nrm))

@@ -52,6 +52,11 @@ def to_device_colmajor(X):
     return t
 
 
+def _shape_of(X):
+    """Anything with .shape as is; nested lists through numpy (host-side shape checks)."""
+    return X if hasattr(X, "shape") else np.asarray(X)
+
+
 def ld_of(t) -> int:
     """Leading dimension (column stride) of a column-major tensor."""
     if t.shape[1] <= 1:
@@ -83,6 +88,10 @@ class LowRankMat:
     __slots__ = ("W1", "W2")
 
     def __init__(self, W1, W2):
+        # shape errors are host logic (lowrank.py:47-50): report them before touching the device
+        s1, s2 = tuple(_shape_of(W1).shape), tuple(_shape_of(W2).shape)
+        if len(s1) > 2 or len(s2) > 2 or (s1[-1] if s1 else 1) != (s2[-1] if s2 else 1):
+            raise ValueError(f"factor shapes {s1} and {s2} are inconsistent")
         W1 = to_device_colmajor(W1)
         W2 = to_device_colmajor(W2)
         if W1.shape[1] != W2.shape[1]:

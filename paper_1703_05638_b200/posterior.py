@@ -15,6 +15,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from .errors import NumericalError
 
 
@@ -43,6 +44,7 @@ class PosteriorSummary:
 def _torch():
     import torch
 
+    _lib.require_cuda()
     return torch
 
 
@@ -88,13 +90,13 @@ def variance_diag(eigenvalues, V, gamma_prior: float, prior=None) -> np.ndarray:
 def build_summary(ritz_values, ritz_vectors, gamma_prior: float, eps_eig: float | None = None,
                   imag_rtol: float = 1e-6, n_x: int | None = None, prior=None) -> PosteriorSummary:
     """Retain λ >= eps_eig, normalise, re-orthonormalise, variance (posterior.py:65-111)."""
-    torch = _torch()
     vals = np.asarray(ritz_values)
     scale = float(np.max(np.abs(vals.real))) if vals.size else 0.0
     if scale > 0 and np.max(np.abs(vals.imag)) > imag_rtol * scale:
         raise NumericalError(
             "Ritz values have a significant imaginary part "
             f"({np.max(np.abs(vals.imag)):.3e} vs scale {scale:.3e})")
+    torch = _torch()
     real = vals.real.astype(float)
     order = np.argsort(-real)
     threshold = eps_eig if eps_eig is not None else 0.0
