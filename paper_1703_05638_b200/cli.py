@@ -33,6 +33,7 @@ from .arnoldi import StopRule, lr_arnoldi, start_vector
 from .errors import InvalidConfigError, NumericalError
 from .forward import SpaceTimeOperator
 from .lowrank import TruncationPolicy, lr_from_dense, lr_singular_values, lr_to_dense
+from .posterior import write_variance_csv, write_variance_pgm  # noqa: F401 (used by cmd_variance)
 
 ENV_PREFIX = "LRPOSTCOV_"
 PROBLEMS = ("heat", "convdiff", "steady-poisson")
@@ -367,23 +368,6 @@ def write_eigs_outputs(run: EigsRun, outdir: Path) -> None:
     (outdir / "diagnostics.log").write_text("\n".join(log) + "\n")
 
 
-def write_variance_csv(field_values, n_side: int, path) -> None:
-    """n_side x n_side grid, row j = x2 level j, 17 significant digits (posterior.py:133-139)."""
-    g = np.asarray(field_values, dtype=float).reshape(n_side, n_side)
-    _table(Path(path), ",".join(f"c{i}" for i in range(n_side)),
-           [",".join(f"{v:.17g}" for v in row) for row in g])
-
-
-def write_variance_pgm(field_values, n_side: int, gamma_prior: float, path) -> None:
-    """Plain-text 8-bit PGM: the field minimum maps to 0, gamma_prior to 255 (posterior.py:142-155)."""
-    g = np.asarray(field_values, dtype=float).reshape(n_side, n_side)
-    lo = float(g.min())
-    span = gamma_prior - lo
-    pix = np.full(g.shape, 255.0) if span <= 0 else np.clip(255.0 * (g - lo) / span, 0.0, 255.0)
-    rows = [" ".join(str(int(v)) for v in row) for row in np.rint(pix)]
-    Path(path).write_text(f"P2\n{n_side} {n_side}\n255\n" + "".join(r + "\n" for r in rows))
-
-
 def _outdir(cfg: RunConfig) -> Path:
     d = Path(cfg.out)
     d.mkdir(parents=True, exist_ok=True)
@@ -440,9 +424,12 @@ def run_oracle(cfg: RunConfig, retain: float = 1e-8, top_k: int = 10):
     """Low-rank path against the dense GPU brute force (cli.py:415-470)."""
     if cfg.prior_gamma > 0 or cfg.obs_every > 1 or cfg.dim != 2:
         raise InvalidConfigError("the dense oracle covers the reference's scalar-prior 2-D instances")
-    probe = build_problem(cfg)
     source = cfg.mode == hessian.MODE_SOURCE
-    dim = probe.grid.n_x * probe.time.n_t if source else probe.ctx.n_param
+    dim = cfg.n_side ** cfg.dim * (cfg.nt if source else 1)
+    if dim > dense.DENSE_DIM_CAP:   # a configuration error, decided before any device work
+        raise InvalidConfigError(
+            f"dense oracle dimension {dim} exceeds the cap {dense.DENSE_DIM_CAP}")
+    probe = build_problem(cfg)
     Hd, asym = _dense_hessian(probe)
     hv = dense.hv_agreement(_stacked_apply(probe), Hd, n_probe=20, seed=cfg.seed)
     run = run_eigs(cfg.replace(m_a=min(cfg.m_a, dim + 8)), force_restart=True)

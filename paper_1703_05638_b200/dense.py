@@ -76,6 +76,17 @@ def _march(step: _StepLU, F_of_k, n_t: int, adjoint: bool):
     return out
 
 
+def dense_forward(L_dense, m_scale: float, tau: float, F, adjoint: bool = False) -> np.ndarray:
+    """Y with K vec(Y) = vec(F) (K^T when adjoint) by block substitution with one dense LU
+    of the step matrix (oracle.py:22-39); F and Y are n_x x n_t, one column per time step."""
+    Fd = _dev(F)
+    n_x, n_t = Fd.shape
+    _guard(n_x)
+    step = _StepLU(L_dense, m_scale, tau)
+    panes = _march(step, lambda k: Fd[:, k:k + 1], n_t, adjoint)
+    return _torch().cat(panes, dim=1).cpu().numpy()
+
+
 def _sym(H):
     """(symmetrised matrix as numpy, asymmetry defect relative to max |H|)."""
     scale = float(H.abs().max())

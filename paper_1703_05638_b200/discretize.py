@@ -318,3 +318,22 @@ def eigvec_dense(m: int, n: int, grid: Grid, k: int | None = None) -> np.ndarray
         f3 = np.sin(k * np.pi * x)
         return np.kron(f3 / np.linalg.norm(f3), np.kron(f2, f1))
     return np.kron(f2, f1)
+
+
+# ------------------------------------------------------------------- text exchange
+def export_coo(op: SpatialOperator, path) -> None:
+    """One 'row col value' line per stored entry, 0-based, 17 significant digits
+    (discretize.py:171-176): the assembled matrix for use outside the package."""
+    m = sp.coo_matrix(op.L)
+    with open(path, "w") as fh:
+        fh.writelines(f"{int(i)} {int(j)} {float(v):.17g}\n" for i, j, v in zip(m.row, m.col, m.data))
+
+
+def import_coo(path, n: int) -> sp.csr_matrix:
+    """Inverse of export_coo (discretize.py:179-190); blank lines are skipped."""
+    triples = [line.split() for line in open(path) if line.strip()]
+    if not triples:
+        return sp.csr_matrix((n, n))
+    r, c, v = zip(*triples)
+    return sp.csr_matrix((np.array(v, dtype=float), (np.array(r, dtype=int), np.array(c, dtype=int))),
+                         shape=(n, n))

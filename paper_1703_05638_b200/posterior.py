@@ -144,3 +144,29 @@ def posterior_apply(v, summary: PosteriorSummary) -> np.ndarray:
         return summary.gamma_prior * v
     V = summary.V
     return summary.gamma_prior * (v - V @ (summary.filters * (V.T @ v)))
+
+
+# ------------------------------------------------------------------- writers
+def variance_to_grid(field_values, n_side: int) -> np.ndarray:
+    """Dof-ordered field -> (x2, x1)-indexed n_side x n_side grid (posterior.py:128-130)."""
+    return np.asarray(field_values, dtype=float).reshape(n_side, n_side)
+
+
+def write_variance_csv(field_values, n_side: int, path) -> None:
+    """Header c0..c{n-1}, then row j = x2 level j with 17 significant digits (posterior.py:133-139)."""
+    lines = [",".join(f"c{i}" for i in range(n_side))]
+    lines += [",".join(f"{v:.17g}" for v in row) for row in variance_to_grid(field_values, n_side)]
+    with open(path, "w") as fh:
+        fh.write("".join(line + "\n" for line in lines))
+
+
+def write_variance_pgm(field_values, n_side: int, gamma_prior: float, path) -> None:
+    """Plain-text 8-bit PGM: the field minimum maps to 0, gamma_prior to 255; a field with no
+    reduction anywhere is all white (posterior.py:142-155)."""
+    g = variance_to_grid(field_values, n_side)
+    lo = float(g.min())
+    span = gamma_prior - lo
+    pix = np.full(g.shape, 255.0) if span <= 0 else np.clip(255.0 * (g - lo) / span, 0.0, 255.0)
+    rows = [" ".join(str(int(v)) for v in row) for row in np.rint(pix)]
+    with open(path, "w") as fh:
+        fh.write(f"P2\n{n_side} {n_side}\n255\n" + "".join(r + "\n" for r in rows))

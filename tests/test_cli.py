@@ -201,3 +201,139 @@ def test_cli_outputs_match_the_reference_cli(tmp_path, case):
     _compare_dir(str(out), os.path.join(GOLD, case), conv)
     if argv[0] in ("eigs", "variance"):
         assert (out / "diagnostics.log").read_text().startswith("iterations=")
+
+
+# --------------------------------------------- reference CLI behaviours beyond the fixtures
+def _quiet_main(argv):
+    with contextlib.redirect_stderr(io.StringIO()):
+        return cli.main(argv)
+
+
+@pytest.mark.gpu
+def test_steady_eigs_leading_value(tmp_path):
+    """test_cli.py:27-39: the first Ritz value of the steady problem is (bp/bn)/lambda_11^2."""
+    import paper_1703_05638_b200 as lp
+    out = tmp_path / "steady"
+    assert _quiet_main(["eigs", "--problem", "steady-poisson", "--mode", "steady", "--n-side", "15",
+                        "--m-a", "60", "--eps-eig", "1e-12", "--check-every", "100", "--k", "5",
+                        "--out", str(out)]) == 0
+    header, rows = _csv(out / "eigenvalues.csv")
+    assert header == ["index", "ritz_value", "imag_part"]
+    want = 1e-4 / lp.discrete_fd_eig(1, 1, lp.build_grid(15)) ** 2
+    assert float(rows[0][1]) == pytest.approx(want, rel=1e-8)
+
+
+@pytest.mark.gpu
+def test_repeated_and_manifest_driven_runs_are_bitwise_identical(tmp_path):
+    """test_cli.py:42-64: the same flags twice, and a rerun from the written manifest,
+    reproduce eigenvalues.csv / ranks.csv / hessenberg.csv byte for byte."""
+    flags = ["eigs", "--problem", "heat", "--n-side", "7", "--nt", "4", "--m-a", "15", "--eps-eig",
+             "1e-10", "--check-every", "100", "--seed", "3", "--start", "random"]
+    a, b, c = tmp_path / "a", tmp_path / "b", tmp_path / "c"
+    assert _quiet_main(flags + ["--out", str(a)]) == 0
+    assert _quiet_main(flags + ["--out", str(b)]) == 0
+    assert _quiet_main(["eigs", "--config", str(a / "manifest.cfg"), "--out", str(c)]) == 0
+    for name in ("eigenvalues.csv", "ranks.csv", "hessenberg.csv"):
+        assert (a / name).read_bytes() == (b / name).read_bytes() == (c / name).read_bytes()
+
+
+@pytest.mark.gpu
+def test_variance_with_nothing_retained_is_the_prior(tmp_path):
+    """test_cli.py:67-80: a vanishing noise weight leaves every eigenvalue below the retention
+    threshold; the field is gamma everywhere and retained.csv has no rows."""
+    out = tmp_path / "flat"
+    assert _quiet_main(["variance", "--problem", "heat", "--n-side", "7", "--nt", "4", "--sensors",
+                        "none", "--beta-ratio", "1e-12", "--m-a", "10", "--eps-eig", "1e-1",
+                        "--check-every", "100", "--gamma-prior", "10", "--out", str(out)]) == 0
+    _, rows = _csv(out / "variance.csv")
+    np.testing.assert_allclose(np.array(rows, dtype=float), 10.0, rtol=1e-12)
+    assert _csv(out / "retained.csv")[1] == []
+
+
+@pytest.mark.gpu
+def test_variance_minimum_lies_on_a_sensor(tmp_path):
+    """test_cli.py:83-95 (heat 31^2, n_t 10, 3x3 sensors) and the PGM header."""
+    import paper_1703_05638_b200 as lp
+    out = tmp_path / "var31"
+    assert _quiet_main(["variance", "--problem", "heat", "--n-side", "31", "--nt", "10", "--m-a", "25",
+                        "--eps-eig", "1e-1", "--out", str(out)]) == 0
+    _, rows = _csv(out / "variance.csv")
+    field = np.array(rows, dtype=float).ravel()
+    assert lp.make_sensor_layout_3x3(lp.build_grid(31)).mask[int(np.argmin(field))]
+    assert (out / "variance.pgm").read_text().startswith("P2\n31 31\n255\n")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("argv", [
+    ["oracle", "--problem", "convdiff", "--nu", "1e-2", "--n-side", "5", "--nt", "4", "--m-a", "100",
+     "--eps-eig", "1e-12", "--check-every", "100"],
+    ["oracle", "--problem", "heat", "--n-side", "4", "--nt", "3", "--sensors", "none", "--mode",
+     "source", "--m-a", "60", "--eps-eig", "1e-14", "--check-every", "100"],
+], ids=["convdiff", "source"])
+def test_oracle_passes_for_convdiff_and_source_mode(tmp_path, argv):
+    """test_cli.py:108-115, 219-225."""
+    out = tmp_path / "orc"
+    assert _quiet_main(argv + ["--out", str(out)]) == 0
+    assert "result=PASS" in (out / "oracle_report.txt").read_text()
+
+
+def test_oracle_refuses_instances_above_the_dense_cap(tmp_path):
+    """test_cli.py:126-129: exit code 2 (configuration error), decided on the host."""
+    assert _quiet_main(["oracle", "--problem", "heat", "--n-side", "63", "--nt", "30",
+                        "--out", str(tmp_path / "big")]) == 2
+
+
+def test_sweep_rejects_an_unknown_axis(tmp_path):
+    """test_cli.py:157-160."""
+    assert _quiet_main(["sweep", "--axis", "bogus", "--values", "1,2", "--out", str(tmp_path / "x")]) == 2
+
+
+@pytest.mark.gpu
+def test_sweep_orders_points_and_survives_a_bad_one(tmp_path):
+    """test_cli.py:132-154: summary.csv header and point labels, the leading eigenvalue grows as
+    nu shrinks, one directory per point; an invalid point is recorded as ERROR, the sweep goes on
+    and the exit code is 3."""
+    out = tmp_path / "sweep"
+    assert _quiet_main(["sweep", "--axis", "nu", "--values", "1e-1,1e-2,1e-3", "--problem", "convdiff",
+                        "--n-side", "15", "--nt", "6", "--m-a", "25", "--eps-eig", "1e-1",
+                        "--out", str(out)]) == 0
+    header, rows = _csv(out / "summary.csv")
+    assert header == ["point", "iterations_to_threshold", "max_rank", "largest_eig"]
+    assert [r[0] for r in rows] == ["1e-1", "1e-2", "1e-3"]
+    top = [float(r[3]) for r in rows]
+    assert top[0] < top[1] < top[2]
+    for r in rows:
+        assert (out / f"nu_{r[0]}" / "eigenvalues.csv").exists()
+    bad = tmp_path / "sweepfail"
+    assert _quiet_main(["sweep", "--axis", "nu", "--values", "1e-2,-1.0", "--problem", "convdiff",
+                        "--n-side", "7", "--nt", "4", "--m-a", "10", "--out", str(bad)]) == 3
+    _, rows = _csv(bad / "summary.csv")
+    assert rows[0][0] == "1e-2" and rows[1][1] == "ERROR"
+
+
+@pytest.mark.gpu
+def test_manifest_lists_every_reference_key_and_notes_degraded_sensors(tmp_path):
+    """test_cli.py:193-208: one key=value line per configuration field; a 3x3 layout on a grid
+    too coarse for it is replaced and the manifest says so."""
+    out = tmp_path / "mani"
+    assert _quiet_main(["eigs", "--problem", "heat", "--n-side", "7", "--nt", "3", "--sensors",
+                        "grid3x3", "--m-a", "5", "--check-every", "100", "--out", str(out)]) == 0
+    text = (out / "manifest.cfg").read_text()
+    for s in cli.SETTINGS:
+        if not s.extension:
+            assert f"{s.key}=" in text, s.key
+    assert "under-resolved" in text
+
+
+@pytest.mark.gpu
+def test_source_mode_eigs_writes_ranks_and_singular_values(tmp_path):
+    """test_cli.py:228-239."""
+    out = tmp_path / "src"
+    assert _quiet_main(["eigs", "--problem", "heat", "--n-side", "9", "--nt", "6", "--sensors", "none",
+                        "--mode", "source", "--m-a", "10", "--check-every", "100", "--out", str(out)]) == 0
+    _, rows = _csv(out / "ranks.csv")
+    assert len(rows) == 10 and all(int(r[1]) >= 1 for r in rows)
+    header, sig = _csv(out / "singular_values.csv")
+    assert header == ["vector", "index", "sigma"]
+    first = [float(r[2]) for r in sig if r[0] == "0"]
+    assert first and all(a >= b for a, b in zip(first, first[1:]))

@@ -717,3 +717,23 @@ def test_compare_reports():
     R = np.eye(4)
     R[1:3, 1:3] = [[c, -s], [s, c]]
     assert dense.compare(v4, V @ R, v4, V).max_principal_angle <= 1e-10
+
+
+def test_dense_substitution_solves_the_kronecker_system_both_ways():
+    """test_oracle.py:66-83: dense_forward against the assembled space-time matrix, forward
+    and adjoint (1e-10)."""
+    grid, op, _ = _heat(5, 3)
+    n, n_t, tau, m = grid.n_x, 3, 1.0 / 3.0, grid.m_scale
+    A = m * (np.eye(n) + tau * op.L.toarray())
+    Kfull = np.kron(np.eye(n_t), A) - m * np.kron(np.diag(np.ones(n_t - 1), -1), np.eye(n))
+    F = np.random.default_rng(152).standard_normal((n, n_t))
+    Y = dense.dense_forward(op.L.toarray(), m, tau, F)
+    np.testing.assert_allclose(Y.reshape(-1, order="F"),
+                               np.linalg.solve(Kfull, F.reshape(-1, order="F")), rtol=1e-10)
+    Z = dense.dense_forward(op.L.toarray(), m, tau, F, adjoint=True)
+    np.testing.assert_allclose(Z.reshape(-1, order="F"),
+                               np.linalg.solve(Kfull.T, F.reshape(-1, order="F")), rtol=1e-10)
+    # and the device sweep solves the same system
+    K = lp.SpaceTimeOperator(op, lp.build_time_grid(n_t))
+    S = lp.lr_to_dense(lp.st_solve_sweep(K, lp.lr_from_dense(F, POL), POL))
+    assert np.linalg.norm(S - Y) <= 1e-8 * np.linalg.norm(Y)

@@ -231,3 +231,85 @@ def test_oracle_report_text_round_trip():
     assert float(parsed["max_eig_rel_error"]) == pytest.approx(1e-9)
     assert float(parsed["variance_rel_error"]) == pytest.approx(4e-6)
     assert float(parsed["tol_eig_rel"]) == pytest.approx(1e-6)
+
+
+def test_dof_indexing_and_coordinates():
+    """test_discretize.py:21-33: (i, j) <-> dof is a bijection with x1 fastest; coords follow it."""
+    g = lp.build_grid(6)
+    seen = {g.ij_to_dof(i, j) for i in range(6) for j in range(6)}
+    assert seen == set(range(36))
+    for k in (0, 5, 6, 17, 35):
+        assert g.ij_to_dof(*g.dof_to_ij(k)) == k
+    x1, x2 = g.coords()
+    k = g.ij_to_dof(4, 2)
+    assert x1[k] == pytest.approx(5 * g.h) and x2[k] == pytest.approx(3 * g.h)
+
+
+def test_laplacian_of_ones_vanishes_away_from_the_boundary():
+    """test_discretize.py:53-62."""
+    g = lp.build_grid(9)
+    out = (sp.csr_matrix(lp.assemble_heat(g).L) @ np.ones(g.n_x)).reshape(9, 9)
+    assert np.abs(out[1:-1, 1:-1]).max() <= 1e-10 * (4 / g.h ** 2)
+    assert (out[0] > 0).all() and (out[:, -1] > 0).all()
+
+
+def test_convdiff_validation_and_row_sums():
+    """test_discretize.py:73-96: nu > 0 required; upwinding keeps row sums nonnegative and the
+    symmetric part positive definite; at most five entries per row."""
+    g = lp.build_grid(7)
+    for nu in (0.0, -1e-2):
+        with pytest.raises(lp.InvalidConfigError):
+            lp.assemble_convdiff(g, nu, (0.0, 1.0))
+    for w in ((1.0, 0.0), (-0.5, 2.0), (0.3, -0.7)):
+        A = sp.csr_matrix(lp.assemble_convdiff(g, 1e-2, w).L)
+        assert np.asarray(A.sum(axis=1)).min() >= -1e-9 * abs(A).max()
+        assert np.linalg.eigvalsh(0.5 * (A + A.T).toarray())[0] > 0
+        assert np.diff(A.indptr).max() <= 5
+
+
+def test_discrete_eigenvalues_order_and_mode_symmetries():
+    """test_discretize.py:98-141: pi^2 (m^2/a^2 + n^2/b^2); the discrete values increase with
+    either index; the first mode is positive; even modes are antisymmetric under reflection."""
+    assert lp.analytic_poisson_eig(1, 1) == pytest.approx(2 * np.pi ** 2, rel=1e-15)
+    assert lp.analytic_poisson_eig(2, 3, a=2.0, b=0.5) == pytest.approx(np.pi ** 2 * (1.0 + 36.0))
+    g = lp.build_grid(9)
+    vals = np.array([[lp.discrete_fd_eig(m, n, g) for n in range(1, 10)] for m in range(1, 10)])
+    assert (np.diff(vals, axis=0) > 0).all() and (np.diff(vals, axis=1) > 0).all()
+    assert (lp.eigvec_dense(1, 1, g) > 0).all()
+    v = lp.eigvec_dense(2, 1, g).reshape(9, 9)       # row j = x2 level, column i = x1
+    np.testing.assert_allclose(v, -v[:, ::-1], atol=1e-14)
+    f1, f2 = lp.analytic_separable_eigvec(2, 3, g)
+    np.testing.assert_allclose(np.outer(f2, f1).ravel() / np.linalg.norm(np.outer(f2, f1)),
+                               lp.eigvec_dense(2, 3, g), atol=1e-14)
+
+
+def test_coo_text_exchange_round_trip(tmp_path):
+    """test_discretize.py:153-158: bit-exact through the 17-digit text form."""
+    from paper_1703_05638_b200 import discretize as dz
+
+    op = lp.assemble_convdiff(lp.build_grid(5), 3e-2, (0.2, 1.0))
+    dz.export_coo(op, tmp_path / "op.coo")
+    back = dz.import_coo(tmp_path / "op.coo", op.grid.n_x)
+    assert np.abs((back - op.L).toarray()).max() == 0.0
+
+
+def test_variance_writers(tmp_path):
+    """test_posterior.py:165-195: CSV grid with header, 17 digits; PGM maps the minimum to 0 and
+    gamma to 255; a flat field at the prior is all white."""
+    rng = np.random.default_rng(7)
+    n = 6
+    field = rng.uniform(2.0, 10.0, n * n)
+    field[13] = 1.0
+    posterior.write_variance_csv(field, n, tmp_path / "v.csv")
+    posterior.write_variance_pgm(field, n, 10.0, tmp_path / "v.pgm")
+    rows = (tmp_path / "v.csv").read_text().strip().splitlines()
+    assert len(rows) == n + 1 and rows[0] == ",".join(f"c{i}" for i in range(n))
+    back = np.array([[float(x) for x in r.split(",")] for r in rows[1:]])
+    np.testing.assert_array_equal(back.ravel(), field)
+    np.testing.assert_array_equal(posterior.variance_to_grid(field, n), back)
+    pgm = (tmp_path / "v.pgm").read_text().split()
+    assert pgm[:4] == ["P2", str(n), str(n), "255"]
+    pix = np.array(pgm[4:], dtype=int)
+    assert pix.size == n * n and pix.min() == 0 and pix[13] == 0 and pix.max() <= 255
+    posterior.write_variance_pgm(np.full(9, 10.0), 3, 10.0, tmp_path / "flat.pgm")
+    assert all(p == "255" for p in (tmp_path / "flat.pgm").read_text().split()[4:])
