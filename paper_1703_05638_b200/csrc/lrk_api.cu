@@ -652,6 +652,21 @@ int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, 
                                       part, flag, STEP_RTOL * STEP_RTOL, c->num_sms, s);
     if (e == cudaSuccess) {
       ++c->launches;
+      static const bool dbg = std::getenv("LRK_RICH_DEBUG") != nullptr;
+      if (dbg) {   // diagnostics: the relative residual the fixed sweep count reached
+        static int shown = 0;
+        if (shown < 40 || shown % 200 == 0) {
+          std::vector<double> hp(2 * 296);
+          CK(cudaStreamSynchronize(s));
+          CK(cudaMemcpy(hp.data(), part, hp.size() * sizeof(double), cudaMemcpyDeviceToHost));
+          double rr = 0.0, bb = 0.0;
+          const int G = std::min(256, 2 * c->num_sms);
+          for (int k = 0; k < G; ++k) { rr += hp[2 * k]; bb += hp[2 * k + 1]; }
+          std::fprintf(stderr, "[rich] solve %d: %d sweeps, ||r||/||b|| = %.3e\n", shown, c->rich_it,
+                       bb > 0 ? std::sqrt(rr / bb) : 0.0);
+        }
+        ++shown;
+      }
       return LRK_OK;
     }
     if (e != cudaErrorNotSupported) CK(e);
@@ -713,6 +728,7 @@ int rich_setup(lrk_ctx* c, cudaStream_t s) {
     // residual after x0 = P^{-1} b is ~ q ||b||; reach 1e-3 * STEP_RTOL with margin
     const double need = std::log(0.1 * STEP_RTOL) / std::log(std::max(q, 1e-6));
     c->rich_it = std::max(2, std::min(60, (int)std::ceil(need) + 1));
+    if (const char* e = std::getenv("LRK_RICH_IT")) c->rich_it = std::max(1, std::atoi(e));  // diagnostics
   }
   c->rich_q = q;
   if (std::getenv("LRK_DEBUG")) {
