@@ -2,7 +2,7 @@
 # Per-phase cycle breakdown of the sweep kernel (CTA 0, thread 0) on the C2
 # bench workload.  Usage (GPU box): bash tools/phase_cycles.sh
 mkdir -p gpurun_out
-LRK_DEBUG=1 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_dbg.json 2> gpurun_out/bench_dbg.err
+LRK_DEBUG=1 python bench.py --config C2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_dbg.json 2> gpurun_out/bench_dbg.err
 echo bench=$?
 python - <<'PY'
 import json, re
