@@ -8,7 +8,6 @@ tighter agreement (1e-10 relative) where the inputs are identical and
 identical rank decisions.
 """
 
-import math
 
 import numpy as np
 import pytest

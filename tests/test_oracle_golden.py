@@ -1,7 +1,6 @@
 """Pin the CPU oracle against the reference's own outputs (tests/golden) and
 the reference's closed-form known answers.  CPU only."""
 
-import math
 
 import numpy as np
 import pytest

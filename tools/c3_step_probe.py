@@ -1,7 +1,6 @@
 """Wall vs device time of the convection-diffusion step solve at C3 size
 (one column, the preconditioned Richardson path): launch-bound or GPU-bound?"""
 import sys, time
-import numpy as np
 import torch
 sys.path.insert(0, ".")
 import paper_1703_05638_b200 as lp

@@ -1,7 +1,7 @@
 """FP64 tensor-pipe reference numbers on this GPU: cuBLAS DGEMM (torch fp64
 matmul) vs our DMMA DST (lrk_step_solve on the heat operator = 4 DST GEMM
 passes + one scaling)."""
-import sys, time
+import sys
 import torch
 sys.path.insert(0, ".")
 import paper_1703_05638_b200 as lp
