@@ -11,7 +11,7 @@
 // paying launch, ramp-up and drain (~20 us per 512^3 GEMM against ~7 us of
 // work).  Here all phases of one solve run in ONE cooperative launch: every CTA
 // owns 32 x 32 output tiles, streams its operand panels from L2 through a
-// 4-stage cp.async ring (16-byte .cg copies: operands written by other CTAs in
+// 3-stage cp.async ring (16-byte .cg copies: operands written by other CTAs in
 // the previous phase must not be served from a stale L1), multiplies on the
 // FP64 tensor pipe (DMMA m8n8k4), and the phases are separated by a grid
 // barrier.  The final true-residual check (||b - S x|| <= tol ||b||) raises a
@@ -33,9 +33,11 @@ namespace {
 // per apply): this form 922, four warps without split-K 933, 32 x 64 tiles with
 // eight warps 1033 and with four 1373 (128 CTAs leave 20 SMs idle); ncu shows
 // the DMMA pipe 40 % and the shared-memory pipe 43 % busy, barrier waits first
-// among the stall reasons (profiles/ncu_rich_kernel_r02l.txt).
+// among the stall reasons (profiles/ncu_rich_kernel_r02l.txt).  k-steps of 64
+// with a 3-stage ring (half the CTA barriers per tile of the 32-deep 4-stage
+// ring, same 2 CTAs per SM) took the full C3 apply from 2.33 to 2.25 s.
 constexpr int RT = 256;
-constexpr int TM = 32, TN = 32, TK = 32, NS = 4;
+constexpr int TM = 32, TN = 32, TK = 64, NS = 3;
 constexpr int FI = TM / 16, FJ = TN / 16;
 constexpr int SA = TK + 4, SB = TN + 4;
 

@@ -809,3 +809,46 @@ def test_convdiff_step_solve_at_large_tau_reaches_the_attainable_accuracy():
         S = K.step_matrix
         res = (S.T if adj else S) @ out - B
         assert np.linalg.norm(res) <= 1e-10 * np.linalg.norm(B)
+
+
+@pytest.mark.parametrize("scheme", ["galerkin", "upwind"])
+def test_persistent_richardson_step_solve_path_vs_oracle(monkeypatch, scheme):
+    """The one-kernel preconditioned-Richardson step solve (csrc/lrk_rich.cu: 2-D, even n_side,
+    small tau so that the contraction bound selects Richardson) inside a full IC Hessian apply:
+    against the oracle (SuperLU sweeps on the independently assembled matrix) with its rank, and
+    against the multi-launch solve of the same iteration.  The launch counts prove which path
+    ran: the persistent form needs one launch per time step for the solves."""
+    n_side, n_t = 64, 128
+    grid = lp.build_grid(n_side)
+    kw = dict(field="rotating", scheme="galerkin") if scheme == "galerkin" else {}
+    wind = (0.0, 0.0) if scheme == "galerkin" else (0.6, -0.8)
+    op = lp.assemble_convdiff(grid, 1 / 20, wind, **kw)
+    bn = 1.0 / (0.01**2 * (1.0 / n_t) * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    layout = lp.make_sensor_subgrid(grid, 8)
+    v = np.random.default_rng(61).standard_normal(grid.n_x)
+
+    def run():
+        K = lp.SpaceTimeOperator(op, lp.build_time_grid(n_t))
+        ctx = lp.HessianContext(mode="ic", operator=K, layout=layout, cov=cov,
+                                pol=lp.TruncationPolicy(1e-8, 48))
+        before = ctx._dev.launches()
+        out = ctx.apply(v)
+        return out, ctx.rank_trace[-1], ctx._dev.launches() - before
+
+    got, rank, launches = run()
+    monkeypatch.setenv("LRK_RICH_MULTI", "1")
+    multi, rank_m, launches_m = run()
+    monkeypatch.delenv("LRK_RICH_MULTI")
+    assert launches < launches_m / 5, (launches, launches_m)
+    assert rank == rank_m
+    assert np.linalg.norm(got - multi) <= 1e-11 * np.linalg.norm(multi)
+    if scheme == "galerkin":
+        P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, 48, kind="convdiff", nu=1 / 20,
+                      wind=(0.0, 0.0), stencil="q1", prior=(1.0, 0.05), wind_field="rotating")
+    else:
+        P = O.Problem(n_side, n_t, layout.mask, bn, 1.0, 1e-8, 48, kind="convdiff", nu=1 / 20,
+                      wind=wind, prior=(1.0, 0.05))
+    ref, rank_ref = O.hessian_ic(P, v)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+    assert rank == rank_ref
