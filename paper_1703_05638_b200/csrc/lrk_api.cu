@@ -662,8 +662,8 @@ int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, 
           double rr = 0.0, bb = 0.0;
           const int G = std::min(256, 2 * c->num_sms);
           for (int k = 0; k < G; ++k) { rr += hp[2 * k]; bb += hp[2 * k + 1]; }
-          std::fprintf(stderr, "[rich] solve %d: %d sweeps, ||r||/||b|| = %.3e\n", shown, c->rich_it,
-                       bb > 0 ? std::sqrt(rr / bb) : 0.0);
+          std::fprintf(stderr, "[rich] solve %d: %d of at most %d sweeps, ||r||/||b|| = %.3e\n", shown,
+                       (int)hp[2 * G], c->rich_it, bb > 0 ? std::sqrt(rr / bb) : 0.0);
         }
         ++shown;
       }

@@ -231,21 +231,30 @@ __global__ void __launch_bounds__(RT) rich_kernel(const RichArgs a) {
     bb_tot = stot[1];
   };
   // The sweep bound comes from the contraction measured once per operator; the loop leaves
-  // as soon as the true residual is below exit2 (a tenth of the step tolerance), which at
-  // C3 is 12-13 of the 16 sweeps the bound allows.  part[] is rewritten only after the four
+  // as soon as the true residual is below exit2 (a tenth of the step tolerance) or has
+  // stopped contracting below the tolerance, which at C3 is 12-13 of the 16 sweeps the bound allows.  part[] is rewritten only after the four
   // GEMM phases (and their barriers) of the next sweep, i.e. after every CTA has read it.
   precond(a.b, 0.0);
   double rr = 0.0, bb = 0.0;
   bool done = false;
-  for (int it = 0; it < a.sweeps; ++it) {
+  int it = 0;
+  double rr_prev = 0.0;
+  for (; it < a.sweeps; ++it) {
     residual(rr, bb);
-    if (rr <= a.exit2 * bb) { done = true; break; }
+    // below a tenth of the tolerance, or below the tolerance and no longer contracting (the
+    // attainable residual eps * cond(S) can sit between the two: n_t 256 at C3's grid)
+    if (rr <= a.exit2 * bb || (it > 0 && rr <= a.tol2 * bb && rr > 0.49 * rr_prev)) {
+      done = true;
+      break;
+    }
+    rr_prev = rr;
     precond(a.r, 1.0);
   }
   if (!done) {
     residual(rr, bb);
     if (blockIdx.x == 0 && threadIdx.x == 0 && rr > a.tol2 * bb) *a.flag = 1;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.part[2 * G] = (double)it;   // sweeps used (diagnostics)
 }
 
 size_t rich_smem_bytes() { return (size_t)NS * (TM * SA + TK * SB) * sizeof(double); }
