@@ -339,7 +339,7 @@ def make_context(cfg, lp):
 
 
 # FP64 tensor-pipe ceiling of this pool's B200s: cuBLAS DGEMM 8192^3, measured with
-# tools/dgemm_peak.py (profiles/dgemm_peak_r02l.txt; 4096^3 gives 35.3).  MEASURED_PEAKS.json
+# tools/dgemm_peak.py (profiles/dgemm_peak_r02o.txt; 4096^3 gives 35.3).  MEASURED_PEAKS.json
 # carries no FP64 figure, so this is our own measurement.
 FP64_DGEMM_PEAK_TFLOPS = 35.5
 
