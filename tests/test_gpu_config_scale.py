@@ -366,3 +366,45 @@ def test_streaming_sweep_is_bitwise_reproducible(shards):
     v = np.random.default_rng(5).standard_normal(grid.n_x)
     outs = [ctx.apply(v) for _ in range(3)]
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("form", ["0", "1"], ids=["persistent", "streaming"])
+@pytest.mark.parametrize("n_side,dim,n_t,r_max,sensors", [
+    (5, 2, 1, None, "full"),      # a single time step: one ragged flush of one column
+    (7, 2, 3, None, "full"),      # fewer steps than one flush
+    (11, 2, 6, 1, "sub"),         # n_x = 121 (cuts the 8-row tiles), rank cap 1
+    (9, 2, 10, 3, "none"),        # no sensors: the observation field is zero
+    (5, 3, 7, None, "sub"),       # 3-D, n_x = 125, ragged last flush
+    (6, 3, 9, 2, "full"),         # 3-D, n_x = 216, tight cap
+])
+def test_sweep_forms_on_ragged_and_degenerate_shapes_vs_oracle(monkeypatch, form, n_side, dim, n_t,
+                                                               r_max, sensors):
+    """Edge shapes through both sweep forms (rows resident / streaming flushes) against the
+    oracle: ragged flushes (n_t not a multiple of compress_every), row counts that cut the
+    8-row tiles, rank caps of 1-3, an empty sensor set, and the zero vector."""
+    monkeypatch.setenv("LRK_SFLUSH", form)
+    grid = lp.build_grid(n_side, dim)
+    K = lp.SpaceTimeOperator(lp.assemble_heat(grid), lp.build_time_grid(n_t))
+    rng = np.random.default_rng(1000 + 37 * n_side + n_t)
+    if sensors == "full":
+        mask = np.ones(grid.n_x, dtype=bool)
+    elif sensors == "none":
+        mask = np.zeros(grid.n_x, dtype=bool)
+    else:
+        mask = rng.random(grid.n_x) < 0.3
+    bn = 1.0 / (0.02**2 * K.time.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0)
+    ctx = lp.HessianContext(mode="ic", operator=K, layout=lp.SensorLayout((), mask), cov=cov,
+                            pol=lp.TruncationPolicy(1e-8, r_max))
+    P = O.Problem(n_side, n_t, mask, bn, 1.0, 1e-8, r_max, dim=dim)
+    assert np.count_nonzero(ctx.apply(np.zeros(grid.n_x))) == 0
+    for _ in range(2):
+        v = rng.standard_normal(grid.n_x)
+        ref, rank = O.hessian_ic(P, v)
+        got = ctx.apply(v)
+        scale = np.linalg.norm(ref)
+        if scale == 0.0:
+            assert np.count_nonzero(got) == 0
+        else:
+            assert np.linalg.norm(got - ref) <= 1e-9 * scale
+        assert ctx.rank_trace[-1] == rank
