@@ -639,7 +639,7 @@ constexpr double STEP_RTOL = 1e-13;
 int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, cudaStream_t s) {
   const int64_t nx = c->n_x;
   WS(double, r, "rs_r", nx);
-  WS(double, part, "rs_part", 2 * 296);
+  WS(double, part, "rs_part", RICH_PART_LEN);
   WS(unsigned, cnt, "rs_cnt", 1);
   StencilArgs a = make_stencil(c->op, adjoint);
   // one persistent kernel per solve where it applies (2-D, even n): every phase of
@@ -656,20 +656,21 @@ int rich_solve(lrk_ctx* c, const double* b, double* x, bool adjoint, int* flag, 
       if (dbg) {   // diagnostics: the relative residual the fixed sweep count reached
         static int shown = 0;
         if (shown < 40 || shown % 200 == 0) {
-          std::vector<double> hp(2 * 296);
+          double hp[3];
           CK(cudaStreamSynchronize(s));
-          CK(cudaMemcpy(hp.data(), part, hp.size() * sizeof(double), cudaMemcpyDeviceToHost));
-          double rr = 0.0, bb = 0.0;
-          const int G = std::min(256, 2 * c->num_sms);
-          for (int k = 0; k < G; ++k) { rr += hp[2 * k]; bb += hp[2 * k + 1]; }
+          CK(cudaMemcpy(hp, part + RICH_PART_DIAG, sizeof(hp), cudaMemcpyDeviceToHost));
           std::fprintf(stderr, "[rich] solve %d: %d of at most %d sweeps, ||r||/||b|| = %.3e\n", shown,
-                       (int)hp[2 * G], c->rich_it, bb > 0 ? std::sqrt(rr / bb) : 0.0);
+                       (int)hp[0], c->rich_it, hp[2] > 0 ? std::sqrt(hp[1] / hp[2]) : 0.0);
         }
         ++shown;
       }
       return LRK_OK;
     }
-    if (e != cudaErrorNotSupported) CK(e);
+    // outside the kernel's scope, or the grid cannot be co-resident here (another context on
+    // the device): take the multi-launch path; anything else is an error
+    if (e != cudaErrorNotSupported && e != cudaErrorCooperativeLaunchTooLarge &&
+        e != cudaErrorLaunchOutOfResources)
+      CK(e);
     cudaGetLastError();
   }
   TRY(precond_apply(c, b, x, s));

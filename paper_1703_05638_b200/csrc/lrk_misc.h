@@ -38,6 +38,10 @@ __global__ void stencil_kernel(StencilArgs a);
 // x0 = P^{-1} b and `sweeps` corrections in one cooperative launch, then the
 // true-residual check (flag raised when ||b - S x||^2 > tol2 ||b||^2).
 // cudaErrorNotSupported: shape outside its scope (3-D, odd n, per-node upwind).
+// part[] of launch_rich: two doubles per CTA (at most 2 CTAs on each of up to 148 SMs), then the
+// diagnostics triple {sweeps used, ||r||^2, ||b||^2}
+constexpr int RICH_PART_DIAG = 2 * 296;
+constexpr int RICH_PART_LEN = RICH_PART_DIAG + 4;
 cudaError_t launch_rich(const StencilArgs& st, int n, int sweeps, const double* S1, const double* D,
                         const double* b, double* x, double* r, double* T1, double* T2, unsigned* bar,
                         double* part, int* flag, double tol2, int num_sms, cudaStream_t s);

@@ -254,7 +254,11 @@ __global__ void __launch_bounds__(RT) rich_kernel(const RichArgs a) {
     residual(rr, bb);
     if (blockIdx.x == 0 && threadIdx.x == 0 && rr > a.tol2 * bb) *a.flag = 1;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.part[2 * G] = (double)it;   // sweeps used (diagnostics)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // diagnostics (LRK_RICH_DEBUG): past the CTA partials
+    a.part[RICH_PART_DIAG] = (double)it;
+    a.part[RICH_PART_DIAG + 1] = rr;
+    a.part[RICH_PART_DIAG + 2] = bb;
+  }
 }
 
 size_t rich_smem_bytes() { return (size_t)NS * (TM * SA + TK * SB) * sizeof(double); }
@@ -283,7 +287,7 @@ cudaError_t launch_rich(const StencilArgs& st, int n, int sweeps, const double* 
   a.n = n; a.sweeps = sweeps; a.ntm = (n + TM - 1) / TM; a.ntn = (n + TN - 1) / TN;
   a.S1 = S1; a.D = D; a.b = b; a.x = x; a.r = r; a.T1 = T1; a.T2 = T2;
   a.bar = bar; a.part = part; a.flag = flag; a.tol2 = tol2; a.exit2 = 0.01 * tol2;
-  const int G = std::min(a.ntm * a.ntn, std::min(max_ctas[dev], 2 * num_sms));
+  const int G = std::min(std::min(a.ntm * a.ntn, RICH_PART_DIAG / 2), std::min(max_ctas[dev], 2 * num_sms));
   void* params[] = {(void*)&a};
   return cudaLaunchCooperativeKernel((const void*)rich_kernel, dim3(G), dim3(RT), params,
                                      rich_smem_bytes(), s);

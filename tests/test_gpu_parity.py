@@ -852,3 +852,31 @@ def test_persistent_richardson_step_solve_path_vs_oracle(monkeypatch, scheme):
     ref, rank_ref = O.hessian_ic(P, v)
     assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
     assert rank == rank_ref
+
+
+def test_persistent_richardson_more_tiles_than_ctas(monkeypatch):
+    """n_side 640: 400 output tiles for at most 296 co-resident CTAs, so CTAs loop over tiles
+    and the partial table is full — the persistent solve against the multi-launch solve of
+    the same iteration on a short horizon (tau = 1/2048 keeps the Richardson contraction)."""
+    n_side, n_t = 640, 8
+    grid = lp.build_grid(n_side)
+    op = lp.assemble_convdiff(grid, 1 / 20, (0.0, 0.0), field="rotating", scheme="galerkin")
+    layout = lp.make_sensor_subgrid(grid, 16)
+    tg = lp.build_time_grid(n_t, T=n_t / 2048)
+    bn = 1.0 / (0.01**2 * tg.tau * grid.m_scale)
+    cov = lp.CovarianceSpec(bn, 1.0, 1.0, prior_delta=1.0, prior_gamma=0.05)
+    v = np.random.default_rng(71).standard_normal(grid.n_x)
+
+    def run():
+        ctx = lp.HessianContext(mode="ic", operator=lp.SpaceTimeOperator(op, tg), layout=layout,
+                                cov=cov, pol=lp.TruncationPolicy(1e-8, 48))
+        before = ctx._dev.launches()
+        out = ctx.apply(v)
+        return out, ctx.rank_trace[-1], ctx._dev.launches() - before
+
+    got, rank, launches = run()
+    monkeypatch.setenv("LRK_RICH_MULTI", "1")
+    multi, rank_m, launches_m = run()
+    assert launches < launches_m / 5, (launches, launches_m)
+    assert rank == rank_m
+    assert np.linalg.norm(got - multi) <= 1e-11 * np.linalg.norm(multi)
