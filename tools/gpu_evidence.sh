@@ -22,7 +22,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 7000 --csv --log-fi
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/${TAG}_traffic_c4_apply.csv python tools/c4_probe.py 128 2048 1 > $O/${TAG}_ncu_traffic.log 2>&1
 python -c "import bench; print(bench.build_hash())" > $O/${TAG}_build_hash.txt
-# full captures of pass A / pass B late in the forward sweep at full size (rank ~27)
+# full captures of pass A / pass B late in the forward sweep at full size (rank 18)
 ncu --set full --clock-control none --import-source on -k regex:sf_pass --launch-skip 900 --launch-count 2 \
   -f -o $O/${TAG}_ncu_sf_pass python tools/c4_probe.py 128 2048 1 > $O/${TAG}_ncu_sf_pass.log 2>&1
 # which counters see the FP64 tensor pipe
